@@ -1,0 +1,246 @@
+/*
+ * librl — B200-native fused LM-head + IcePop policy-loss step (C ABI).
+ *
+ * The operation is the per-token policy-gradient loss of PAPER.md §3.3
+ * (arXiv 2512.16144, INTELLECT-3), lines 449-472:
+ *
+ *   Eq.1 (L451-463)  J = 1/sum_i|y_i| * sum_i sum_t M(pi_train(y_it)/pi_infer(y_it); a, b) * A_it
+ *   Eq.2 (L465-468)  M(k) = k if k in [a, b] else 0          (a = 0.5, b = 5 by default)
+ *   L470             A_it = S_i - mean_G(S)                   (no std division)
+ *   L472             a rollout is masked if any of its token ratios < 1e-5
+ *
+ * where log pi_train(y_t) is the log-softmax, at the sampled token, of the LM
+ * head logits z_t = invT * W_vocab h_t over the full vocabulary. The library
+ * minimises loss = -J and returns d loss / d hidden and d loss / d W_vocab.
+ * The readings of every point the paper leaves open are listed in DESIGN.md §2
+ * (R1-R15) and cited below as "R<n>".
+ *
+ * Conventions for every call:
+ *  - Pointers are DEVICE pointers unless the argument says HOST. The caller
+ *    owns and allocates every buffer, including the workspace; the library
+ *    never allocates device memory, never frees, and never synchronises the
+ *    device (the *_hostio call is the one exception: it waits on `stream`).
+ *  - bf16 tensors are passed as uint16_t bit patterns. All matrices are
+ *    row-major and contiguous along the hidden dimension: hidden [T, H],
+ *    W_vocab [V_local, H] (the nn.Linear layout, no transpose), d_hidden [T, H],
+ *    d_w_vocab [V_local, H].
+ *  - Work is enqueued on `stream` (a cudaStream_t; NULL = legacy default stream).
+ *  - Host-checkable errors (null pointers, bad sizes, misaligned pointers,
+ *    bad parameters, short workspace, a device that is not sm_100) return a
+ *    status synchronously with a message from rl_last_error_message(), and
+ *    enqueue nothing. Data-dependent problems (non-finite or positive stored
+ *    log-probs, targets outside [0, V_global), malformed rollout offsets) are
+ *    counted in rl_loss_report and neutralised on the device (R-faults in
+ *    DESIGN.md §4): the token is excluded, or, for bad offsets, the whole batch
+ *    gets coef = 0.
+ *  - Every 16-byte-vectorised pointer (hidden, W_vocab, d_hidden, d_w_vocab,
+ *    workspace) must be 16-byte aligned; H must be a multiple of 8.
+ */
+#ifndef RL_H_
+#define RL_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RL_ABI_VERSION 1
+
+typedef enum rl_status {
+  RL_OK = 0,
+  RL_ERR_INVALID_ARGUMENT = 1, /* null pointer, bad parameter value           */
+  RL_ERR_SHAPE = 2,            /* size out of range or inconsistent          */
+  RL_ERR_UNSUPPORTED = 3,      /* device is not sm_100, or feature not built  */
+  RL_ERR_CUDA = 4,             /* a CUDA runtime/driver call failed          */
+  RL_ERR_WORKSPACE = 5,        /* workspace null or smaller than required    */
+  RL_ERR_ALIGNMENT = 6         /* pointer not 16-byte aligned                */
+} rl_status;
+
+/* Shape of the LM-head contraction on this rank. */
+typedef struct rl_lm_shape {
+  int64_t T;               /* packed token rows (>= 0)                              */
+  int64_t H;               /* hidden size (multiple of 8, <= 65536)                  */
+  int64_t V_local;         /* rows of W_vocab on this rank (>= 1)                    */
+  int64_t vocab_offset;    /* global id of W_vocab row 0 (vocab-parallel shard start) */
+  int64_t V_global;        /* full vocabulary size (>= vocab_offset + V_local)       */
+  float inv_temperature;   /* 1/tau applied to the logits, > 0 (R8; default 1)       */
+  int32_t _pad;
+} rl_lm_shape;
+
+/* Loss hyper-parameters. */
+typedef struct rl_loss_params {
+  float alpha;             /* Eq.2 lower bound, 0 < alpha <= 1                        */
+  float beta;              /* Eq.2 upper bound, beta >= 1 (closed interval, R4)       */
+  float guard_threshold;   /* rollout masked iff min_t k_t < guard (strict, R4); 0 off */
+  int32_t num_rollouts;    /* R = number of packed rollouts on this rank (>= 1)       */
+  double loss_denominator; /* D = sum_i |y_i| over the GLOBAL step batch, > 0 (R5)     */
+} rl_loss_params;
+
+/* Device-resident loss report (SPEC LossReport + counters). Written, not
+ * accumulated, by every call that takes it. Sums use a fixed-order reduction,
+ * so two identical calls give bit-identical reports. */
+typedef struct rl_loss_report {
+  double loss;               /* -J contribution of this rank: -(1/D) sum_t coef_t*D (R3) */
+  double mismatch_kl_sum;    /* sum over valid tokens of k - log k - 1                  */
+  uint32_t kept_tokens;      /* tokens with keep = 1                                    */
+  uint32_t masked_low;       /* valid tokens with k < alpha                             */
+  uint32_t masked_high;      /* valid tokens with k > beta                              */
+  uint32_t guarded_rollouts; /* rollouts with min k < guard                             */
+  uint32_t guarded_tokens;   /* valid tokens inside guarded rollouts                    */
+  uint32_t nonfinite_inputs; /* loss tokens whose stored log-prob is NaN/inf or > 0     */
+  uint32_t bad_targets;      /* loss tokens whose target is outside [0, V_global)       */
+  uint32_t bad_offsets;      /* 1 if rollout_offsets is not 0 = o_0 <= ... <= o_R = T  */
+} rl_loss_report;
+
+/* Outputs of rl_policy_loss_fwd_bwd. Optional pointers may be NULL. */
+typedef struct rl_loss_outputs {
+  rl_loss_report* report;  /* [1] device, required                                     */
+  float* logprob;          /* [T] log pi_train(y_t), required                          */
+  float* entropy;          /* [T] entropy of the scaled distribution (R9), optional    */
+  float* lse;              /* [T] log-sum-exp of the scaled logits, optional           */
+  float* coef;             /* [T] keep_t k_t A_i / D (d loss / d logp_t = -coef_t), opt */
+  uint8_t* token_keep;     /* [T] 1 if the token contributes, optional                 */
+  uint8_t* rollout_guarded;/* [R] 1 if the rollout was masked by the guard, optional   */
+  uint16_t* d_hidden;      /* [T, H] bf16 d loss / d hidden; or NULL                    */
+  float* d_hidden_f32;     /* [T, H] fp32 alternative (vocab-parallel partial); or NULL */
+  float* d_w_vocab;        /* [V_local, H] fp32 d loss / d W_vocab; or NULL             */
+  int32_t accumulate_dw;   /* 0: d_w_vocab is overwritten; 1: the gradient is added     */
+  int32_t _pad;
+} rl_loss_outputs;
+
+/* ---------------------------------------------------------------- S0 */
+/* A[g*G + j] = rewards[g*G + j] - mean_j rewards[g*G + j].
+ * rewards, advantages: [num_groups * group_size] fp32, group-major.
+ * group_size < 2 -> RL_ERR_INVALID_ARGUMENT (no baseline). */
+rl_status rl_group_advantages(const float* rewards, int32_t num_groups, int32_t group_size,
+                              float* advantages, void* stream);
+
+/* ------------------------------------------------------------- S1 + S2 */
+/* logprob[t] = z_t[y_t] - lse_t,  entropy[t] = -sum_v p_tv log p_tv,  lse[t],
+ * with z_t = invT * W h_t over the full vocabulary (Eq.1's pi_train). The
+ * logits exist only in tensor memory; nothing T x V touches HBM.
+ * Requires V_local == V_global (single shard); vocab-parallel callers use
+ * rl_fwd_partials + rl_merge_partials. entropy and lse may be NULL. */
+rl_status rl_logprob_fwd(const rl_lm_shape* shape, const uint16_t* hidden,
+                         const uint16_t* w_vocab, const int32_t* targets, float* logprob,
+                         float* entropy, float* lse, void* workspace, size_t workspace_bytes,
+                         void* stream);
+
+/* ----------------------------------------------------------- S0 .. S6 */
+/* The whole step for one rank: logits (TMEM only) -> online log-softmax ->
+ * k_t = exp(logprob_t - infer_logprobs_t) -> Eq.2 gate + rollout guard ->
+ * coef_t -> loss, then the backward d loss / d u_tv = coef_t invT (p_tv - [v==y_t])
+ * folded into d_hidden = dU W and d_w_vocab = dU^T hidden.
+ *   targets          [T] int32 global vocab ids (row t is scored on targets[t];
+ *                    shifting labels is the caller's job)
+ *   infer_logprobs   [T] fp32, log pi_infer(y_t) as stored by the inference engine
+ *   rollout_adv      [R] fp32, A_i (from rl_group_advantages)
+ *   rollout_offsets  [R+1] int32 CSR row offsets of the packed rollouts
+ *   loss_mask        [T] uint8 or NULL (= all ones); 0 rows get logprob/entropy
+ *                    but no loss, guard participation or gradient (R4, R5)
+ * Requires V_local == V_global; vocab-parallel callers use the split phases. */
+rl_status rl_policy_loss_fwd_bwd(const rl_lm_shape* shape, const rl_loss_params* params,
+                                 const uint16_t* hidden, const uint16_t* w_vocab,
+                                 const int32_t* targets, const float* infer_logprobs,
+                                 const float* rollout_adv, const int32_t* rollout_offsets,
+                                 const uint8_t* loss_mask, const rl_loss_outputs* out,
+                                 void* workspace, size_t workspace_bytes, void* stream);
+
+/* Same step with the per-step inputs in HOST memory (pinned for async copies):
+ * hidden_host, targets_host, infer_host, rewards_host ([R] fp32, grouped by
+ * group_size), offsets_host, loss_mask_host (or NULL) are copied into the
+ * workspace on `stream`, advantages are computed on the device, the step runs,
+ * and the report is copied back to report_host before returning (the call
+ * synchronises `stream`). W_vocab, d_hidden and d_w_vocab stay on the device
+ * (they are model state). Workspace: rl_workspace_bytes_hostio. */
+rl_status rl_policy_loss_fwd_bwd_hostio(const rl_lm_shape* shape, const rl_loss_params* params,
+                                        int32_t group_size, const uint16_t* hidden_host,
+                                        const uint16_t* w_vocab, const int32_t* targets_host,
+                                        const float* infer_host, const float* rewards_host,
+                                        const int32_t* offsets_host, const uint8_t* loss_mask_host,
+                                        const rl_loss_outputs* out, rl_loss_report* report_host,
+                                        void* workspace, size_t workspace_bytes, void* stream);
+
+/* ------------------------------------------- split phases (vocab-parallel) */
+/* S1 on the local shard, reduced to ONE partial per row:
+ * partials[t] = (m_t, s_t, u_t, zt_t) with, over the shard's scaled logits,
+ * m = max z, s = sum e^{z-m}, u = sum e^{z-m}(z-m), zt = z_{y_t} if y_t is in
+ * [vocab_offset, vocab_offset + V_local) else -inf.  partials: [T] float4 (16 B/row). */
+rl_status rl_fwd_partials(const rl_lm_shape* shape, const uint16_t* hidden,
+                          const uint16_t* w_vocab, const int32_t* targets, float* partials,
+                          void* workspace, size_t workspace_bytes, void* stream);
+
+/* S2: merge n_parts partial arrays ([n_parts, T] float4, e.g. all-gathered from
+ * every vocab shard, merged in index order) into logprob, entropy, lse ([T]). */
+rl_status rl_merge_partials(const float* partials, int32_t n_parts, int64_t T, float* logprob,
+                            float* entropy, float* lse, void* stream);
+
+/* S3: Eq.1/Eq.2/guard from logprob. Writes coef [T] (required), token_keep,
+ * rollout_guarded (optional) and the report. targets/V_global only feed the
+ * bad-target counter (targets may be NULL to skip it). */
+rl_status rl_loss_coef(const rl_loss_params* params, int64_t T, int64_t V_global,
+                       const float* logprob, const float* infer_logprobs, const int32_t* targets,
+                       const float* rollout_adv, const int32_t* rollout_offsets,
+                       const uint8_t* loss_mask, float* coef, uint8_t* token_keep,
+                       uint8_t* rollout_guarded, rl_loss_report* report, void* workspace,
+                       size_t workspace_bytes, void* stream);
+
+/* S4-S6 on the local shard, given lse and coef for every row:
+ * dU = coef invT (softmax - onehot) recomputed chunk by chunk (dz_chunk_rows
+ * rows at a time, 0 = all T), d_hidden(_f32) = dU W_shard (a partial sum over
+ * the shard when vocab-parallel), d_w_vocab (+)= dU^T hidden. */
+rl_status rl_bwd(const rl_lm_shape* shape, const uint16_t* hidden, const uint16_t* w_vocab,
+                 const int32_t* targets, const float* lse, const float* coef, uint16_t* d_hidden,
+                 float* d_hidden_f32, float* d_w_vocab, int32_t accumulate_dw,
+                 int64_t dz_chunk_rows, void* workspace, size_t workspace_bytes, void* stream);
+
+/* ------------------------------------------------------------ utilities */
+/* Workspace needed by rl_logprob_fwd / rl_policy_loss_fwd_bwd / the split
+ * phases for this shape. dz_chunk_rows = rows of the bf16 dU buffer (0 = T). */
+size_t rl_workspace_bytes(const rl_lm_shape* shape, int32_t num_rollouts, int64_t dz_chunk_rows);
+size_t rl_workspace_bytes_hostio(const rl_lm_shape* shape, int32_t num_rollouts);
+
+/* Default dU chunk rows used when dz_chunk_rows == 0 (currently T). */
+int64_t rl_default_dz_chunk_rows(const rl_lm_shape* shape);
+
+const char* rl_status_string(rl_status s);
+const char* rl_last_error_message(void); /* thread-local, last failing call */
+int32_t rl_abi_version(void);
+
+/* Number of kernels the last successful call on this thread enqueued
+ * (reported as gpu_launches by bench.py). */
+int32_t rl_last_launch_count(void);
+
+/* ------------------------------------------------- kernel timing (bench) */
+/* When enabled (per host thread), every kernel that later calls enqueue is
+ * bracketed by two CUDA events recorded on the call's stream. rl_profile_read
+ * waits for the recorded events, writes up to `cap` entries (kernel id +
+ * milliseconds, in launch order), clears the record and returns how many
+ * launches were recorded (which may exceed cap). Timing adds two event records
+ * per launch and nothing else; it is off by default. */
+typedef enum rl_kernel_id {
+  RL_K_GROUP_ADV = 0,  /* K0 S0                                  */
+  RL_K_FWD_GEMM = 1,   /* K1 S1+S2 tile partials (tcgen05)       */
+  RL_K_MERGE = 2,      /* K2 S2 merge                            */
+  RL_K_LOSS = 3,       /* K3 S3 per-rollout coef + counters      */
+  RL_K_FINALIZE = 4,   /* K3b report reduction                   */
+  RL_K_DZ_GEMM = 5,    /* K4 S4 recompute + dU (tcgen05)         */
+  RL_K_DH_GEMM = 6,    /* K5 S5 dH = dU W (tcgen05)              */
+  RL_K_DW_GEMM = 7,    /* K6 S6 dW (+)= dU^T h (tcgen05)         */
+  RL_K_MEMSET = 8      /* zero fill of an empty batch's dW       */
+} rl_kernel_id;
+
+typedef struct rl_kernel_time {
+  int32_t kernel; /* rl_kernel_id */
+  float ms;
+} rl_kernel_time;
+
+rl_status rl_profile_enable(int32_t enable);
+int32_t rl_profile_read(rl_kernel_time* out, int32_t cap);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RL_H_ */

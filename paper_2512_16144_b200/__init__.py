@@ -1,0 +1,301 @@
+"""Python binding of librl (include/rl.h): argument marshalling only.
+
+Every function keeps the C name and forwards torch tensors' device pointers and
+the current CUDA stream to the C ABI; every step of the path runs in librl's
+sm_100a kernels. There is no CPU or PyTorch fallback: importing works without a
+GPU (so the ABI can be inspected), but every compute call needs the built
+librl.so and a B200, and raises RLError otherwise.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "librl.so")
+
+RL_OK = 0
+STATUS_NAMES = {0: "RL_OK", 1: "RL_ERR_INVALID_ARGUMENT", 2: "RL_ERR_SHAPE", 3: "RL_ERR_UNSUPPORTED",
+                4: "RL_ERR_CUDA", 5: "RL_ERR_WORKSPACE", 6: "RL_ERR_ALIGNMENT"}
+
+# paper constants
+ALPHA, BETA, GUARD = 0.5, 5.0, 1e-5
+
+
+class RLError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS_NAMES.get(status, status)}: {msg}")
+        self.status = status
+
+
+class rl_lm_shape(ctypes.Structure):
+    _fields_ = [("T", ctypes.c_int64), ("H", ctypes.c_int64), ("V_local", ctypes.c_int64),
+                ("vocab_offset", ctypes.c_int64), ("V_global", ctypes.c_int64),
+                ("inv_temperature", ctypes.c_float), ("_pad", ctypes.c_int32)]
+
+
+class rl_loss_params(ctypes.Structure):
+    _fields_ = [("alpha", ctypes.c_float), ("beta", ctypes.c_float), ("guard_threshold", ctypes.c_float),
+                ("num_rollouts", ctypes.c_int32), ("loss_denominator", ctypes.c_double)]
+
+
+class rl_loss_report(ctypes.Structure):
+    _fields_ = [("loss", ctypes.c_double), ("mismatch_kl_sum", ctypes.c_double),
+                ("kept_tokens", ctypes.c_uint32), ("masked_low", ctypes.c_uint32),
+                ("masked_high", ctypes.c_uint32), ("guarded_rollouts", ctypes.c_uint32),
+                ("guarded_tokens", ctypes.c_uint32), ("nonfinite_inputs", ctypes.c_uint32),
+                ("bad_targets", ctypes.c_uint32), ("bad_offsets", ctypes.c_uint32)]
+
+    def as_dict(self) -> dict:
+        return {name: getattr(self, name) for name, _ in self._fields_}
+
+
+class rl_loss_outputs(ctypes.Structure):
+    _fields_ = [("report", ctypes.c_void_p), ("logprob", ctypes.c_void_p), ("entropy", ctypes.c_void_p),
+                ("lse", ctypes.c_void_p), ("coef", ctypes.c_void_p), ("token_keep", ctypes.c_void_p),
+                ("rollout_guarded", ctypes.c_void_p), ("d_hidden", ctypes.c_void_p),
+                ("d_hidden_f32", ctypes.c_void_p), ("d_w_vocab", ctypes.c_void_p),
+                ("accumulate_dw", ctypes.c_int32), ("_pad", ctypes.c_int32)]
+
+
+class rl_kernel_time(ctypes.Structure):
+    _fields_ = [("kernel", ctypes.c_int32), ("ms", ctypes.c_float)]
+
+
+KERNEL_NAMES = {0: "K0_group_adv", 1: "K1_fwd_gemm_lse", 2: "K2_merge", 3: "K3_loss_coef", 4: "K3b_finalize",
+                5: "K4_bwd_dz_gemm", 6: "K5_dh_gemm", 7: "K6_dw_gemm", 8: "memset"}
+
+REPORT_BYTES = ctypes.sizeof(rl_loss_report)
+assert REPORT_BYTES == 48
+
+_P = ctypes.c_void_p
+_SIGS = {
+    "rl_group_advantages": (ctypes.c_int, [_P, ctypes.c_int32, ctypes.c_int32, _P, _P]),
+    "rl_logprob_fwd": (ctypes.c_int, [ctypes.POINTER(rl_lm_shape), _P, _P, _P, _P, _P, _P, _P, ctypes.c_size_t, _P]),
+    "rl_policy_loss_fwd_bwd": (ctypes.c_int, [ctypes.POINTER(rl_lm_shape), ctypes.POINTER(rl_loss_params), _P, _P,
+                                              _P, _P, _P, _P, _P, ctypes.POINTER(rl_loss_outputs), _P,
+                                              ctypes.c_size_t, _P]),
+    "rl_policy_loss_fwd_bwd_hostio": (ctypes.c_int, [ctypes.POINTER(rl_lm_shape), ctypes.POINTER(rl_loss_params),
+                                                     ctypes.c_int32, _P, _P, _P, _P, _P, _P, _P,
+                                                     ctypes.POINTER(rl_loss_outputs),
+                                                     ctypes.POINTER(rl_loss_report), _P, ctypes.c_size_t, _P]),
+    "rl_fwd_partials": (ctypes.c_int, [ctypes.POINTER(rl_lm_shape), _P, _P, _P, _P, _P, ctypes.c_size_t, _P]),
+    "rl_merge_partials": (ctypes.c_int, [_P, ctypes.c_int32, ctypes.c_int64, _P, _P, _P, _P]),
+    "rl_loss_coef": (ctypes.c_int, [ctypes.POINTER(rl_loss_params), ctypes.c_int64, ctypes.c_int64, _P, _P, _P, _P,
+                                    _P, _P, _P, _P, _P, _P, _P, ctypes.c_size_t, _P]),
+    "rl_bwd": (ctypes.c_int, [ctypes.POINTER(rl_lm_shape), _P, _P, _P, _P, _P, _P, _P, _P, ctypes.c_int32,
+                              ctypes.c_int64, _P, ctypes.c_size_t, _P]),
+    "rl_workspace_bytes": (ctypes.c_size_t, [ctypes.POINTER(rl_lm_shape), ctypes.c_int32, ctypes.c_int64]),
+    "rl_workspace_bytes_hostio": (ctypes.c_size_t, [ctypes.POINTER(rl_lm_shape), ctypes.c_int32]),
+    "rl_default_dz_chunk_rows": (ctypes.c_int64, [ctypes.POINTER(rl_lm_shape)]),
+    "rl_status_string": (ctypes.c_char_p, [ctypes.c_int]),
+    "rl_last_error_message": (ctypes.c_char_p, []),
+    "rl_abi_version": (ctypes.c_int32, []),
+    "rl_last_launch_count": (ctypes.c_int32, []),
+    "rl_profile_enable": (ctypes.c_int, [ctypes.c_int32]),
+    "rl_profile_read": (ctypes.c_int32, [_P, ctypes.c_int32]),
+}
+EXPORTED = tuple(_SIGS)
+
+_lib = None
+
+
+def load_library(path: str | None = None) -> ctypes.CDLL:
+    """dlopen librl.so (in-tree). Raises if it has not been built."""
+    global _lib
+    if _lib is not None and path is None:
+        return _lib
+    p = path or LIB_PATH
+    if not os.path.exists(p):
+        raise RLError(3, f"{p} is missing: run `python -c 'import __graft_entry__ as g; g.build()'`")
+    lib = ctypes.CDLL(p)
+    for name, (res, args) in _SIGS.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    if path is None:
+        _lib = lib
+    return lib
+
+
+def _check(status: int):
+    if status != RL_OK:
+        msg = load_library().rl_last_error_message().decode(errors="replace")
+        raise RLError(status, msg)
+
+
+def _ptr(t: torch.Tensor | None):
+    if t is None:
+        return None
+    if not t.is_cuda:
+        raise RLError(1, "expected a CUDA tensor")
+    if not t.is_contiguous():
+        raise RLError(1, "expected a contiguous tensor")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(stream=None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def make_shape(T, H, V_local, vocab_offset=0, V_global=None, inv_temperature=1.0) -> rl_lm_shape:
+    return rl_lm_shape(int(T), int(H), int(V_local), int(vocab_offset),
+                       int(V_local + vocab_offset if V_global is None else V_global), float(inv_temperature), 0)
+
+
+def make_params(num_rollouts, loss_denominator, alpha=ALPHA, beta=BETA, guard_threshold=GUARD) -> rl_loss_params:
+    return rl_loss_params(float(alpha), float(beta), float(guard_threshold), int(num_rollouts),
+                          float(loss_denominator))
+
+
+def _bf16(t: torch.Tensor | None, name: str) -> torch.Tensor | None:
+    if t is not None and t.dtype not in (torch.bfloat16, torch.int16, torch.uint16):
+        raise RLError(1, f"{name} must be bf16")
+    return t
+
+
+# ---------------------------------------------------------------- C names
+def rl_workspace_bytes(shape: rl_lm_shape, num_rollouts: int = 1, dz_chunk_rows: int = 0) -> int:
+    return int(load_library().rl_workspace_bytes(ctypes.byref(shape), int(num_rollouts), int(dz_chunk_rows)))
+
+
+def rl_workspace_bytes_hostio(shape: rl_lm_shape, num_rollouts: int) -> int:
+    return int(load_library().rl_workspace_bytes_hostio(ctypes.byref(shape), int(num_rollouts)))
+
+
+def alloc_workspace(nbytes: int, device=None) -> torch.Tensor:
+    return torch.empty(max(int(nbytes), 16), dtype=torch.uint8, device=device or "cuda")
+
+
+def rl_group_advantages(rewards: torch.Tensor, group_size: int, advantages: torch.Tensor | None = None,
+                        stream=None) -> torch.Tensor:
+    """S0: A = S - mean_G(S). rewards: [Np*G] fp32 group-major."""
+    r = rewards.reshape(-1)
+    if advantages is None:
+        advantages = torch.empty_like(r)
+    if r.numel() % group_size:
+        raise RLError(2, "len(rewards) must be a multiple of group_size")
+    _check(load_library().rl_group_advantages(_ptr(r), r.numel() // group_size, int(group_size),
+                                              _ptr(advantages), _stream(stream)))
+    return advantages
+
+
+def rl_logprob_fwd(shape: rl_lm_shape, hidden, w_vocab, targets, logprob, entropy=None, lse=None,
+                   workspace=None, stream=None):
+    """S1+S2: logprob/entropy/lse of the targets, logits only in TMEM."""
+    ws = workspace if workspace is not None else alloc_workspace(rl_workspace_bytes(shape), hidden.device)
+    _check(load_library().rl_logprob_fwd(ctypes.byref(shape), _ptr(_bf16(hidden, "hidden")),
+                                         _ptr(_bf16(w_vocab, "w_vocab")), _ptr(targets), _ptr(logprob),
+                                         _ptr(entropy), _ptr(lse), _ptr(ws), ws.numel(), _stream(stream)))
+
+
+def _outputs(report, logprob, entropy=None, lse=None, coef=None, token_keep=None, rollout_guarded=None,
+             d_hidden=None, d_hidden_f32=None, d_w_vocab=None, accumulate_dw=False) -> rl_loss_outputs:
+    return rl_loss_outputs(_ptr(report), _ptr(logprob), _ptr(entropy), _ptr(lse), _ptr(coef), _ptr(token_keep),
+                           _ptr(rollout_guarded), _ptr(d_hidden), _ptr(d_hidden_f32), _ptr(d_w_vocab),
+                           1 if accumulate_dw else 0, 0)
+
+
+def rl_policy_loss_fwd_bwd(shape: rl_lm_shape, params: rl_loss_params, hidden, w_vocab, targets, infer_logprobs,
+                           rollout_adv, rollout_offsets, loss_mask=None, *, report, logprob, entropy=None,
+                           lse=None, coef=None, token_keep=None, rollout_guarded=None, d_hidden=None,
+                           d_hidden_f32=None, d_w_vocab=None, accumulate_dw=False, workspace=None, stream=None):
+    """S0..S6 on one rank (see include/rl.h). `report` is a [48] uint8 CUDA tensor."""
+    ws = workspace if workspace is not None else alloc_workspace(
+        rl_workspace_bytes(shape, params.num_rollouts), w_vocab.device)
+    out = _outputs(report, logprob, entropy, lse, coef, token_keep, rollout_guarded, d_hidden, d_hidden_f32,
+                   d_w_vocab, accumulate_dw)
+    _check(load_library().rl_policy_loss_fwd_bwd(
+        ctypes.byref(shape), ctypes.byref(params), _ptr(_bf16(hidden, "hidden")), _ptr(_bf16(w_vocab, "w_vocab")),
+        _ptr(targets), _ptr(infer_logprobs), _ptr(rollout_adv), _ptr(rollout_offsets), _ptr(loss_mask),
+        ctypes.byref(out), _ptr(ws), ws.numel(), _stream(stream)))
+
+
+def rl_policy_loss_fwd_bwd_hostio(shape: rl_lm_shape, params: rl_loss_params, group_size: int, hidden_host,
+                                  w_vocab, targets_host, infer_host, rewards_host, offsets_host,
+                                  loss_mask_host=None, *, report, d_hidden=None, d_hidden_f32=None,
+                                  d_w_vocab=None, accumulate_dw=False, workspace=None,
+                                  stream=None) -> rl_loss_report:
+    """The same step with per-step inputs in (pinned) host tensors; returns the report."""
+    ws = workspace if workspace is not None else alloc_workspace(
+        rl_workspace_bytes_hostio(shape, params.num_rollouts), w_vocab.device)
+
+    def hp(t):
+        if t is None:
+            return None
+        if t.is_cuda or not t.is_contiguous():
+            raise RLError(1, "host inputs must be contiguous CPU tensors")
+        return ctypes.c_void_p(t.data_ptr())
+
+    out = _outputs(report, None, d_hidden=d_hidden, d_hidden_f32=d_hidden_f32, d_w_vocab=d_w_vocab,
+                   accumulate_dw=accumulate_dw)
+    rep = rl_loss_report()
+    _check(load_library().rl_policy_loss_fwd_bwd_hostio(
+        ctypes.byref(shape), ctypes.byref(params), int(group_size), hp(hidden_host), _ptr(w_vocab),
+        hp(targets_host), hp(infer_host), hp(rewards_host), hp(offsets_host), hp(loss_mask_host),
+        ctypes.byref(out), ctypes.byref(rep), _ptr(ws), ws.numel(), _stream(stream)))
+    return rep
+
+
+def rl_fwd_partials(shape: rl_lm_shape, hidden, w_vocab, targets, partials, workspace=None, stream=None):
+    """S1 on a vocab shard -> one (m, s, u, z_target) float4 per row ([T, 4] fp32)."""
+    ws = workspace if workspace is not None else alloc_workspace(rl_workspace_bytes(shape), hidden.device)
+    _check(load_library().rl_fwd_partials(ctypes.byref(shape), _ptr(_bf16(hidden, "hidden")),
+                                          _ptr(_bf16(w_vocab, "w_vocab")), _ptr(targets), _ptr(partials),
+                                          _ptr(ws), ws.numel(), _stream(stream)))
+
+
+def rl_merge_partials(partials, n_parts: int, T: int, logprob, entropy=None, lse=None, stream=None):
+    """S2: merge [n_parts, T, 4] partials (index order) into logprob / entropy / lse."""
+    _check(load_library().rl_merge_partials(_ptr(partials), int(n_parts), int(T), _ptr(logprob), _ptr(entropy),
+                                            _ptr(lse), _stream(stream)))
+
+
+def rl_loss_coef(params: rl_loss_params, T: int, V_global: int, logprob, infer_logprobs, targets, rollout_adv,
+                 rollout_offsets, loss_mask, coef, token_keep=None, rollout_guarded=None, *, report,
+                 workspace=None, stream=None):
+    """S3: Eq.1/Eq.2/guard -> coef, keep, guarded, report."""
+    ws = workspace if workspace is not None else alloc_workspace(48 * max(1, params.num_rollouts), coef.device)
+    _check(load_library().rl_loss_coef(ctypes.byref(params), int(T), int(V_global), _ptr(logprob),
+                                       _ptr(infer_logprobs), _ptr(targets), _ptr(rollout_adv),
+                                       _ptr(rollout_offsets), _ptr(loss_mask), _ptr(coef), _ptr(token_keep),
+                                       _ptr(rollout_guarded), _ptr(report), _ptr(ws), ws.numel(), _stream(stream)))
+
+
+def rl_bwd(shape: rl_lm_shape, hidden, w_vocab, targets, lse, coef, d_hidden=None, d_hidden_f32=None,
+           d_w_vocab=None, accumulate_dw=False, dz_chunk_rows=0, workspace=None, stream=None):
+    """S4-S6 on a vocab shard."""
+    ws = workspace if workspace is not None else alloc_workspace(
+        rl_workspace_bytes(shape, 1, dz_chunk_rows), w_vocab.device)
+    _check(load_library().rl_bwd(ctypes.byref(shape), _ptr(hidden), _ptr(w_vocab), _ptr(targets), _ptr(lse),
+                                 _ptr(coef), _ptr(d_hidden), _ptr(d_hidden_f32), _ptr(d_w_vocab),
+                                 1 if accumulate_dw else 0, int(dz_chunk_rows), _ptr(ws), ws.numel(),
+                                 _stream(stream)))
+
+
+def rl_profile_enable(enable: bool = True):
+    load_library().rl_profile_enable(1 if enable else 0)
+
+
+def rl_profile_read(cap: int = 4096) -> list:
+    """[(kernel_name, ms), ...] for launches recorded since the last read (waits on their events)."""
+    buf = (rl_kernel_time * cap)()
+    n = load_library().rl_profile_read(ctypes.cast(buf, ctypes.c_void_p), cap)
+    return [(KERNEL_NAMES.get(buf[i].kernel, str(buf[i].kernel)), float(buf[i].ms)) for i in range(min(n, cap))]
+
+
+def rl_last_launch_count() -> int:
+    return int(load_library().rl_last_launch_count())
+
+
+def read_report(report: torch.Tensor) -> rl_loss_report:
+    """Copy a device report ([48] uint8) to the host (synchronises)."""
+    b = bytes(report.cpu().numpy().tobytes())
+    return rl_loss_report.from_buffer_copy(b)
+
+
+def new_report(device=None) -> torch.Tensor:
+    return torch.zeros(REPORT_BYTES, dtype=torch.uint8, device=device or "cuda")

@@ -1,0 +1,709 @@
+// librl host side: argument validation, workspace carving, TMA tensor maps and
+// kernel launches behind the C ABI of include/rl.h.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <mutex>
+#include <vector>
+
+#include "../../include/rl.h"
+#include "rl_gemm.cuh"
+#include "rl_small.cuh"
+
+namespace {
+
+thread_local char g_err[512] = "";
+thread_local int g_launches = 0;
+
+// ---------------------------------------------------- optional event timing
+struct ProfRec {
+  int kernel;
+  cudaEvent_t a, b;
+};
+thread_local bool g_prof = false;
+thread_local std::vector<ProfRec> g_prof_recs;
+thread_local std::vector<cudaEvent_t> g_prof_pool;
+
+cudaEvent_t prof_event() {
+  if (!g_prof_pool.empty()) {
+    cudaEvent_t e = g_prof_pool.back();
+    g_prof_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+
+// Brackets one launch with events when timing is enabled.
+struct ProfScope {
+  int kernel;
+  cudaStream_t st;
+  cudaEvent_t a = nullptr;
+  ProfScope(int k, cudaStream_t s) : kernel(k), st(s) {
+    if (g_prof) {
+      a = prof_event();
+      cudaEventRecord(a, st);
+    }
+  }
+  ~ProfScope() {
+    if (a) {
+      cudaEvent_t b = prof_event();
+      cudaEventRecord(b, st);
+      g_prof_recs.push_back({kernel, a, b});
+    }
+  }
+};
+
+rl_status fail(rl_status s, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return s;
+}
+
+#define RL_CUDA(call)                                                                         \
+  do {                                                                                        \
+    cudaError_t e_ = (call);                                                                  \
+    if (e_ != cudaSuccess) return fail(RL_ERR_CUDA, "%s failed: %s", #call, cudaGetErrorString(e_)); \
+  } while (0)
+
+#define RL_CHECK_LAUNCH()                                                                      \
+  do {                                                                                         \
+    cudaError_t e_ = cudaGetLastError();                                                       \
+    if (e_ != cudaSuccess) return fail(RL_ERR_CUDA, "kernel launch failed: %s", cudaGetErrorString(e_)); \
+    ++g_launches;                                                                              \
+  } while (0)
+
+// ------------------------------------------------------------- device info
+struct DevInfo {
+  int sms = 0;
+  bool ok = false;
+};
+
+rl_status device_info(DevInfo& d) {
+  int dev = 0;
+  RL_CUDA(cudaGetDevice(&dev));
+  static std::mutex mu;
+  static DevInfo cache[64];
+  static bool have[64] = {};
+  std::lock_guard<std::mutex> lk(mu);
+  if (dev < 0 || dev >= 64) return fail(RL_ERR_UNSUPPORTED, "device index %d out of range", dev);
+  if (!have[dev]) {
+    int major = 0, minor = 0, sms = 0;
+    RL_CUDA(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev));
+    RL_CUDA(cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev));
+    RL_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    cache[dev].sms = sms;
+    cache[dev].ok = (major == 10 && minor == 0);
+    have[dev] = true;
+  }
+  d = cache[dev];
+  if (!d.ok) return fail(RL_ERR_UNSUPPORTED, "librl is built for sm_100a (B200); device %d is not compute 10.0", dev);
+  return RL_OK;
+}
+
+// ------------------------------------------------------------ tensor maps
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+rl_status get_encode(EncodeTiledFn& fn) {
+  static EncodeTiledFn cached = nullptr;
+  static std::once_flag once;
+  static cudaError_t err = cudaSuccess;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    err = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q);
+    if (err == cudaSuccess && q == cudaDriverEntryPointSuccess) cached = reinterpret_cast<EncodeTiledFn>(p);
+  });
+  if (!cached) return fail(RL_ERR_CUDA, "cuTensorMapEncodeTiled unavailable (%s)", cudaGetErrorString(err));
+  fn = cached;
+  return RL_OK;
+}
+
+// 2-D row-major tensor [outer][inner], 128-byte swizzle, zero fill out of bounds.
+rl_status make_map(CUtensorMap* m, const void* ptr, bool f32, int64_t inner, int64_t outer, int64_t row_elems,
+                   int box_inner, int box_outer) {
+  EncodeTiledFn enc;
+  rl_status s = get_encode(enc);
+  if (s != RL_OK) return s;
+  const int esz = f32 ? 4 : 2;
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(inner), static_cast<cuuint64_t>(outer > 0 ? outer : 1)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(row_elems * esz)};
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(box_inner), static_cast<cuuint32_t>(box_outer)};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(m, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                   const_cast<void*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return fail(RL_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d) for [%lld x %lld] box %dx%d", (int)r,
+                (long long)outer, (long long)inner, box_outer, box_inner);
+  return RL_OK;
+}
+
+// ----------------------------------------------------------------- GEMMs
+constexpr int kStages = 4;
+
+template <int MODE, bool A_MN, bool B_MN>
+rl_status launch_gemm(int kid, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c, int64_t M, int64_t N,
+                      int64_t K, int group_m, const rl::EpiParams& ep, int sms, cudaStream_t st) {
+  if (M <= 0 || N <= 0) return RL_OK;
+  auto kern = rl::gemm_kernel<MODE, A_MN, B_MN, kStages>;
+  constexpr int smem = rl::gemm_smem_bytes<kStages>();
+  static bool attr_set = false;  // per instantiation
+  if (!attr_set) {
+    RL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    attr_set = true;
+  }
+  rl::GemmShape sh;
+  sh.m_blocks = static_cast<int>((M + rl::BM - 1) / rl::BM);
+  sh.n_blocks = static_cast<int>((N + rl::BN - 1) / rl::BN);
+  sh.k_blocks = static_cast<int>((K + rl::BK - 1) / rl::BK);
+  sh.group_m = group_m;
+  if (sh.k_blocks == 0) return fail(RL_ERR_SHAPE, "GEMM with K = 0");
+  const int64_t tiles = static_cast<int64_t>(sh.m_blocks) * sh.n_blocks;
+  const int grid = static_cast<int>(tiles < sms ? tiles : sms);
+  {
+    ProfScope ps(kid, st);
+    kern<<<grid, rl::GEMM_THREADS, smem, st>>>(a, b, c, sh, ep);
+  }
+  RL_CHECK_LAUNCH();
+  return RL_OK;
+}
+
+// ------------------------------------------------------------ workspace
+inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+struct Carve {
+  size_t off = 0;
+  size_t take(size_t bytes) {
+    size_t o = align_up(off, 1024);
+    off = o + bytes;
+    return o;
+  }
+};
+
+struct WsLayout {
+  size_t partials, lse, coef, rp, dz, end;
+  int64_t n_tiles_v, ldz, chunk;
+};
+
+int64_t n_vocab_tiles(const rl_lm_shape* s) { return (s->V_local + rl::BN - 1) / rl::BN; }
+
+WsLayout ws_layout(const rl_lm_shape* s, int32_t R, int64_t chunk_rows) {
+  WsLayout w;
+  Carve c;
+  const int64_t T = s->T > 0 ? s->T : 0;
+  w.n_tiles_v = n_vocab_tiles(s);
+  w.ldz = (s->V_local + 7) / 8 * 8;
+  w.chunk = (chunk_rows <= 0 || chunk_rows > T) ? T : chunk_rows;
+  w.partials = c.take(static_cast<size_t>(w.n_tiles_v) * T * 16);
+  w.lse = c.take(static_cast<size_t>(T) * 4);
+  w.coef = c.take(static_cast<size_t>(T) * 4);
+  w.rp = c.take(static_cast<size_t>(R > 0 ? R : 1) * sizeof(rl::RolloutPartial));
+  w.dz = c.take(static_cast<size_t>(w.chunk) * w.ldz * 2);
+  w.end = align_up(c.off, 1024);
+  return w;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+rl_status check_shape(const rl_lm_shape* s) {
+  if (!s) return fail(RL_ERR_INVALID_ARGUMENT, "shape is NULL");
+  if (s->T < 0 || s->T > (int64_t(1) << 31) - 1) return fail(RL_ERR_SHAPE, "T = %lld out of range", (long long)s->T);
+  if (s->H <= 0 || s->H % 8 != 0 || s->H > 65536) return fail(RL_ERR_SHAPE, "H = %lld must be a positive multiple of 8 <= 65536", (long long)s->H);
+  if (s->V_local <= 0 || s->V_local > (int64_t(1) << 31) - 1) return fail(RL_ERR_SHAPE, "V_local = %lld out of range", (long long)s->V_local);
+  if (s->vocab_offset < 0 || s->V_global < s->vocab_offset + s->V_local)
+    return fail(RL_ERR_SHAPE, "vocab_offset %lld + V_local %lld exceeds V_global %lld", (long long)s->vocab_offset,
+                (long long)s->V_local, (long long)s->V_global);
+  if (!(s->inv_temperature > 0.f) || !isfinite(s->inv_temperature))
+    return fail(RL_ERR_INVALID_ARGUMENT, "inv_temperature must be finite and > 0");
+  return RL_OK;
+}
+
+rl_status check_params(const rl_loss_params* p) {
+  if (!p) return fail(RL_ERR_INVALID_ARGUMENT, "params is NULL");
+  if (!(p->alpha > 0.f) || !(p->alpha <= 1.f) || !(p->beta >= 1.f) || !isfinite(p->beta))
+    return fail(RL_ERR_INVALID_ARGUMENT, "need 0 < alpha <= 1 <= beta (got alpha=%g beta=%g)", p->alpha, p->beta);
+  if (!(p->guard_threshold >= 0.f) || !isfinite(p->guard_threshold))
+    return fail(RL_ERR_INVALID_ARGUMENT, "guard_threshold must be finite and >= 0");
+  if (!(p->loss_denominator > 0.0) || !isfinite(p->loss_denominator))
+    return fail(RL_ERR_INVALID_ARGUMENT, "loss_denominator must be finite and > 0");
+  if (p->num_rollouts < 1) return fail(RL_ERR_INVALID_ARGUMENT, "num_rollouts must be >= 1");
+  return RL_OK;
+}
+
+#define RL_TRY(x)                  \
+  do {                             \
+    rl_status s_ = (x);            \
+    if (s_ != RL_OK) return s_;    \
+  } while (0)
+
+#define RL_NONNULL(p) \
+  if (!(p)) return fail(RL_ERR_INVALID_ARGUMENT, "%s is NULL", #p)
+
+// K1 (+ K2): forward over the local shard. If `merged` is non-null, write one
+// merged partial per row; else write logprob/entropy/lse.
+rl_status forward_impl(const rl_lm_shape* s, const uint16_t* hidden, const uint16_t* w, const int32_t* targets,
+                       float* logprob, float* entropy, float* lse, float4* merged, uint8_t* ws, const WsLayout& L,
+                       int sms, cudaStream_t st) {
+  const int64_t T = s->T;
+  if (T == 0) return RL_OK;
+  CUtensorMap ta, tb;
+  RL_TRY(make_map(&ta, hidden, false, s->H, T, s->H, 64, rl::BM));
+  RL_TRY(make_map(&tb, w, false, s->H, s->V_local, s->H, 64, rl::BN));
+  rl::EpiParams ep = {};
+  ep.rows = T;
+  ep.cols = s->V_local;
+  ep.inv_temperature = s->inv_temperature;
+  ep.scale_log2 = s->inv_temperature * 1.4426950408889634f;
+  ep.targets = targets;
+  ep.vocab_offset = s->vocab_offset;
+  float4* parts = reinterpret_cast<float4*>(ws + L.partials);
+  ep.partials = parts;
+  RL_TRY((launch_gemm<rl::EPI_LSE, false, false>(RL_K_FWD_GEMM, ta, tb, ta, T, s->V_local, s->H, 16, ep, sms, st)));
+  const int blocks = static_cast<int>((T + 63) / 64);
+  {
+    ProfScope ps(RL_K_MERGE, st);
+    rl::merge_partials_kernel<<<blocks, 256, 0, st>>>(parts, static_cast<int>(L.n_tiles_v), T, logprob, entropy,
+                                                        lse, merged);
+  }
+  RL_CHECK_LAUNCH();
+  return RL_OK;
+}
+
+rl_status loss_impl(const rl_loss_params* p, int64_t T, int64_t V_global, const float* logprob, const float* infer,
+                    const int32_t* targets, const float* adv, const int32_t* offsets, const uint8_t* loss_mask,
+                    float* coef, uint8_t* keep, uint8_t* guarded, rl_loss_report* rep, rl::RolloutPartial* rp,
+                    cudaStream_t st) {
+  rl::LossArgs a;
+  a.alpha = p->alpha;
+  a.beta = p->beta;
+  a.guard = p->guard_threshold;
+  a.inv_D = 1.0 / p->loss_denominator;
+  a.R = p->num_rollouts;
+  a.T = T;
+  a.V_global = V_global;
+  a.logprob = logprob;
+  a.infer = infer;
+  a.targets = targets;
+  a.adv = adv;
+  a.offsets = offsets;
+  a.loss_mask = loss_mask;
+  a.coef = coef;
+  a.keep = keep;
+  a.guarded = guarded;
+  a.rp = rp;
+  {
+    ProfScope ps(RL_K_LOSS, st);
+    rl::loss_coef_kernel<<<p->num_rollouts, 256, 0, st>>>(a);
+  }
+  RL_CHECK_LAUNCH();
+  {
+    ProfScope ps(RL_K_FINALIZE, st);
+    rl::loss_finalize_kernel<<<1, 32, 0, st>>>(rp, p->num_rollouts, rep);
+  }
+  RL_CHECK_LAUNCH();
+  return RL_OK;
+}
+
+// K4 -> K5 -> K6 per chunk of rows.
+rl_status bwd_impl(const rl_lm_shape* s, const uint16_t* hidden, const uint16_t* w, const int32_t* targets,
+                   const float* lse, const float* coef, uint16_t* dh, float* dh32, float* dw, int accumulate_dw,
+                   uint8_t* ws, const WsLayout& L, int sms, cudaStream_t st) {
+  const int64_t T = s->T, H = s->H, V = s->V_local;
+  if (T == 0) {
+    if (dw && !accumulate_dw) RL_CUDA(cudaMemsetAsync(dw, 0, static_cast<size_t>(V) * H * 4, st));
+    return RL_OK;
+  }
+  uint16_t* dz = reinterpret_cast<uint16_t*>(ws + L.dz);
+  const int64_t chunk = L.chunk;
+  CUtensorMap t_h_k, t_w_k, t_dz_st, t_dz_k, t_w_mn, t_dh, t_dz_mn, t_h_mn, t_dw;
+  RL_TRY(make_map(&t_w_k, w, false, H, V, H, 64, rl::BN));
+  RL_TRY(make_map(&t_w_mn, w, false, H, V, H, 64, 64));
+  if (dw) RL_TRY(make_map(&t_dw, dw, true, H, V, H, 32, 32));
+  for (int64_t c0 = 0; c0 < T; c0 += chunk) {
+    const int64_t rows = (T - c0 < chunk) ? (T - c0) : chunk;
+    const uint16_t* hc = hidden + c0 * H;
+    RL_TRY(make_map(&t_h_k, hc, false, H, rows, H, 64, rl::BM));
+    RL_TRY(make_map(&t_dz_st, dz, false, V, rows, L.ldz, 64, 32));
+    // K4: dU chunk = coef invT (softmax - onehot), bf16
+    rl::EpiParams ep = {};
+    ep.rows = rows;
+    ep.cols = V;
+    ep.inv_temperature = s->inv_temperature;
+    ep.scale_log2 = s->inv_temperature * 1.4426950408889634f;
+    ep.targets = targets + c0;
+    ep.vocab_offset = s->vocab_offset;
+    ep.lse = lse + c0;
+    ep.coef = coef + c0;
+    RL_TRY((launch_gemm<rl::EPI_DZ, false, false>(RL_K_DZ_GEMM, t_h_k, t_w_k, t_dz_st, rows, V, H, 16, ep, sms, st)));
+    // K5: dH chunk = dU W
+    if (dh || dh32) {
+      RL_TRY(make_map(&t_dz_k, dz, false, V, rows, L.ldz, 64, rl::BM));
+      rl::EpiParams e5 = {};
+      e5.rows = rows;
+      e5.cols = H;
+      if (dh) {
+        RL_TRY(make_map(&t_dh, dh + c0 * H, false, H, rows, H, 64, 32));
+        RL_TRY((launch_gemm<rl::EPI_BF16, false, true>(RL_K_DH_GEMM, t_dz_k, t_w_mn, t_dh, rows, H, V, 8, e5, sms, st)));
+      } else {
+        RL_TRY(make_map(&t_dh, dh32 + c0 * H, true, H, rows, H, 32, 32));
+        RL_TRY((launch_gemm<rl::EPI_F32, false, true>(RL_K_DH_GEMM, t_dz_k, t_w_mn, t_dh, rows, H, V, 8, e5, sms, st)));
+      }
+    }
+    // K6: dW (+)= dU^T h
+    if (dw) {
+      RL_TRY(make_map(&t_dz_mn, dz, false, V, rows, L.ldz, 64, 64));
+      RL_TRY(make_map(&t_h_mn, hc, false, H, rows, H, 64, 64));
+      rl::EpiParams e6 = {};
+      e6.rows = V;
+      e6.cols = H;
+      if (c0 == 0 && !accumulate_dw) {
+        RL_TRY((launch_gemm<rl::EPI_F32, true, true>(RL_K_DW_GEMM, t_dz_mn, t_h_mn, t_dw, V, H, rows, 8, e6, sms, st)));
+      } else {
+        RL_TRY((launch_gemm<rl::EPI_F32_ADD, true, true>(RL_K_DW_GEMM, t_dz_mn, t_h_mn, t_dw, V, H, rows, 8, e6, sms, st)));
+      }
+    }
+  }
+  return RL_OK;
+}
+
+}  // namespace
+
+// =================================================================== C ABI
+extern "C" {
+
+const char* rl_status_string(rl_status s) {
+  switch (s) {
+    case RL_OK: return "RL_OK";
+    case RL_ERR_INVALID_ARGUMENT: return "RL_ERR_INVALID_ARGUMENT";
+    case RL_ERR_SHAPE: return "RL_ERR_SHAPE";
+    case RL_ERR_UNSUPPORTED: return "RL_ERR_UNSUPPORTED";
+    case RL_ERR_CUDA: return "RL_ERR_CUDA";
+    case RL_ERR_WORKSPACE: return "RL_ERR_WORKSPACE";
+    case RL_ERR_ALIGNMENT: return "RL_ERR_ALIGNMENT";
+  }
+  return "RL_ERR_UNKNOWN";
+}
+
+const char* rl_last_error_message(void) { return g_err; }
+int32_t rl_abi_version(void) { return RL_ABI_VERSION; }
+int32_t rl_last_launch_count(void) { return g_launches; }
+
+rl_status rl_profile_enable(int32_t enable) {
+  g_prof = enable != 0;
+  return RL_OK;
+}
+
+int32_t rl_profile_read(rl_kernel_time* out, int32_t cap) {
+  const int32_t n = static_cast<int32_t>(g_prof_recs.size());
+  for (int32_t i = 0; i < n; ++i) {
+    ProfRec& r = g_prof_recs[i];
+    float ms = 0.f;
+    cudaEventSynchronize(r.b);
+    cudaEventElapsedTime(&ms, r.a, r.b);
+    if (out && i < cap) out[i] = rl_kernel_time{r.kernel, ms};
+    g_prof_pool.push_back(r.a);
+    g_prof_pool.push_back(r.b);
+  }
+  g_prof_recs.clear();
+  return n;
+}
+
+int64_t rl_default_dz_chunk_rows(const rl_lm_shape* shape) { return shape ? shape->T : 0; }
+
+size_t rl_workspace_bytes(const rl_lm_shape* shape, int32_t num_rollouts, int64_t dz_chunk_rows) {
+  if (check_shape(shape) != RL_OK) return 0;
+  return ws_layout(shape, num_rollouts, dz_chunk_rows).end;
+}
+
+size_t rl_workspace_bytes_hostio(const rl_lm_shape* shape, int32_t num_rollouts) {
+  if (check_shape(shape) != RL_OK) return 0;
+  const size_t base = ws_layout(shape, num_rollouts, 0).end;
+  Carve c;
+  c.off = base;
+  const size_t T = static_cast<size_t>(shape->T), R = static_cast<size_t>(num_rollouts > 0 ? num_rollouts : 1);
+  c.take(T * shape->H * 2);  // hidden
+  c.take(T * 4);             // targets
+  c.take(T * 4);             // infer
+  c.take(R * 4);             // rewards
+  c.take(R * 4);             // advantages
+  c.take((R + 1) * 4);       // offsets
+  c.take(T);                 // loss mask
+  c.take(T * 4);             // logprob
+  return align_up(c.off, 1024);
+}
+
+rl_status rl_group_advantages(const float* rewards, int32_t num_groups, int32_t group_size, float* advantages,
+                              void* stream) {
+  g_launches = 0;
+  RL_NONNULL(rewards);
+  RL_NONNULL(advantages);
+  if (num_groups < 0) return fail(RL_ERR_SHAPE, "num_groups < 0");
+  if (group_size < 2) return fail(RL_ERR_INVALID_ARGUMENT, "group_size must be >= 2 (got %d)", group_size);
+  DevInfo d;
+  RL_TRY(device_info(d));
+  if (num_groups == 0) return RL_OK;
+  const int threads = 256;
+  const int blocks = static_cast<int>((static_cast<int64_t>(num_groups) * 32 + threads - 1) / threads);
+  {
+    ProfScope ps(RL_K_GROUP_ADV, static_cast<cudaStream_t>(stream));
+    rl::group_adv_kernel<<<blocks, threads, 0, static_cast<cudaStream_t>(stream)>>>(rewards, num_groups,
+                                                                                    group_size, advantages);
+  }
+  RL_CHECK_LAUNCH();
+  return RL_OK;
+}
+
+rl_status rl_logprob_fwd(const rl_lm_shape* shape, const uint16_t* hidden, const uint16_t* w_vocab,
+                         const int32_t* targets, float* logprob, float* entropy, float* lse, void* workspace,
+                         size_t workspace_bytes, void* stream) {
+  g_launches = 0;
+  RL_TRY(check_shape(shape));
+  if (shape->V_local != shape->V_global || shape->vocab_offset != 0)
+    return fail(RL_ERR_SHAPE, "rl_logprob_fwd needs the full vocabulary; use rl_fwd_partials for a shard");
+  if (shape->T > 0) {
+    RL_NONNULL(hidden);
+    RL_NONNULL(w_vocab);
+    RL_NONNULL(targets);
+    RL_NONNULL(logprob);
+    if (!aligned16(hidden) || !aligned16(w_vocab) || !aligned16(workspace))
+      return fail(RL_ERR_ALIGNMENT, "hidden, w_vocab and workspace must be 16-byte aligned");
+  }
+  const WsLayout L = ws_layout(shape, 1, 0);
+  if (shape->T > 0 && (!workspace || workspace_bytes < L.end))
+    return fail(RL_ERR_WORKSPACE, "workspace needs %zu bytes, got %zu", L.end, workspace_bytes);
+  DevInfo d;
+  RL_TRY(device_info(d));
+  return forward_impl(shape, hidden, w_vocab, targets, logprob, entropy, lse, nullptr,
+                      static_cast<uint8_t*>(workspace), L, d.sms, static_cast<cudaStream_t>(stream));
+}
+
+rl_status rl_fwd_partials(const rl_lm_shape* shape, const uint16_t* hidden, const uint16_t* w_vocab,
+                          const int32_t* targets, float* partials, void* workspace, size_t workspace_bytes,
+                          void* stream) {
+  g_launches = 0;
+  RL_TRY(check_shape(shape));
+  if (shape->T > 0) {
+    RL_NONNULL(hidden);
+    RL_NONNULL(w_vocab);
+    RL_NONNULL(targets);
+    RL_NONNULL(partials);
+    if (!aligned16(hidden) || !aligned16(w_vocab) || !aligned16(workspace) || !aligned16(partials))
+      return fail(RL_ERR_ALIGNMENT, "hidden, w_vocab, partials and workspace must be 16-byte aligned");
+  }
+  const WsLayout L = ws_layout(shape, 1, 0);
+  if (shape->T > 0 && (!workspace || workspace_bytes < L.end))
+    return fail(RL_ERR_WORKSPACE, "workspace needs %zu bytes, got %zu", L.end, workspace_bytes);
+  DevInfo d;
+  RL_TRY(device_info(d));
+  return forward_impl(shape, hidden, w_vocab, targets, nullptr, nullptr, nullptr, reinterpret_cast<float4*>(partials),
+                      static_cast<uint8_t*>(workspace), L, d.sms, static_cast<cudaStream_t>(stream));
+}
+
+rl_status rl_merge_partials(const float* partials, int32_t n_parts, int64_t T, float* logprob, float* entropy,
+                            float* lse, void* stream) {
+  g_launches = 0;
+  if (T < 0 || n_parts < 1) return fail(RL_ERR_SHAPE, "need T >= 0 and n_parts >= 1");
+  if (T == 0) return RL_OK;
+  RL_NONNULL(partials);
+  RL_NONNULL(logprob);
+  if (!aligned16(partials)) return fail(RL_ERR_ALIGNMENT, "partials must be 16-byte aligned");
+  DevInfo d;
+  RL_TRY(device_info(d));
+  const int blocks = static_cast<int>((T + 63) / 64);
+  {
+    ProfScope ps(RL_K_MERGE, static_cast<cudaStream_t>(stream));
+    rl::merge_partials_kernel<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+        reinterpret_cast<const float4*>(partials), n_parts, T, logprob, entropy, lse, nullptr);
+  }
+  RL_CHECK_LAUNCH();
+  return RL_OK;
+}
+
+rl_status rl_loss_coef(const rl_loss_params* params, int64_t T, int64_t V_global, const float* logprob,
+                       const float* infer_logprobs, const int32_t* targets, const float* rollout_adv,
+                       const int32_t* rollout_offsets, const uint8_t* loss_mask, float* coef, uint8_t* token_keep,
+                       uint8_t* rollout_guarded, rl_loss_report* report, void* workspace, size_t workspace_bytes,
+                       void* stream) {
+  g_launches = 0;
+  RL_TRY(check_params(params));
+  if (T < 0) return fail(RL_ERR_SHAPE, "T < 0");
+  RL_NONNULL(rollout_adv);
+  RL_NONNULL(rollout_offsets);
+  RL_NONNULL(report);
+  if (T > 0) {
+    RL_NONNULL(logprob);
+    RL_NONNULL(infer_logprobs);
+    RL_NONNULL(coef);
+  }
+  const size_t need = static_cast<size_t>(params->num_rollouts) * sizeof(rl::RolloutPartial);
+  if (!workspace || workspace_bytes < need)
+    return fail(RL_ERR_WORKSPACE, "workspace needs %zu bytes, got %zu", need, workspace_bytes);
+  DevInfo d;
+  RL_TRY(device_info(d));
+  return loss_impl(params, T, V_global, logprob, infer_logprobs, targets, rollout_adv, rollout_offsets, loss_mask,
+                   coef, token_keep, rollout_guarded, report, static_cast<rl::RolloutPartial*>(workspace),
+                   static_cast<cudaStream_t>(stream));
+}
+
+rl_status rl_bwd(const rl_lm_shape* shape, const uint16_t* hidden, const uint16_t* w_vocab, const int32_t* targets,
+                 const float* lse, const float* coef, uint16_t* d_hidden, float* d_hidden_f32, float* d_w_vocab,
+                 int32_t accumulate_dw, int64_t dz_chunk_rows, void* workspace, size_t workspace_bytes,
+                 void* stream) {
+  g_launches = 0;
+  RL_TRY(check_shape(shape));
+  if (d_hidden && d_hidden_f32) return fail(RL_ERR_INVALID_ARGUMENT, "pass d_hidden or d_hidden_f32, not both");
+  RL_NONNULL(w_vocab);
+  if (shape->T > 0) {
+    RL_NONNULL(hidden);
+    RL_NONNULL(targets);
+    RL_NONNULL(lse);
+    RL_NONNULL(coef);
+  }
+  if (!aligned16(hidden) || !aligned16(w_vocab) || !aligned16(workspace) || !aligned16(d_hidden) ||
+      !aligned16(d_hidden_f32) || !aligned16(d_w_vocab))
+    return fail(RL_ERR_ALIGNMENT, "matrix pointers and workspace must be 16-byte aligned");
+  const WsLayout L = ws_layout(shape, 1, dz_chunk_rows);
+  if (shape->T > 0 && (!workspace || workspace_bytes < L.end))
+    return fail(RL_ERR_WORKSPACE, "workspace needs %zu bytes, got %zu", L.end, workspace_bytes);
+  DevInfo d;
+  RL_TRY(device_info(d));
+  return bwd_impl(shape, hidden, w_vocab, targets, lse, coef, d_hidden, d_hidden_f32, d_w_vocab, accumulate_dw,
+                  static_cast<uint8_t*>(workspace), L, d.sms, static_cast<cudaStream_t>(stream));
+}
+
+static rl_status step_impl(const rl_lm_shape* shape, const rl_loss_params* params, const uint16_t* hidden,
+                           const uint16_t* w_vocab, const int32_t* targets, const float* infer_logprobs,
+                           const float* rollout_adv, const int32_t* rollout_offsets, const uint8_t* loss_mask,
+                           const rl_loss_outputs* out, uint8_t* ws, const WsLayout& L, int sms, cudaStream_t st) {
+  float* lse = out->lse ? out->lse : reinterpret_cast<float*>(ws + L.lse);
+  float* coef = out->coef ? out->coef : reinterpret_cast<float*>(ws + L.coef);
+  RL_TRY(forward_impl(shape, hidden, w_vocab, targets, out->logprob, out->entropy, lse, nullptr, ws, L, sms, st));
+  const int fwd = g_launches;
+  RL_TRY(loss_impl(params, shape->T, shape->V_global, out->logprob, infer_logprobs, targets, rollout_adv,
+                   rollout_offsets, loss_mask, coef, out->token_keep, out->rollout_guarded, out->report,
+                   reinterpret_cast<rl::RolloutPartial*>(ws + L.rp), st));
+  const int mid = g_launches;
+  RL_TRY(bwd_impl(shape, hidden, w_vocab, targets, lse, coef, out->d_hidden, out->d_hidden_f32, out->d_w_vocab,
+                  out->accumulate_dw, ws, L, sms, st));
+  (void)fwd;
+  (void)mid;
+  return RL_OK;
+}
+
+static rl_status check_step_args(const rl_lm_shape* shape, const rl_loss_params* params, const uint16_t* w_vocab,
+                                 const rl_loss_outputs* out, bool need_logprob) {
+  RL_TRY(check_shape(shape));
+  RL_TRY(check_params(params));
+  if (shape->V_local != shape->V_global || shape->vocab_offset != 0)
+    return fail(RL_ERR_SHAPE, "rl_policy_loss_fwd_bwd needs the full vocabulary; vocab-parallel callers use the split phases");
+  RL_NONNULL(out);
+  RL_NONNULL(out->report);
+  RL_NONNULL(w_vocab);
+  if (out->d_hidden && out->d_hidden_f32) return fail(RL_ERR_INVALID_ARGUMENT, "pass d_hidden or d_hidden_f32, not both");
+  if (!aligned16(w_vocab) || !aligned16(out->d_hidden) || !aligned16(out->d_hidden_f32) || !aligned16(out->d_w_vocab))
+    return fail(RL_ERR_ALIGNMENT, "matrix pointers must be 16-byte aligned");
+  if (need_logprob && shape->T > 0) RL_NONNULL(out->logprob);
+  return RL_OK;
+}
+
+rl_status rl_policy_loss_fwd_bwd(const rl_lm_shape* shape, const rl_loss_params* params, const uint16_t* hidden,
+                                 const uint16_t* w_vocab, const int32_t* targets, const float* infer_logprobs,
+                                 const float* rollout_adv, const int32_t* rollout_offsets, const uint8_t* loss_mask,
+                                 const rl_loss_outputs* out, void* workspace, size_t workspace_bytes, void* stream) {
+  g_launches = 0;
+  RL_TRY(check_step_args(shape, params, w_vocab, out, true));
+  RL_NONNULL(rollout_adv);
+  RL_NONNULL(rollout_offsets);
+  if (shape->T > 0) {
+    RL_NONNULL(hidden);
+    RL_NONNULL(targets);
+    RL_NONNULL(infer_logprobs);
+    if (!aligned16(hidden)) return fail(RL_ERR_ALIGNMENT, "hidden must be 16-byte aligned");
+  }
+  const WsLayout L = ws_layout(shape, params->num_rollouts, 0);
+  if (!workspace || workspace_bytes < L.end)
+    return fail(RL_ERR_WORKSPACE, "workspace needs %zu bytes, got %zu", L.end, workspace_bytes);
+  if (!aligned16(workspace)) return fail(RL_ERR_ALIGNMENT, "workspace must be 16-byte aligned");
+  DevInfo d;
+  RL_TRY(device_info(d));
+  return step_impl(shape, params, hidden, w_vocab, targets, infer_logprobs, rollout_adv, rollout_offsets, loss_mask,
+                   out, static_cast<uint8_t*>(workspace), L, d.sms, static_cast<cudaStream_t>(stream));
+}
+
+rl_status rl_policy_loss_fwd_bwd_hostio(const rl_lm_shape* shape, const rl_loss_params* params, int32_t group_size,
+                                        const uint16_t* hidden_host, const uint16_t* w_vocab,
+                                        const int32_t* targets_host, const float* infer_host,
+                                        const float* rewards_host, const int32_t* offsets_host,
+                                        const uint8_t* loss_mask_host, const rl_loss_outputs* out,
+                                        rl_loss_report* report_host, void* workspace, size_t workspace_bytes,
+                                        void* stream) {
+  g_launches = 0;
+  RL_TRY(check_step_args(shape, params, w_vocab, out, false));
+  RL_NONNULL(rewards_host);
+  RL_NONNULL(offsets_host);
+  RL_NONNULL(report_host);
+  if (group_size < 2 || params->num_rollouts % group_size != 0)
+    return fail(RL_ERR_INVALID_ARGUMENT, "group_size must be >= 2 and divide num_rollouts");
+  const int64_t T = shape->T;
+  if (T > 0) {
+    RL_NONNULL(hidden_host);
+    RL_NONNULL(targets_host);
+    RL_NONNULL(infer_host);
+  }
+  const size_t need = rl_workspace_bytes_hostio(shape, params->num_rollouts);
+  if (!workspace || workspace_bytes < need)
+    return fail(RL_ERR_WORKSPACE, "workspace needs %zu bytes, got %zu", need, workspace_bytes);
+  if (!aligned16(workspace)) return fail(RL_ERR_ALIGNMENT, "workspace must be 16-byte aligned");
+  DevInfo d;
+  RL_TRY(device_info(d));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  uint8_t* ws = static_cast<uint8_t*>(workspace);
+  const WsLayout L = ws_layout(shape, params->num_rollouts, 0);
+  Carve c;
+  c.off = L.end;
+  const size_t R = static_cast<size_t>(params->num_rollouts);
+  uint16_t* d_hidden_in = reinterpret_cast<uint16_t*>(ws + c.take(T * shape->H * 2));
+  int32_t* d_tg = reinterpret_cast<int32_t*>(ws + c.take(T * 4));
+  float* d_inf = reinterpret_cast<float*>(ws + c.take(T * 4));
+  float* d_rw = reinterpret_cast<float*>(ws + c.take(R * 4));
+  float* d_adv = reinterpret_cast<float*>(ws + c.take(R * 4));
+  int32_t* d_off = reinterpret_cast<int32_t*>(ws + c.take((R + 1) * 4));
+  uint8_t* d_lm = ws + c.take(T);
+  float* d_lp = reinterpret_cast<float*>(ws + c.take(T * 4));
+  if (T > 0) {
+    RL_CUDA(cudaMemcpyAsync(d_hidden_in, hidden_host, T * shape->H * 2, cudaMemcpyHostToDevice, st));
+    RL_CUDA(cudaMemcpyAsync(d_tg, targets_host, T * 4, cudaMemcpyHostToDevice, st));
+    RL_CUDA(cudaMemcpyAsync(d_inf, infer_host, T * 4, cudaMemcpyHostToDevice, st));
+    if (loss_mask_host) RL_CUDA(cudaMemcpyAsync(d_lm, loss_mask_host, T, cudaMemcpyHostToDevice, st));
+  }
+  RL_CUDA(cudaMemcpyAsync(d_rw, rewards_host, R * 4, cudaMemcpyHostToDevice, st));
+  RL_CUDA(cudaMemcpyAsync(d_off, offsets_host, (R + 1) * 4, cudaMemcpyHostToDevice, st));
+  const int ng = static_cast<int>(R / group_size);
+  {
+    ProfScope ps(RL_K_GROUP_ADV, st);
+    rl::group_adv_kernel<<<(ng * 32 + 255) / 256, 256, 0, st>>>(d_rw, ng, group_size, d_adv);
+  }
+  RL_CHECK_LAUNCH();
+  rl_loss_outputs o = *out;
+  if (!o.logprob) o.logprob = d_lp;
+  const int before = g_launches;
+  rl_status s = step_impl(shape, params, d_hidden_in, w_vocab, d_tg, d_inf, d_adv, d_off,
+                          loss_mask_host ? d_lm : nullptr, &o, ws, L, d.sms, st);
+  (void)before;
+  if (s != RL_OK) return s;
+  RL_CUDA(cudaMemcpyAsync(report_host, out->report, sizeof(rl_loss_report), cudaMemcpyDeviceToHost, st));
+  RL_CUDA(cudaStreamSynchronize(st));
+  return RL_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,338 @@
+// Persistent warp-specialised tcgen05 GEMM with the path's fused epilogues.
+//
+//   D[m, n] = sum_k A[m, k] * B[n, k]      (bf16 in, fp32 accumulate in TMEM)
+//
+// One CTA per SM, 128x256 output tiles, BK = 64, a STAGES-deep TMA->SMEM ring,
+// two TMEM accumulators (2 x 256 columns) so the epilogue of tile i overlaps the
+// MMAs of tile i+1. Warp roles: warp 0 = TMA producer (one thread), warp 1 =
+// TMEM owner + MMA issuer (one thread), warps 2..5 = epilogue (thread = row).
+//
+// Epilogues:
+//   EPI_LSE  (K1): per row of the tile, online (m, s, u, z_target) over the
+//                  tile's 256 scaled logits -> one float4 partial per (n-tile, row).
+//                  Logits never leave TMEM/registers.
+//   EPI_DZ   (K4): dU = coef*invT*(exp(z - lse) - [v == y]) -> bf16 -> TMA store.
+//   EPI_BF16 (K5): plain bf16 store.   EPI_F32 / EPI_F32_ADD (K5/K6): fp32 store
+//                  or TMA reduce-add into the destination.
+#pragma once
+#include "rl_ptx.cuh"
+
+namespace rl {
+
+constexpr int BM = 128, BN = 256, BK = 64;
+constexpr int GEMM_THREADS = 192;
+constexpr int A_STAGE_BYTES = BM * BK * 2;  // 16 KB
+constexpr int B_STAGE_BYTES = BN * BK * 2;  // 32 KB
+constexpr int EPI_BUF_BYTES = 32 * 128;     // one warp's 32-row x 128-byte store chunk
+constexpr int EPI_BYTES = 4 * 2 * EPI_BUF_BYTES;
+constexpr int BAR_BYTES = 256;
+
+enum EpiMode { EPI_LSE = 0, EPI_DZ = 1, EPI_BF16 = 2, EPI_F32 = 3, EPI_F32_ADD = 4 };
+
+template <int STAGES>
+constexpr int gemm_smem_bytes() {
+  return 1024 + STAGES * (A_STAGE_BYTES + B_STAGE_BYTES) + EPI_BYTES + BAR_BYTES;
+}
+
+struct GemmShape {
+  int m_blocks, n_blocks, k_blocks;
+  int group_m;  // raster: tiles walk n inside groups of group_m m-blocks
+};
+
+struct EpiParams {
+  int64_t rows;          // valid rows of D (M)
+  int64_t cols;          // valid columns of D (N)
+  float scale_log2;      // invT * log2(e)
+  float inv_temperature; // invT
+  // EPI_LSE / EPI_DZ
+  const int32_t* targets;  // [rows] global ids, row-indexed from D's row 0
+  int64_t vocab_offset;    // global id of D's column 0
+  float4* partials;        // EPI_LSE: [n_blocks][rows]
+  const float* lse;        // EPI_DZ:  [rows]
+  const float* coef;       // EPI_DZ:  [rows]
+};
+
+__device__ __forceinline__ void tile_coords(int tile, const GemmShape& sh, int& m, int& n) {
+  const int per_group = sh.group_m * sh.n_blocks;
+  const int g = tile / per_group;
+  const int first_m = g * sh.group_m;
+  const int gsize = min(sh.group_m, sh.m_blocks - first_m);
+  const int r = tile - g * per_group;
+  m = first_m + r % gsize;
+  n = r / gsize;
+}
+
+// Write one thread's 128-byte row chunk into a 128B-swizzled 32-row staging buffer.
+__device__ __forceinline__ void stage_row(uint32_t buf, int row, const uint32_t (&w)[32], int base) {
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const uint32_t addr = buf + row * 128 + ((j ^ (row & 7)) << 4);
+    st_shared_v4(addr, w[base + 4 * j], w[base + 4 * j + 1], w[base + 4 * j + 2], w[base + 4 * j + 3]);
+  }
+}
+
+template <int MODE, bool A_MN, bool B_MN, int STAGES>
+__global__ void __launch_bounds__(GEMM_THREADS, 1)
+    gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                const __grid_constant__ CUtensorMap tmC, const GemmShape sh, const EpiParams ep) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = sA + STAGES * A_STAGE_BYTES;
+  uint8_t* sEpi = sB + STAGES * B_STAGE_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sEpi + EPI_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 4);
+    }
+    fence_mbar_init();
+    tma_prefetch(&tmA);
+    tma_prefetch(&tmB);
+    if (MODE != EPI_LSE) tma_prefetch(&tmC);
+  }
+  if (warp == 1) {
+    tmem_alloc(tmem_slot, 512);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  const int total = sh.m_blocks * sh.n_blocks;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ----------------------------------------------------------- producer
+      int s = 0;
+      uint32_t ph = 0;
+      for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
+        int m, n;
+        tile_coords(tile, sh, m, n);
+        for (int kb = 0; kb < sh.k_blocks; ++kb) {
+          mbar_wait(&empty[s], ph ^ 1);
+          mbar_expect_tx(&full[s], A_STAGE_BYTES + B_STAGE_BYTES);
+          const int k0 = kb * BK;
+          uint8_t* a = sA + s * A_STAGE_BYTES;
+          uint8_t* b = sB + s * B_STAGE_BYTES;
+          if (!A_MN) {
+            tma_load_2d(a, &tmA, &full[s], k0, m * BM);
+          } else {
+            tma_load_2d(a, &tmA, &full[s], m * BM, k0);
+            tma_load_2d(a + 8192, &tmA, &full[s], m * BM + 64, k0);
+          }
+          if (!B_MN) {
+            tma_load_2d(b, &tmB, &full[s], k0, n * BN);
+          } else {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) tma_load_2d(b + j * 8192, &tmB, &full[s], n * BN + 64 * j, k0);
+          }
+          if (++s == STAGES) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // -------------------------------------------------------- MMA issuer
+      constexpr uint32_t idesc = umma_idesc_bf16(BM, BN, A_MN, B_MN);
+      int s = 0;
+      uint32_t ph = 0;
+      int acc = 0;
+      uint32_t aph = 0;
+      for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
+        mbar_wait(&tempty[acc], aph ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem_base + acc * BN;
+        for (int kb = 0; kb < sh.k_blocks; ++kb) {
+          mbar_wait(&full[s], ph);
+          tc_fence_after();
+          const uint32_t a0 = smem_u32(sA + s * A_STAGE_BYTES);
+          const uint32_t b0 = smem_u32(sB + s * B_STAGE_BYTES);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            const uint64_t ad = A_MN ? sw128_desc(a0 + k * 2048, 8192, 1024) : sw128_desc(a0 + k * 32, 16, 1024);
+            const uint64_t bd = B_MN ? sw128_desc(b0 + k * 2048, 8192, 1024) : sw128_desc(b0 + k * 32, 16, 1024);
+            umma_bf16(d, ad, bd, idesc, (kb | k) != 0);
+          }
+          umma_commit(&empty[s]);
+          if (++s == STAGES) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+        umma_commit(&tfull[acc]);
+        acc ^= 1;
+        if (acc == 0) aph ^= 1;
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ epilogue
+    const int q = warp & 3;  // TMEM lane quarter this warp may access
+    const int r_in_tile = q * 32 + lane;
+    const uint32_t buf0 = smem_u32(sEpi + (warp - 2) * 2 * EPI_BUF_BYTES);
+    int acc = 0;
+    uint32_t aph = 0;
+    int chunk_ctr = 0;
+    for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
+      int m, n;
+      tile_coords(tile, sh, m, n);
+      const int64_t row = static_cast<int64_t>(m) * BM + r_in_tile;
+      const bool row_ok = row < ep.rows;
+      const int n0 = n * BN;
+      mbar_wait(&tfull[acc], aph);
+      tc_fence_after();
+      const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN;
+
+      if constexpr (MODE == EPI_LSE) {
+        int64_t y = row_ok ? static_cast<int64_t>(ep.targets[row]) - ep.vocab_offset : -1;
+        if (y >= ep.cols) y = -1;  // target lives in another vocab shard
+        const int64_t tl64 = y - n0;
+        const int tl = (tl64 >= 0 && tl64 < BN) ? static_cast<int>(tl64) : -1;
+        const int64_t nv64 = ep.cols - n0;
+        const int nvalid = nv64 < BN ? static_cast<int>(nv64) : BN;
+        float mrun = -1e30f, srun = 0.f, trun = 0.f, zt = -INFINITY;
+#pragma unroll 1
+        for (int c = 0; c < BN / 32; ++c) {
+          uint32_t r[32];
+          tmem_ld32(taddr + c * 32, r);
+          tmem_wait_ld();
+          float u[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) u[j] = __uint_as_float(r[j]) * ep.scale_log2;
+          if (nvalid < BN) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (c * 32 + j >= nvalid) u[j] = -1e30f;
+          }
+          if (tl >= c * 32 && tl < c * 32 + 32) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (j == tl - c * 32) zt = __uint_as_float(r[j]) * ep.inv_temperature;
+          }
+          float cm = u[0];
+#pragma unroll
+          for (int j = 1; j < 32; ++j) cm = fmaxf(cm, u[j]);
+          const float mn = fmaxf(mrun, cm);
+          const float sc = ex2f(mrun - mn);
+          trun = sc * fmaf(srun, mrun - mn, trun);
+          srun *= sc;
+          mrun = mn;
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const float d = u[j] - mn;
+            const float e = ex2f(d);
+            srun += e;
+            trun = fmaf(e, d, trun);
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[acc]);
+        if (row_ok) {
+          constexpr float LN2 = 0.69314718055994530942f;
+          ep.partials[static_cast<int64_t>(n) * ep.rows + row] = make_float4(mrun * LN2, srun, trun * LN2, zt);
+        }
+      } else {
+        // store epilogues: TMEM -> regs -> (math) -> swizzled smem -> TMA store
+        float g = 0.f, b2 = 0.f;
+        int tl = -1;
+        if constexpr (MODE == EPI_DZ) {
+          if (row_ok) {
+            g = ep.coef[row] * ep.inv_temperature;
+            b2 = ep.lse[row] * 1.4426950408889634f;
+            const int64_t yl = static_cast<int64_t>(ep.targets[row]) - ep.vocab_offset;
+            const int64_t t64 = yl - n0;
+            tl = (yl < ep.cols && t64 >= 0 && t64 < BN) ? static_cast<int>(t64) : -1;
+          }
+        }
+        constexpr int COLS = (MODE == EPI_DZ || MODE == EPI_BF16) ? 64 : 32;  // columns per 128-byte chunk
+#pragma unroll 1
+        for (int c = 0; c < BN / COLS; ++c) {
+          uint32_t w[32];
+          if constexpr (COLS == 64) {
+            uint32_t r0[32], r1[32];
+            tmem_ld32(taddr + c * 64, r0);
+            tmem_ld32(taddr + c * 64 + 32, r1);
+            tmem_wait_ld();
+            if (c == BN / COLS - 1) {
+              tc_fence_before();
+              __syncwarp();
+              if (lane == 0) mbar_arrive(&tempty[acc]);
+            }
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              float v0 = __uint_as_float(r0[2 * j]), v1 = __uint_as_float(r0[2 * j + 1]);
+              float v2 = __uint_as_float(r1[2 * j]), v3 = __uint_as_float(r1[2 * j + 1]);
+              if constexpr (MODE == EPI_DZ) {
+                v0 = g * ex2f(fmaf(v0, ep.scale_log2, -b2));
+                v1 = g * ex2f(fmaf(v1, ep.scale_log2, -b2));
+                v2 = g * ex2f(fmaf(v2, ep.scale_log2, -b2));
+                v3 = g * ex2f(fmaf(v3, ep.scale_log2, -b2));
+                const int cb = c * 64;
+                if (tl == cb + 2 * j) v0 -= g;
+                if (tl == cb + 2 * j + 1) v1 -= g;
+                if (tl == cb + 32 + 2 * j) v2 -= g;
+                if (tl == cb + 32 + 2 * j + 1) v3 -= g;
+              }
+              w[j] = pack_bf16x2(v0, v1);
+              w[16 + j] = pack_bf16x2(v2, v3);
+            }
+          } else {
+            uint32_t r0[32];
+            tmem_ld32(taddr + c * 32, r0);
+            tmem_wait_ld();
+            if (c == BN / COLS - 1) {
+              tc_fence_before();
+              __syncwarp();
+              if (lane == 0) mbar_arrive(&tempty[acc]);
+            }
+#pragma unroll
+            for (int j = 0; j < 32; ++j) w[j] = r0[j];
+          }
+          const uint32_t buf = buf0 + (chunk_ctr & 1) * EPI_BUF_BYTES;
+          if (lane == 0) bulk_wait_read<1>();
+          __syncwarp();
+          stage_row(buf, lane, w, 0);
+          fence_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            const int c0 = n0 + c * COLS;
+            const int c1 = m * BM + q * 32;
+            if constexpr (MODE == EPI_F32_ADD)
+              tma_reduce_add_2d(&tmC, sEpi + (buf - smem_u32(sEpi)), c0, c1);
+            else
+              tma_store_2d(&tmC, sEpi + (buf - smem_u32(sEpi)), c0, c1);
+            bulk_commit();
+          }
+          ++chunk_ctr;
+        }
+      }
+      acc ^= 1;
+      if (acc == 0) aph ^= 1;
+    }
+    if (lane == 0) bulk_wait_all();
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, 512);
+  }
+}
+
+}  // namespace rl

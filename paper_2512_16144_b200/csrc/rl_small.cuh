@@ -1,0 +1,249 @@
+// SIMT kernels of the path: S0 advantages (K0), S2 partial merge (K2), S3 loss
+// coefficients + report (K3a/K3b). All are memory/latency bound and tiny next to
+// the GEMMs; reductions use fixed-order trees so results are bit-reproducible.
+#pragma once
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "../../include/rl.h"
+
+namespace rl {
+
+// ------------------------------------------------------------------- K0
+// One warp per group: A = S - mean(S). Mean accumulated in fp64
+// in index order by lane 0 (G is small: 16 in the paper's run).
+__global__ void group_adv_kernel(const float* __restrict__ S, int num_groups, int G, float* __restrict__ A) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= num_groups) return;
+  const float* s = S + static_cast<int64_t>(warp) * G;
+  double sum = 0.0;
+  if (lane == 0)
+    for (int j = 0; j < G; ++j) sum += static_cast<double>(s[j]);
+  sum = __shfl_sync(0xffffffffu, sum, 0);
+  const double mean = sum / G;
+  for (int j = lane; j < G; j += 32)
+    A[static_cast<int64_t>(warp) * G + j] = static_cast<float>(static_cast<double>(s[j]) - mean);
+}
+
+// ------------------------------------------------------------------- K2
+// Merge n_parts partials (m, s, u, zt) per row in index order. 256 threads =
+// 64 rows x 4 slices; slice j takes parts j, j+4, ...; the 4 slice results are
+// merged in slice order. Output either final (logprob, entropy, lse) or one
+// merged float4 partial per row.
+struct Part {
+  float m, s, u, zt;
+};
+__device__ __forceinline__ Part merge2(Part a, Part b) {
+  // m' = max; s' = s_a e^{m_a-m'} + s_b e^{m_b-m'};
+  // u' = sum_x e^{m_x-m'} (u_x + s_x (m_x - m'));  zt' = max(zt)
+  const float M = fmaxf(a.m, b.m);
+  const float ea = (a.s > 0.f) ? expf(a.m - M) : 0.f;
+  const float eb = (b.s > 0.f) ? expf(b.m - M) : 0.f;
+  Part r;
+  r.m = M;
+  r.s = a.s * ea + b.s * eb;
+  r.u = ea * (a.u + a.s * (a.m - M)) + eb * (b.u + b.s * (b.m - M));
+  r.zt = fmaxf(a.zt, b.zt);
+  return r;
+}
+
+__global__ void merge_partials_kernel(const float4* __restrict__ parts, int n_parts, int64_t T,
+                                      float* __restrict__ logprob, float* __restrict__ entropy,
+                                      float* __restrict__ lse, float4* __restrict__ merged) {
+  __shared__ Part sh[4][64];
+  const int r = threadIdx.x & 63;
+  const int slice = threadIdx.x >> 6;
+  const int64_t row = static_cast<int64_t>(blockIdx.x) * 64 + r;
+  Part acc = {-1e30f, 0.f, 0.f, -INFINITY};
+  if (row < T) {
+    for (int p = slice; p < n_parts; p += 4) {
+      const float4 v = parts[static_cast<int64_t>(p) * T + row];
+      acc = merge2(acc, Part{v.x, v.y, v.z, v.w});
+    }
+  }
+  sh[slice][r] = acc;
+  __syncthreads();
+  if (slice == 0 && row < T) {
+    Part a = merge2(merge2(sh[0][r], sh[1][r]), merge2(sh[2][r], sh[3][r]));
+    if (merged != nullptr) {
+      merged[row] = make_float4(a.m, a.s, a.u, a.zt);
+    } else {
+      const float ls = logf(a.s);
+      const float l = a.m + ls;
+      logprob[row] = a.zt - l;
+      if (entropy) entropy[row] = ls - a.u / a.s;
+      if (lse) lse[row] = l;
+    }
+  }
+}
+
+// ------------------------------------------------------------------- K3
+struct RolloutPartial {
+  double loss;  // sum of coef over the rollout
+  double kl;
+  uint32_t kept, low, high, guarded, gtokens, nonfinite, badtgt, badoff;
+};
+
+template <typename T>
+__device__ __forceinline__ T block_reduce_sum(T v, T* sh) {
+  // fixed-order tree over blockDim.x (power of two) -> deterministic
+  sh[threadIdx.x] = v;
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) sh[threadIdx.x] = sh[threadIdx.x] + sh[threadIdx.x + s];
+    __syncthreads();
+  }
+  T r = sh[0];
+  __syncthreads();
+  return r;
+}
+
+struct LossArgs {
+  float alpha, beta, guard;
+  double inv_D;
+  int R;
+  int64_t T;
+  int64_t V_global;
+  const float* logprob;
+  const float* infer;
+  const int32_t* targets;
+  const float* adv;
+  const int32_t* offsets;
+  const uint8_t* loss_mask;
+  float* coef;
+  uint8_t* keep;
+  uint8_t* guarded;
+  RolloutPartial* rp;
+};
+
+// One block per rollout (256 threads). Pass 1: guard min over valid tokens.
+// Pass 2: Eq.2 gate, coef, counters. Offsets are validated by every block so all
+// blocks take the same decision without a grid-wide sync.
+__global__ void __launch_bounds__(256) loss_coef_kernel(const LossArgs a) {
+  __shared__ double shd[256];
+  __shared__ uint32_t shu[256];
+  __shared__ float shf[256];
+  __shared__ int bad;
+  const int i = blockIdx.x;
+  if (threadIdx.x == 0) bad = (a.offsets[0] != 0 || a.offsets[a.R] != a.T) ? 1 : 0;
+  __syncthreads();
+  for (int j = threadIdx.x; j < a.R; j += blockDim.x)
+    if (a.offsets[j] > a.offsets[j + 1]) bad = 1;
+  __syncthreads();
+  if (bad) {
+    const int64_t t0 = a.T * i / a.R, t1 = a.T * (i + 1) / a.R;
+    for (int64_t t = t0 + threadIdx.x; t < t1; t += blockDim.x) {
+      a.coef[t] = 0.f;
+      if (a.keep) a.keep[t] = 0;
+    }
+    if (threadIdx.x == 0) {
+      if (a.guarded) a.guarded[i] = 0;
+      RolloutPartial p = {};
+      p.badoff = (i == 0) ? 1u : 0u;
+      a.rp[i] = p;
+    }
+    return;
+  }
+  const int64_t t0 = a.offsets[i], t1 = a.offsets[i + 1];
+  const double A = static_cast<double>(a.adv[i]);
+
+  float kmin = INFINITY;
+  for (int64_t t = t0 + threadIdx.x; t < t1; t += blockDim.x) {
+    const bool lm = a.loss_mask ? (a.loss_mask[t] != 0) : true;
+    const float inf = a.infer[t];
+    const bool fin = isfinite(inf) && inf <= 0.f;
+    bool tg = true;
+    if (a.targets) {
+      const int32_t y = a.targets[t];
+      tg = y >= 0 && static_cast<int64_t>(y) < a.V_global;
+    }
+    if (lm && fin && tg) kmin = fminf(kmin, expf(a.logprob[t] - inf));
+  }
+  // block min (fixed tree)
+  shf[threadIdx.x] = kmin;
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) shf[threadIdx.x] = fminf(shf[threadIdx.x], shf[threadIdx.x + s]);
+    __syncthreads();
+  }
+  const bool g = shf[0] < a.guard;
+  __syncthreads();
+
+  double loss = 0.0, kl = 0.0;
+  uint32_t kept = 0, low = 0, high = 0, gtok = 0, nonfin = 0, badtgt = 0;
+  for (int64_t t = t0 + threadIdx.x; t < t1; t += blockDim.x) {
+    const bool lm = a.loss_mask ? (a.loss_mask[t] != 0) : true;
+    const float inf = a.infer[t];
+    const bool fin = isfinite(inf) && inf <= 0.f;
+    bool tg = true;
+    if (a.targets) {
+      const int32_t y = a.targets[t];
+      tg = y >= 0 && static_cast<int64_t>(y) < a.V_global;
+    }
+    const bool valid = lm && fin && tg;
+    float c = 0.f;
+    bool kp = false;
+    if (valid) {
+      const float d = a.logprob[t] - inf;
+      const float k = expf(d);
+      low += (k < a.alpha);
+      high += (k > a.beta);
+      gtok += g;
+      kl += static_cast<double>(k) - static_cast<double>(d) - 1.0;
+      kp = (k >= a.alpha) && (k <= a.beta) && !g;
+      if (kp) {
+        const double cd = static_cast<double>(k) * A * a.inv_D;
+        c = static_cast<float>(cd);
+        loss += cd;
+        ++kept;
+      }
+    } else if (lm) {
+      nonfin += !fin;
+      badtgt += (fin && !tg);
+    }
+    a.coef[t] = c;
+    if (a.keep) a.keep[t] = kp ? 1 : 0;
+  }
+  RolloutPartial p;
+  p.loss = block_reduce_sum(loss, shd);
+  p.kl = block_reduce_sum(kl, shd);
+  p.kept = block_reduce_sum(kept, shu);
+  p.low = block_reduce_sum(low, shu);
+  p.high = block_reduce_sum(high, shu);
+  p.gtokens = block_reduce_sum(gtok, shu);
+  p.nonfinite = block_reduce_sum(nonfin, shu);
+  p.badtgt = block_reduce_sum(badtgt, shu);
+  p.guarded = g ? 1u : 0u;
+  p.badoff = 0;
+  if (threadIdx.x == 0) {
+    a.rp[i] = p;
+    if (a.guarded) a.guarded[i] = g ? 1 : 0;
+  }
+}
+
+// One block: sum the R rollout partials in index order -> report.
+__global__ void loss_finalize_kernel(const RolloutPartial* __restrict__ rp, int R, rl_loss_report* rep) {
+  if (threadIdx.x != 0) return;
+  rl_loss_report r = {};
+  double loss = 0.0, kl = 0.0;
+  for (int i = 0; i < R; ++i) {
+    const RolloutPartial p = rp[i];
+    loss += p.loss;
+    kl += p.kl;
+    r.kept_tokens += p.kept;
+    r.masked_low += p.low;
+    r.masked_high += p.high;
+    r.guarded_rollouts += p.guarded;
+    r.guarded_tokens += p.gtokens;
+    r.nonfinite_inputs += p.nonfinite;
+    r.bad_targets += p.badtgt;
+    r.bad_offsets += p.badoff;
+  }
+  r.loss = -loss;
+  r.mismatch_kl_sum = kl;
+  *rep = r;
+}
+
+}  // namespace rl

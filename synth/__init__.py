@@ -209,3 +209,53 @@ def compose_infer_logprobs(logp_ref: np.ndarray, delta_noise: np.ndarray,
 def bf16_bits_to_float32(bits: np.ndarray) -> np.ndarray:
     """Exact widening of bf16 bit patterns to float32 (for building device tensors)."""
     return (np.asarray(bits, dtype=np.uint16).astype(np.uint32) << np.uint32(16)).view(np.float32)
+
+
+# ----------------------------------------------------------- device-side draw
+def make_batch_device(wl: Workload, seed: int = 0, *, device="cuda", tokens: int | None = None,
+                      vocab: int | None = None, vocab_offset: int = 0, vocab_total: int | None = None,
+                      w_seed: int = 12345):
+    """The same recipe as make_batch, drawn with torch's device generator (fast at
+    GLM sizes; used by bench.py, whose timed numbers need no oracle parity).
+    W rows [vocab_offset, vocab_offset + vocab) of a (vocab_total x H) matrix drawn
+    from `w_seed` (identical on every rank). Returns a dict of device tensors plus
+    host-side rewards/offsets/loss mask and the Delta noise / spikes as tensors."""
+    import torch
+
+    T = wl.tokens if tokens is None else int(tokens)
+    Vt = wl.vocab if vocab_total is None else int(vocab_total)
+    V = Vt - vocab_offset if vocab is None else int(vocab)
+    H = wl.hidden
+    g = torch.Generator(device=device)
+    g.manual_seed(int(seed) * 7919 + 1)
+    hidden = torch.empty(T, H, dtype=torch.bfloat16, device=device)
+    for r0 in range(0, T, 8192):
+        r1 = min(T, r0 + 8192)
+        hidden[r0:r1] = torch.randn(r1 - r0, H, generator=g, device=device).to(torch.bfloat16)
+    gw = torch.Generator(device=device)
+    std = wl.sigma_z / math.sqrt(H)
+    w = torch.empty(V, H, dtype=torch.bfloat16, device=device)
+    # draw the full matrix block by block so every shard sees the same rows
+    blk = 8192
+    for b0 in range(0, Vt, blk):
+        b1 = min(Vt, b0 + blk)
+        lo, hi = max(b0, vocab_offset), min(b1, vocab_offset + V)
+        if lo >= hi:
+            continue
+        gw.manual_seed(int(w_seed) * 1000003 + b0)
+        x = torch.randn(b1 - b0, H, generator=gw, device=device) * std
+        w[lo - vocab_offset: hi - vocab_offset] = x[lo - b0: hi - b0].to(torch.bfloat16)
+    targets = torch.randint(0, Vt, (T,), generator=g, device=device, dtype=torch.int64).to(torch.int32)
+    S = group_rewards(wl, seed)
+    L = rollout_lengths(wl, seed, T)
+    offsets = np.zeros(wl.num_rollouts + 1, dtype=np.int64)
+    offsets[1:] = np.cumsum(L)
+    lm = np.ones(T, dtype=np.uint8)
+    if wl.prompt_frac > 0:
+        for i in range(wl.num_rollouts):
+            a, b = int(offsets[i]), int(offsets[i + 1])
+            lm[a: a + int(math.floor(wl.prompt_frac * (b - a)))] = 0
+    delta = torch.randn(T, generator=g, device=device, dtype=torch.float32) * wl.delta_sigma
+    spikes = torch.rand(T, generator=g, device=device) < wl.spike_rate
+    return dict(hidden=hidden, w=w, targets=targets, rewards=S.reshape(-1).copy(),
+                offsets=offsets.astype(np.int32), loss_mask=lm, delta=delta, spikes=spikes)

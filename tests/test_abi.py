@@ -1,0 +1,66 @@
+"""The C-ABI library loads and exports every symbol include/rl.h declares;
+host-only entry points validate arguments (CPU, no compute calls)."""
+import ctypes
+import os
+import re
+
+import pytest
+
+import paper_2512_16144_b200 as rl
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared():
+    src = open(os.path.join(ROOT, "include", "rl.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(rl_[a-z0-9_]+)\s*\(", src)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    import __graft_entry__
+    __graft_entry__.build()
+    return rl.load_library()
+
+
+def test_every_declared_symbol_is_exported(lib):
+    names = _declared()
+    assert len(names) >= 14
+    for n in names:
+        assert hasattr(lib, n), n
+    assert set(names) == set(rl.EXPORTED)
+
+
+def test_struct_layouts_match_header(lib):
+    assert ctypes.sizeof(rl.rl_lm_shape) == 48
+    assert ctypes.sizeof(rl.rl_loss_params) == 24
+    assert ctypes.sizeof(rl.rl_loss_report) == 48
+    assert ctypes.sizeof(rl.rl_loss_outputs) == 88
+    assert lib.rl_abi_version() == 1
+
+
+def test_status_strings(lib):
+    assert lib.rl_status_string(0) == b"RL_OK"
+    assert lib.rl_status_string(5) == b"RL_ERR_WORKSPACE"
+
+
+def test_workspace_bytes_host_only(lib):
+    s = rl.make_shape(16384, 4096, 151552)
+    n = rl.rl_workspace_bytes(s, 16)
+    # partials (592 tiles x T x 16 B) + dU (T x V bf16) dominate
+    assert n >= 592 * 16384 * 16 + 16384 * 151552 * 2
+    assert rl.rl_workspace_bytes(s, 16, 1024) < n
+    bad = rl.make_shape(16, 60, 100)
+    assert rl.rl_workspace_bytes(bad, 1) == 0
+
+
+def test_host_validation_before_any_device_work(lib):
+    st = lib.rl_group_advantages(ctypes.c_void_p(16), 4, 1, ctypes.c_void_p(16), None)
+    assert st == 1 and b"group_size" in lib.rl_last_error_message()
+    p = rl.make_params(4, 0.0)
+    st = lib.rl_loss_coef(ctypes.byref(p), 10, 100, *([ctypes.c_void_p(16)] * 10), None, 0, None)
+    assert st == 1 and b"loss_denominator" in lib.rl_last_error_message()
+    p = rl.make_params(4, 10.0, alpha=0.6, beta=0.9)
+    st = lib.rl_loss_coef(ctypes.byref(p), 10, 100, *([ctypes.c_void_p(16)] * 10), None, 0, None)
+    assert st == 1

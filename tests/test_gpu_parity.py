@@ -1,0 +1,260 @@
+"""CUDA path vs the fp64 oracle, element by element, through the C ABI (`-m gpu`).
+
+Sizes span several 128x256 tiles with ragged tails in T, V and H (K), and the
+BASELINE.json tiny config; edge cases: empty batch, empty rollouts, malformed
+offsets, non-finite stored log-probs, out-of-range targets, loss-mask rows,
+temperature, chunked backward, gradient accumulation, fp32 dH, determinism.
+"""
+import numpy as np
+import pytest
+
+import harness
+import oracle
+import synth
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover - GPU box only
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+import paper_2512_16144_b200 as rl  # noqa: E402
+
+TINY = synth.CONFIGS["tiny"]
+RAGGED = synth.Workload("ragged", 3, 4, 28, 200, 1000, ragged=True, prompt_frac=0.1, delta_sigma=0.8,
+                        spike_rate=0.02)
+
+
+def test_group_advantages_vs_oracle():
+    rng = np.random.default_rng(0)
+    for Np, G in ((2, 4), (37, 16), (5, 2), (3, 33)):
+        S = (rng.random((Np, G)) < 0.5).astype(np.float32)
+        S[:, 0] = 0.3  # non-binary values too
+        got = rl.rl_group_advantages(torch.from_numpy(S.reshape(-1)).cuda(), G).cpu().numpy()
+        ref = oracle.group_advantages(S.astype(np.float64)).reshape(-1)
+        np.testing.assert_allclose(got, ref, atol=1e-7)
+    with pytest.raises(rl.RLError):
+        rl.rl_group_advantages(torch.zeros(4, device="cuda"), 1)
+
+
+@pytest.mark.parametrize("wl,tokens,vocab,hidden,invT", [
+    (TINY, None, None, None, 1.0),
+    (RAGGED, 333, 1000, 200, 1.0),
+    (RAGGED, 333, 1000, 200, 1 / 0.7),
+    (synth.Workload("mid", 2, 8, 80, 512, 4184, ragged=True, delta_sigma=1.0, spike_rate=1e-3), None, None, None, 1.0),
+])
+def test_logprob_fwd(wl, tokens, vocab, hidden, invT):
+    c = harness.make_case(wl, 1, tokens=tokens, vocab=vocab, hidden=hidden, inv_temperature=invT)
+    ref = harness.run_oracle(c, backward=False)
+    d = harness.to_device(c)
+    b = c.batch
+    shape = rl.make_shape(b.T, b.H, b.V, 0, b.V, invT)
+    lp, ent, lse = (torch.empty(b.T, device="cuda") for _ in range(3))
+    rl.rl_logprob_fwd(shape, d["hidden"], d["w"], d["targets"], lp, ent, lse)
+    torch.cuda.synchronize()
+    assert np.max(np.abs(lp.cpu().numpy() - ref.logp)) <= harness.LOGP_TOL
+    assert np.max(np.abs(ent.cpu().numpy() - ref.entropy)) <= harness.LOGP_TOL
+    assert np.max(np.abs(lse.cpu().numpy() - ref.lse)) <= harness.LOGP_TOL
+
+
+@pytest.mark.parametrize("wl,tokens,vocab,hidden,invT", [
+    (TINY, None, None, None, 1.0),
+    (RAGGED, 333, 1000, 200, 1 / 0.7),
+    (synth.Workload("mid", 2, 8, 80, 512, 4184, ragged=True, prompt_frac=0.1, delta_sigma=1.0,
+                    spike_rate=1e-3), None, None, None, 1.0),
+])
+def test_policy_loss_step(wl, tokens, vocab, hidden, invT):
+    c = harness.make_case(wl, 2, tokens=tokens, vocab=vocab, hidden=hidden, inv_temperature=invT)
+    ref = harness.run_oracle(c)
+    gpu = harness.run_gpu_step(c)
+    err = harness.compare(c, ref, gpu)
+    print(err)
+    assert gpu["launches"] > 0
+
+
+def test_step_fp32_dh_and_accumulate():
+    c = harness.make_case(RAGGED, 3, tokens=300, vocab=1000, hidden=200)
+    ref = harness.run_oracle(c)
+    gpu = harness.run_gpu_step(c, dh_f32=True)
+    harness.compare(c, ref, gpu)
+    init = torch.from_numpy(np.random.default_rng(0).standard_normal((1000, 200)).astype(np.float32)).cuda()
+    gpu2 = harness.run_gpu_step(c, dh_f32=True, accumulate_dw=True, dw_init=init)
+    got = gpu2["d_w_vocab"] - init.cpu().numpy().astype(np.float64)
+    assert harness.rel_fro(got, ref.d_w_vocab) <= 2e-2
+
+
+def test_chunked_backward_matches():
+    c = harness.make_case(RAGGED, 4, tokens=333, vocab=1000, hidden=200)
+    ref = harness.run_oracle(c)
+    d = harness.to_device(c)
+    b = c.batch
+    T, H, V = b.T, b.H, b.V
+    shape = rl.make_shape(T, H, V, 0, V)
+    lse = torch.from_numpy(ref.lse.astype(np.float32)).cuda()
+    coef = torch.from_numpy(ref.report.coef.astype(np.float32)).cuda()
+    for chunk in (0, 128, 100):
+        dh = torch.empty(T, H, dtype=torch.bfloat16, device="cuda")
+        dw = torch.empty(V, H, device="cuda")
+        rl.rl_bwd(shape, d["hidden"], d["w"], d["targets"], lse, coef, d_hidden=dh, d_w_vocab=dw,
+                  dz_chunk_rows=chunk)
+        torch.cuda.synchronize()
+        assert harness.rel_fro(dh.float().cpu().numpy(), ref.d_hidden) <= harness.GRAD_RTOL
+        assert harness.rel_fro(dw.cpu().numpy(), ref.d_w_vocab) <= harness.GRAD_RTOL
+        # invariant: sum_v dW[v, :] = 0 (oracle gives ~1e-16); bf16 dU leaves ~1e-3
+        assert np.linalg.norm(dw.cpu().numpy().sum(0)) / np.linalg.norm(dw.cpu().numpy()) < 1e-2
+
+
+def test_determinism_bitwise():
+    c = harness.make_case(RAGGED, 5, tokens=333, vocab=1000, hidden=200)
+    g1 = harness.run_gpu_step(c)
+    g2 = harness.run_gpu_step(c)
+    for k in ("logprob", "entropy", "coef", "keep", "d_hidden", "d_w_vocab"):
+        assert np.array_equal(g1[k], g2[k]), k
+    assert g1["report"] == g2["report"]
+
+
+def test_faults_are_counted_and_neutralised():
+    def corrupt(b, infer):
+        infer[3] = np.nan
+        infer[10] = np.inf
+        infer[11] = 0.25          # positive stored log-prob
+        b.targets[20] = -1
+        b.targets[21] = b.V + 5
+    c = harness.make_case(RAGGED, 6, tokens=120, vocab=1000, hidden=64, corrupt=corrupt)
+    ref = harness.run_oracle(c)
+    gpu = harness.run_gpu_step(c)
+    assert gpu["report"]["nonfinite_inputs"] == ref.report.nonfinite_inputs > 0
+    assert gpu["report"]["bad_targets"] == ref.report.bad_targets == 2
+    ok = np.ones(c.batch.T, bool)
+    ok[[20, 21]] = False   # logprob of an out-of-range target is undefined
+    assert np.max(np.abs(gpu["logprob"][ok] - ref.logp[ok])) <= harness.LOGP_TOL
+    for t in (3, 10, 11, 20, 21):
+        assert gpu["coef"][t] == 0.0 and gpu["keep"][t] == 0
+    assert abs(gpu["report"]["loss"] - ref.report.loss) <= harness.LOSS_TOL
+
+
+def test_bad_offsets_neutralise():
+    c = harness.make_case(RAGGED, 7, tokens=120, vocab=1000, hidden=64)
+    c.batch.rollout_offsets[2], c.batch.rollout_offsets[3] = c.batch.rollout_offsets[3], c.batch.rollout_offsets[2]
+    gpu = harness.run_gpu_step(c)
+    assert gpu["report"]["bad_offsets"] == 1
+    assert not gpu["coef"].any() and gpu["report"]["loss"] == 0.0
+    assert not np.any(gpu["d_hidden"]) and not np.any(gpu["d_w_vocab"])
+
+
+def test_empty_rollouts_and_all_masked_rows():
+    def corrupt(b, infer):
+        b.rollout_offsets[1:4] = b.rollout_offsets[1]   # rollouts 1, 2 empty
+        b.loss_mask[: b.rollout_offsets[1]] = 0          # rollout 0 all prompt
+    c = harness.make_case(RAGGED, 8, tokens=200, vocab=1000, hidden=64, corrupt=corrupt)
+    ref = harness.run_oracle(c)
+    gpu = harness.run_gpu_step(c)
+    harness.compare(c, ref, gpu)
+
+
+def test_empty_batch():
+    H, V = 64, 1000
+    shape = rl.make_shape(0, H, V, 0, V)
+    params = rl.make_params(2, 1.0)
+    report = rl.new_report()
+    dw = torch.full((V, H), 7.0, device="cuda")
+    off = torch.zeros(3, dtype=torch.int32, device="cuda")
+    adv = torch.zeros(2, device="cuda")
+    w = torch.zeros(V, H, dtype=torch.bfloat16, device="cuda")
+    e = torch.empty(0, device="cuda")
+    rl.rl_policy_loss_fwd_bwd(shape, params, None, w, None, None, adv, off, None, report=report, logprob=e,
+                              d_w_vocab=dw)
+    torch.cuda.synchronize()
+    r = rl.read_report(report).as_dict()
+    assert r["loss"] == 0.0 and r["kept_tokens"] == 0 and r["bad_offsets"] == 0
+    assert not dw.any()
+
+
+def test_uniform_logits_closed_form_on_gpu():
+    """W = 0 -> logprob = -ln V and entropy = ln V exactly up to fp32."""
+    T, H, V = 300, 64, 1000
+    hidden = torch.randn(T, H, device="cuda").to(torch.bfloat16)
+    w = torch.zeros(V, H, dtype=torch.bfloat16, device="cuda")
+    tg = torch.randint(0, V, (T,), dtype=torch.int32, device="cuda")
+    lp, ent = torch.empty(T, device="cuda"), torch.empty(T, device="cuda")
+    rl.rl_logprob_fwd(rl.make_shape(T, H, V), hidden, w, tg, lp, ent)
+    torch.cuda.synchronize()
+    assert np.allclose(lp.cpu().numpy(), -np.log(V), atol=1e-5)
+    assert np.allclose(ent.cpu().numpy(), np.log(V), atol=1e-5)
+
+
+def test_vocab_parallel_split_phases_single_gpu():
+    """Emulate n vocab shards on one GPU through the split-phase ABI; the merge of
+    the shards' partials and the sum of dH partials must equal the oracle."""
+    c = harness.make_case(RAGGED, 9, tokens=333, vocab=1000, hidden=200)
+    ref = harness.run_oracle(c)
+    d = harness.to_device(c)
+    b = c.batch
+    T, H, V, R = b.T, b.H, b.V, len(c.adv)
+    cuts = [0, 256, 600, 1000]
+    parts = torch.empty(len(cuts) - 1, T, 4, device="cuda")
+    for j, (a, e) in enumerate(zip(cuts[:-1], cuts[1:])):
+        shp = rl.make_shape(T, H, e - a, a, V)
+        rl.rl_fwd_partials(shp, d["hidden"], d["w"][a:e].contiguous(), d["targets"], parts[j])
+    lp, ent, lse = (torch.empty(T, device="cuda") for _ in range(3))
+    rl.rl_merge_partials(parts, len(cuts) - 1, T, lp, ent, lse)
+    coef = torch.empty(T, device="cuda")
+    keep = torch.empty(T, dtype=torch.uint8, device="cuda")
+    guarded = torch.empty(R, dtype=torch.uint8, device="cuda")
+    report = rl.new_report()
+    params = rl.make_params(R, b.loss_denominator)
+    rl.rl_loss_coef(params, T, V, lp, d["infer"], d["targets"], d["adv"], d["offsets"], d["loss_mask"], coef,
+                    keep, guarded, report=report)
+    dh = torch.zeros(T, H, device="cuda")
+    dws = []
+    for a, e in zip(cuts[:-1], cuts[1:]):
+        shp = rl.make_shape(T, H, e - a, a, V)
+        dhp = torch.empty(T, H, device="cuda")
+        dw = torch.empty(e - a, H, device="cuda")
+        rl.rl_bwd(shp, d["hidden"], d["w"][a:e].contiguous(), d["targets"], lse, coef, d_hidden_f32=dhp,
+                  d_w_vocab=dw)
+        dh += dhp
+        dws.append(dw)
+    torch.cuda.synchronize()
+    gpu = dict(logprob=lp.cpu().numpy(), entropy=ent.cpu().numpy(), lse=lse.cpu().numpy(),
+               coef=coef.cpu().numpy(), keep=keep.cpu().numpy(), guarded=guarded.cpu().numpy(),
+               report=rl.read_report(report).as_dict(), d_hidden=dh.cpu().numpy().astype(np.float64),
+               d_w_vocab=torch.cat(dws).cpu().numpy().astype(np.float64))
+    harness.compare(c, ref, gpu)
+
+
+def test_hostio_matches_device_path():
+    c = harness.make_case(RAGGED, 10, tokens=333, vocab=1000, hidden=200)
+    gdev = harness.run_gpu_step(c)
+    b = c.batch
+    T, H, V, R = b.T, b.H, b.V, len(c.adv)
+    d = harness.to_device(c)
+    shape = rl.make_shape(T, H, V)
+    params = rl.make_params(R, b.loss_denominator)
+    report = rl.new_report()
+    dh = torch.empty(T, H, dtype=torch.bfloat16, device="cuda")
+    dw = torch.empty(V, H, device="cuda")
+    pin = lambda x: torch.from_numpy(np.ascontiguousarray(x)).pin_memory()  # noqa: E731
+    rep = rl.rl_policy_loss_fwd_bwd_hostio(
+        shape, params, b.wl.group_size, pin(b.hidden.view(np.int16)), d["w"], pin(b.targets), pin(c.infer),
+        pin(b.rewards.reshape(-1)), pin(b.rollout_offsets), pin(b.loss_mask), report=report, d_hidden=dh,
+        d_w_vocab=dw)
+    assert rep.as_dict() == gdev["report"]
+    assert np.array_equal(dh.float().cpu().numpy(), gdev["d_hidden"])
+    assert np.array_equal(dw.cpu().numpy(), gdev["d_w_vocab"])
+
+
+def test_host_validation_errors():
+    shape = rl.make_shape(10, 60, 100)   # H not a multiple of 8
+    with pytest.raises(rl.RLError) as e:
+        rl.rl_logprob_fwd(shape, torch.zeros(10, 60, dtype=torch.bfloat16, device="cuda"),
+                          torch.zeros(100, 60, dtype=torch.bfloat16, device="cuda"),
+                          torch.zeros(10, dtype=torch.int32, device="cuda"), torch.empty(10, device="cuda"))
+    assert e.value.status == 2
+    shape = rl.make_shape(10, 64, 100)
+    with pytest.raises(rl.RLError) as e:
+        rl.rl_logprob_fwd(shape, torch.zeros(10, 64, dtype=torch.bfloat16, device="cuda"),
+                          torch.zeros(100, 64, dtype=torch.bfloat16, device="cuda"),
+                          torch.zeros(10, dtype=torch.int32, device="cuda"), torch.empty(10, device="cuda"),
+                          workspace=torch.empty(16, dtype=torch.uint8, device="cuda"))
+    assert e.value.status == 5
