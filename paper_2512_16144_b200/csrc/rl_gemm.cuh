@@ -115,15 +115,17 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   const int total = sh.m_blocks * sh.n_blocks;
 
   if (warp == 0) {
-    if (lane == 0) {
-      // ----------------------------------------------------------- producer
-      int s = 0;
-      uint32_t ph = 0;
-      for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
-        int m, n;
-        tile_coords(tile, sh, m, n);
-        for (int kb = 0; kb < sh.k_blocks; ++kb) {
-          mbar_wait(&empty[s], ph ^ 1);
+    // ------------------------------------------------------------- producer
+    // The whole warp walks the schedule (warp-uniform state lives in uniform
+    // registers); one elected lane issues the TMA copies.
+    int s = 0;
+    uint32_t ph = 0;
+    for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
+      int m, n;
+      tile_coords(tile, sh, m, n);
+      for (int kb = 0; kb < sh.k_blocks; ++kb) {
+        mbar_wait_sleep(&empty[s], ph ^ 1);
+        if (elect_one()) {
           mbar_expect_tx(&full[s], A_STAGE_BYTES + B_STAGE_BYTES);
           const int k0 = kb * BK;
           uint8_t* a = sA + s * A_STAGE_BYTES;
@@ -140,30 +142,32 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 #pragma unroll
             for (int j = 0; j < 4; ++j) tma_load_2d(b + j * 8192, &tmB, &full[s], n * BN + 64 * j, k0);
           }
-          if (++s == STAGES) {
-            s = 0;
-            ph ^= 1;
-          }
+        }
+        __syncwarp();
+        if (++s == STAGES) {
+          s = 0;
+          ph ^= 1;
         }
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      // -------------------------------------------------------- MMA issuer
-      constexpr uint32_t idesc = umma_idesc_bf16(BM, BN, A_MN, B_MN);
-      int s = 0;
-      uint32_t ph = 0;
-      int acc = 0;
-      uint32_t aph = 0;
-      for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
-        mbar_wait(&tempty[acc], aph ^ 1);
+    // ----------------------------------------------------------- MMA issuer
+    constexpr uint32_t idesc = umma_idesc_bf16(BM, BN, A_MN, B_MN);
+    int s = 0;
+    uint32_t ph = 0;
+    int acc = 0;
+    uint32_t aph = 0;
+    const uint32_t a_base = smem_u32(sA), b_base = smem_u32(sB);
+    for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
+      mbar_wait(&tempty[acc], aph ^ 1);
+      tc_fence_after();
+      const uint32_t d = tmem_base + acc * BN;
+      for (int kb = 0; kb < sh.k_blocks; ++kb) {
+        mbar_wait(&full[s], ph);
         tc_fence_after();
-        const uint32_t d = tmem_base + acc * BN;
-        for (int kb = 0; kb < sh.k_blocks; ++kb) {
-          mbar_wait(&full[s], ph);
-          tc_fence_after();
-          const uint32_t a0 = smem_u32(sA + s * A_STAGE_BYTES);
-          const uint32_t b0 = smem_u32(sB + s * B_STAGE_BYTES);
+        if (elect_one()) {
+          const uint32_t a0 = a_base + s * A_STAGE_BYTES;
+          const uint32_t b0 = b_base + s * B_STAGE_BYTES;
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k) {
             const uint64_t ad = A_MN ? sw128_desc(a0 + k * 2048, 8192, 1024) : sw128_desc(a0 + k * 32, 16, 1024);
@@ -171,15 +175,17 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             umma_bf16(d, ad, bd, idesc, (kb | k) != 0);
           }
           umma_commit(&empty[s]);
-          if (++s == STAGES) {
-            s = 0;
-            ph ^= 1;
-          }
         }
-        umma_commit(&tfull[acc]);
-        acc ^= 1;
-        if (acc == 0) aph ^= 1;
+        __syncwarp();
+        if (++s == STAGES) {
+          s = 0;
+          ph ^= 1;
+        }
       }
+      if (elect_one()) umma_commit(&tfull[acc]);
+      __syncwarp();
+      acc ^= 1;
+      if (acc == 0) aph ^= 1;
     }
   } else {
     // ------------------------------------------------------------ epilogue
@@ -195,7 +201,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       const int64_t row = static_cast<int64_t>(m) * BM + r_in_tile;
       const bool row_ok = row < ep.rows;
       const int n0 = n * BN;
-      mbar_wait(&tfull[acc], aph);
+      mbar_wait_sleep(&tfull[acc], aph);
       tc_fence_after();
       const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN;
 
@@ -221,9 +227,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
               if (c * 32 + j >= nvalid) u[j] = -1e30f;
           }
           if (tl >= c * 32 && tl < c * 32 + 32) {
+            const int jt = tl - c * 32;
+            float z = -INFINITY;
 #pragma unroll
-            for (int j = 0; j < 32; ++j)
-              if (j == tl - c * 32) zt = __uint_as_float(r[j]) * ep.inv_temperature;
+            for (int j = 0; j < 32; ++j) z = fmaxf(z, (j == jt) ? __uint_as_float(r[j]) : -INFINITY);
+            zt = z * ep.inv_temperature;
           }
           float cm = u[0];
 #pragma unroll
