@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <stdarg.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <mutex>
@@ -149,34 +150,72 @@ rl_status make_map(CUtensorMap* m, const void* ptr, bool f32, int64_t inner, int
 }
 
 // ----------------------------------------------------------------- GEMMs
-constexpr int kStages = 4;
+// CTA-pair (cta_group::2, 256x256 tiles) by default; RL_CTA_GROUP=1 selects the
+// single-CTA 128x256 variant (kept for A/B measurements and as a fallback).
+int cta_group() {
+  static int cg = [] {
+    const char* e = getenv("RL_CTA_GROUP");
+    return (e && atoi(e) == 1) ? 1 : 2;
+  }();
+  return cg;
+}
 
-template <int MODE, bool A_MN, bool B_MN>
-rl_status launch_gemm(int kid, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c, int64_t M, int64_t N,
-                      int64_t K, int group_m, const rl::EpiParams& ep, int sms, cudaStream_t st) {
-  if (M <= 0 || N <= 0) return RL_OK;
-  auto kern = rl::gemm_kernel<MODE, A_MN, B_MN, kStages>;
-  constexpr int smem = rl::gemm_smem_bytes<kStages>();
+template <int CG>
+constexpr int stages_for() {
+  return CG == 2 ? 6 : 4;
+}
+
+template <int MODE, bool A_MN, bool B_MN, int CG>
+rl_status launch_gemm_cg(int kid, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c, int64_t M,
+                         int64_t N, int64_t K, int group_m, const rl::EpiParams& ep, int sms, cudaStream_t st) {
+  constexpr int S = stages_for<CG>();
+  auto kern = rl::gemm_kernel<MODE, A_MN, B_MN, CG, S>;
+  constexpr int smem = rl::gemm_smem_bytes<CG, S>();
   static bool attr_set = false;  // per instantiation
   if (!attr_set) {
     RL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     attr_set = true;
   }
+  using TL = rl::Tiling<CG>;
   rl::GemmShape sh;
-  sh.m_blocks = static_cast<int>((M + rl::BM - 1) / rl::BM);
+  sh.m_blocks = static_cast<int>((M + TL::TILE_M - 1) / TL::TILE_M);
   sh.n_blocks = static_cast<int>((N + rl::BN - 1) / rl::BN);
   sh.k_blocks = static_cast<int>((K + rl::BK - 1) / rl::BK);
   sh.group_m = group_m;
   if (sh.k_blocks == 0) return fail(RL_ERR_SHAPE, "GEMM with K = 0");
   const int64_t tiles = static_cast<int64_t>(sh.m_blocks) * sh.n_blocks;
-  const int grid = static_cast<int>(tiles < sms ? tiles : sms);
+  const int units = static_cast<int>(tiles < sms / CG ? tiles : sms / CG);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(units * CG);
+  cfg.blockDim = dim3(rl::GEMM_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CG;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
   {
     ProfScope ps(kid, st);
-    kern<<<grid, rl::GEMM_THREADS, smem, st>>>(a, b, c, sh, ep);
+    RL_CUDA(cudaLaunchKernelEx(&cfg, kern, a, b, c, sh, ep));
   }
   RL_CHECK_LAUNCH();
   return RL_OK;
 }
+
+template <int MODE, bool A_MN, bool B_MN>
+rl_status launch_gemm(int kid, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c, int64_t M, int64_t N,
+                      int64_t K, int group_m, const rl::EpiParams& ep, int sms, cudaStream_t st) {
+  if (M <= 0 || N <= 0) return RL_OK;
+  if (cta_group() == 2)
+    return launch_gemm_cg<MODE, A_MN, B_MN, 2>(kid, a, b, c, M, N, K, group_m, ep, sms, st);
+  return launch_gemm_cg<MODE, A_MN, B_MN, 1>(kid, a, b, c, M, N, K, group_m, ep, sms, st);
+}
+
+// Rows of A staged per CTA per tile (the TMA box height for A loads).
+constexpr int kARows = 128;
 
 // ------------------------------------------------------------ workspace
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
@@ -257,8 +296,8 @@ rl_status forward_impl(const rl_lm_shape* s, const uint16_t* hidden, const uint1
   const int64_t T = s->T;
   if (T == 0) return RL_OK;
   CUtensorMap ta, tb;
-  RL_TRY(make_map(&ta, hidden, false, s->H, T, s->H, 64, rl::BM));
-  RL_TRY(make_map(&tb, w, false, s->H, s->V_local, s->H, 64, rl::BN));
+  RL_TRY(make_map(&ta, hidden, false, s->H, T, s->H, 64, kARows));
+  RL_TRY(make_map(&tb, w, false, s->H, s->V_local, s->H, 64, rl::BN / cta_group()));
   rl::EpiParams ep = {};
   ep.rows = T;
   ep.cols = s->V_local;
@@ -326,13 +365,13 @@ rl_status bwd_impl(const rl_lm_shape* s, const uint16_t* hidden, const uint16_t*
   uint16_t* dz = reinterpret_cast<uint16_t*>(ws + L.dz);
   const int64_t chunk = L.chunk;
   CUtensorMap t_h_k, t_w_k, t_dz_st, t_dz_k, t_w_mn, t_dh, t_dz_mn, t_h_mn, t_dw;
-  RL_TRY(make_map(&t_w_k, w, false, H, V, H, 64, rl::BN));
+  RL_TRY(make_map(&t_w_k, w, false, H, V, H, 64, rl::BN / cta_group()));
   RL_TRY(make_map(&t_w_mn, w, false, H, V, H, 64, 64));
   if (dw) RL_TRY(make_map(&t_dw, dw, true, H, V, H, 32, 32));
   for (int64_t c0 = 0; c0 < T; c0 += chunk) {
     const int64_t rows = (T - c0 < chunk) ? (T - c0) : chunk;
     const uint16_t* hc = hidden + c0 * H;
-    RL_TRY(make_map(&t_h_k, hc, false, H, rows, H, 64, rl::BM));
+    RL_TRY(make_map(&t_h_k, hc, false, H, rows, H, 64, kARows));
     RL_TRY(make_map(&t_dz_st, dz, false, V, rows, L.ldz, 64, 32));
     // K4: dU chunk = coef invT (softmax - onehot), bf16
     rl::EpiParams ep = {};
@@ -347,7 +386,7 @@ rl_status bwd_impl(const rl_lm_shape* s, const uint16_t* hidden, const uint16_t*
     RL_TRY((launch_gemm<rl::EPI_DZ, false, false>(RL_K_DZ_GEMM, t_h_k, t_w_k, t_dz_st, rows, V, H, 16, ep, sms, st)));
     // K5: dH chunk = dU W
     if (dh || dh32) {
-      RL_TRY(make_map(&t_dz_k, dz, false, V, rows, L.ldz, 64, rl::BM));
+      RL_TRY(make_map(&t_dz_k, dz, false, V, rows, L.ldz, 64, kARows));
       rl::EpiParams e5 = {};
       e5.rows = rows;
       e5.cols = H;

@@ -2,10 +2,16 @@
 //
 //   D[m, n] = sum_k A[m, k] * B[n, k]      (bf16 in, fp32 accumulate in TMEM)
 //
-// One CTA per SM, 128x256 output tiles, BK = 64, a STAGES-deep TMA->SMEM ring,
-// two TMEM accumulators (2 x 256 columns) so the epilogue of tile i overlaps the
-// MMAs of tile i+1. Warp roles: warp 0 = TMA producer (one thread), warp 1 =
-// TMEM owner + MMA issuer (one thread), warps 2..5 = epilogue (thread = row).
+// CG = 1: one CTA per SM computes 128 x 256 tiles.
+// CG = 2: a CTA pair (cluster of 2 on one TPC) computes 256 x 256 tiles with
+//         tcgen05.mma.cta_group::2: each CTA stages half of A (128 rows) and half
+//         of B (128 rows) per k-block and holds 128 rows x 256 fp32 columns of D in
+//         its own TMEM; the leader CTA issues the MMAs. Per SM this moves 2/3 of
+//         the operand bytes of CG = 1 for the same FLOPs.
+// BK = 64 (one 128-byte swizzle atom of bf16), a STAGES-deep TMA ring, two TMEM
+// accumulators (2 x 256 columns) so the epilogue of tile i overlaps the MMAs of
+// tile i+1. Warp roles: warp 0 = TMA producer, warp 1 = TMEM owner + MMA issuer
+// (leader CTA), warps 2..5 = epilogue (thread = accumulator row).
 //
 // Epilogues:
 //   EPI_LSE  (K1): per row of the tile, online (m, s, u, z_target) over the
@@ -19,24 +25,32 @@
 
 namespace rl {
 
-constexpr int BM = 128, BN = 256, BK = 64;
+constexpr int BN = 256, BK = 64;
 constexpr int GEMM_THREADS = 192;
-constexpr int A_STAGE_BYTES = BM * BK * 2;  // 16 KB
-constexpr int B_STAGE_BYTES = BN * BK * 2;  // 32 KB
-constexpr int EPI_BUF_BYTES = 32 * 128;     // one warp's 32-row x 128-byte store chunk
+constexpr int EPI_BUF_BYTES = 32 * 128;  // one warp's 32-row x 128-byte store chunk
 constexpr int EPI_BYTES = 4 * 2 * EPI_BUF_BYTES;
 constexpr int BAR_BYTES = 256;
 
 enum EpiMode { EPI_LSE = 0, EPI_DZ = 1, EPI_BF16 = 2, EPI_F32 = 3, EPI_F32_ADD = 4 };
 
-template <int STAGES>
+template <int CG>
+struct Tiling {
+  static constexpr int TILE_M = 128 * CG;          // output rows per tile (per CTA pair)
+  static constexpr int A_ROWS = 128;               // A rows staged per CTA
+  static constexpr int B_ROWS = BN / CG;           // B rows (n) staged per CTA
+  static constexpr int A_STAGE = A_ROWS * BK * 2;  // bytes per stage per CTA
+  static constexpr int B_STAGE = B_ROWS * BK * 2;
+  static constexpr int STAGE = A_STAGE + B_STAGE;
+};
+
+template <int CG, int STAGES>
 constexpr int gemm_smem_bytes() {
-  return 1024 + STAGES * (A_STAGE_BYTES + B_STAGE_BYTES) + EPI_BYTES + BAR_BYTES;
+  return 1024 + STAGES * Tiling<CG>::STAGE + EPI_BYTES + BAR_BYTES;
 }
 
 struct GemmShape {
-  int m_blocks, n_blocks, k_blocks;
-  int group_m;  // raster: tiles walk n inside groups of group_m m-blocks
+  int m_blocks, n_blocks, k_blocks;  // m_blocks counts TILE_M-row tiles
+  int group_m;                       // raster: tiles walk n inside groups of group_m m-blocks
 };
 
 struct EpiParams {
@@ -63,23 +77,24 @@ __device__ __forceinline__ void tile_coords(int tile, const GemmShape& sh, int& 
 }
 
 // Write one thread's 128-byte row chunk into a 128B-swizzled 32-row staging buffer.
-__device__ __forceinline__ void stage_row(uint32_t buf, int row, const uint32_t (&w)[32], int base) {
+__device__ __forceinline__ void stage_row(uint32_t buf, int row, const uint32_t (&w)[32]) {
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
     const uint32_t addr = buf + row * 128 + ((j ^ (row & 7)) << 4);
-    st_shared_v4(addr, w[base + 4 * j], w[base + 4 * j + 1], w[base + 4 * j + 2], w[base + 4 * j + 3]);
+    st_shared_v4(addr, w[4 * j], w[4 * j + 1], w[4 * j + 2], w[4 * j + 3]);
   }
 }
 
-template <int MODE, bool A_MN, bool B_MN, int STAGES>
+template <int MODE, bool A_MN, bool B_MN, int CG, int STAGES>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const __grid_constant__ CUtensorMap tmC, const GemmShape sh, const EpiParams ep) {
+  using TL = Tiling<CG>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
-  uint8_t* sB = sA + STAGES * A_STAGE_BYTES;
-  uint8_t* sEpi = sB + STAGES * B_STAGE_BYTES;
+  uint8_t* sB = sA + STAGES * TL::A_STAGE;
+  uint8_t* sEpi = sB + STAGES * TL::B_STAGE;
   uint64_t* full = reinterpret_cast<uint64_t*>(sEpi + EPI_BYTES);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
@@ -88,6 +103,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  const uint32_t rank = (CG == 2) ? cluster_ctarank() : 0u;
+  const bool leader = rank == 0;
+  const int unit = blockIdx.x / CG;  // CTA pair (or CTA) index
+  const int n_units = gridDim.x / CG;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -96,7 +115,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 4);
+      mbar_init(&tempty[a], 4 * CG);
     }
     fence_mbar_init();
     tma_prefetch(&tmA);
@@ -104,11 +123,19 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     if (MODE != EPI_LSE) tma_prefetch(&tmC);
   }
   if (warp == 1) {
-    tmem_alloc(tmem_slot, 512);
-    tmem_relinquish();
+    if constexpr (CG == 2) {
+      tmem_alloc2(tmem_slot, 512);
+      tmem_relinquish2();
+    } else {
+      tmem_alloc(tmem_slot, 512);
+      tmem_relinquish();
+    }
   }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CG == 2)
+    cluster_sync();
+  else
+    __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
@@ -120,27 +147,46 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     // registers); one elected lane issues the TMA copies.
     int s = 0;
     uint32_t ph = 0;
-    for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
+    for (int tile = unit; tile < total; tile += n_units) {
       int m, n;
       tile_coords(tile, sh, m, n);
+      const int a_row = m * TL::TILE_M + rank * TL::A_ROWS;
+      const int b_row = n * BN + rank * TL::B_ROWS;
       for (int kb = 0; kb < sh.k_blocks; ++kb) {
         mbar_wait_sleep(&empty[s], ph ^ 1);
         if (elect_one()) {
-          mbar_expect_tx(&full[s], A_STAGE_BYTES + B_STAGE_BYTES);
+          if (leader) mbar_expect_tx(&full[s], CG * TL::STAGE);
           const int k0 = kb * BK;
-          uint8_t* a = sA + s * A_STAGE_BYTES;
-          uint8_t* b = sB + s * B_STAGE_BYTES;
-          if (!A_MN) {
-            tma_load_2d(a, &tmA, &full[s], k0, m * BM);
-          } else {
-            tma_load_2d(a, &tmA, &full[s], m * BM, k0);
-            tma_load_2d(a + 8192, &tmA, &full[s], m * BM + 64, k0);
-          }
-          if (!B_MN) {
-            tma_load_2d(b, &tmB, &full[s], k0, n * BN);
-          } else {
+          uint8_t* a = sA + s * TL::A_STAGE;
+          uint8_t* b = sB + s * TL::B_STAGE;
+          if constexpr (CG == 2) {
+            if (!A_MN) {
+              tma_load_2d_pair(a, &tmA, &full[s], k0, a_row);
+            } else {
+              tma_load_2d_pair(a, &tmA, &full[s], a_row, k0);
+              tma_load_2d_pair(a + 8192, &tmA, &full[s], a_row + 64, k0);
+            }
+            if (!B_MN) {
+              tma_load_2d_pair(b, &tmB, &full[s], k0, b_row);
+            } else {
 #pragma unroll
-            for (int j = 0; j < 4; ++j) tma_load_2d(b + j * 8192, &tmB, &full[s], n * BN + 64 * j, k0);
+              for (int j = 0; j < TL::B_ROWS / 64; ++j)
+                tma_load_2d_pair(b + j * 8192, &tmB, &full[s], b_row + 64 * j, k0);
+            }
+          } else {
+            if (!A_MN) {
+              tma_load_2d(a, &tmA, &full[s], k0, a_row);
+            } else {
+              tma_load_2d(a, &tmA, &full[s], a_row, k0);
+              tma_load_2d(a + 8192, &tmA, &full[s], a_row + 64, k0);
+            }
+            if (!B_MN) {
+              tma_load_2d(b, &tmB, &full[s], k0, b_row);
+            } else {
+#pragma unroll
+              for (int j = 0; j < TL::B_ROWS / 64; ++j)
+                tma_load_2d(b + j * 8192, &tmB, &full[s], b_row + 64 * j, k0);
+            }
           }
         }
         __syncwarp();
@@ -152,53 +198,77 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     }
   } else if (warp == 1) {
     // ----------------------------------------------------------- MMA issuer
-    constexpr uint32_t idesc = umma_idesc_bf16(BM, BN, A_MN, B_MN);
-    int s = 0;
-    uint32_t ph = 0;
-    int acc = 0;
-    uint32_t aph = 0;
-    const uint32_t a_base = smem_u32(sA), b_base = smem_u32(sB);
-    for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
-      mbar_wait(&tempty[acc], aph ^ 1);
-      tc_fence_after();
-      const uint32_t d = tmem_base + acc * BN;
-      for (int kb = 0; kb < sh.k_blocks; ++kb) {
-        mbar_wait(&full[s], ph);
+    if (leader) {
+      constexpr uint32_t idesc = umma_idesc_bf16(TL::TILE_M, BN, A_MN, B_MN);
+      int s = 0;
+      uint32_t ph = 0;
+      int acc = 0;
+      uint32_t aph = 0;
+      const uint32_t a_base = smem_u32(sA), b_base = smem_u32(sB);
+      for (int tile = unit; tile < total; tile += n_units) {
+        mbar_wait(&tempty[acc], aph ^ 1);
         tc_fence_after();
-        if (elect_one()) {
-          const uint32_t a0 = a_base + s * A_STAGE_BYTES;
-          const uint32_t b0 = b_base + s * B_STAGE_BYTES;
+        const uint32_t d = tmem_base + acc * BN;
+        for (int kb = 0; kb < sh.k_blocks; ++kb) {
+          mbar_wait(&full[s], ph);
+          tc_fence_after();
+          if (elect_one()) {
+            const uint32_t a0 = a_base + s * TL::A_STAGE;
+            const uint32_t b0 = b_base + s * TL::B_STAGE;
 #pragma unroll
-          for (int k = 0; k < BK / 16; ++k) {
-            const uint64_t ad = A_MN ? sw128_desc(a0 + k * 2048, 8192, 1024) : sw128_desc(a0 + k * 32, 16, 1024);
-            const uint64_t bd = B_MN ? sw128_desc(b0 + k * 2048, 8192, 1024) : sw128_desc(b0 + k * 32, 16, 1024);
-            umma_bf16(d, ad, bd, idesc, (kb | k) != 0);
+            for (int k = 0; k < BK / 16; ++k) {
+              const uint64_t ad = A_MN ? sw128_desc(a0 + k * 2048, 8192, 1024) : sw128_desc(a0 + k * 32, 16, 1024);
+              const uint64_t bd = B_MN ? sw128_desc(b0 + k * 2048, 8192, 1024) : sw128_desc(b0 + k * 32, 16, 1024);
+              if constexpr (CG == 2)
+                umma_bf16_pair(d, ad, bd, idesc, (kb | k) != 0);
+              else
+                umma_bf16(d, ad, bd, idesc, (kb | k) != 0);
+            }
+            if constexpr (CG == 2)
+              umma_commit_pair(&empty[s], 0x3);
+            else
+              umma_commit(&empty[s]);
           }
-          umma_commit(&empty[s]);
+          __syncwarp();
+          if (++s == STAGES) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+        if (elect_one()) {
+          if constexpr (CG == 2)
+            umma_commit_pair(&tfull[acc], 0x3);
+          else
+            umma_commit(&tfull[acc]);
         }
         __syncwarp();
-        if (++s == STAGES) {
-          s = 0;
-          ph ^= 1;
-        }
+        acc ^= 1;
+        if (acc == 0) aph ^= 1;
       }
-      if (elect_one()) umma_commit(&tfull[acc]);
-      __syncwarp();
-      acc ^= 1;
-      if (acc == 0) aph ^= 1;
     }
   } else {
     // ------------------------------------------------------------ epilogue
     const int q = warp & 3;  // TMEM lane quarter this warp may access
-    const int r_in_tile = q * 32 + lane;
+    const int r_in_tile = rank * 128 + q * 32 + lane;
     const uint32_t buf0 = smem_u32(sEpi + (warp - 2) * 2 * EPI_BUF_BYTES);
+    const uint32_t tempty_leader0 = (CG == 2) ? mapa_shared(smem_u32(&tempty[0]), 0) : 0u;
     int acc = 0;
     uint32_t aph = 0;
     int chunk_ctr = 0;
-    for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
+    auto release_tmem = [&](int a) {
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        if constexpr (CG == 2)
+          mbar_arrive_cluster(tempty_leader0 + a * 8);
+        else
+          mbar_arrive(&tempty[a]);
+      }
+    };
+    for (int tile = unit; tile < total; tile += n_units) {
       int m, n;
       tile_coords(tile, sh, m, n);
-      const int64_t row = static_cast<int64_t>(m) * BM + r_in_tile;
+      const int64_t row = static_cast<int64_t>(m) * TL::TILE_M + r_in_tile;
       const bool row_ok = row < ep.rows;
       const int n0 = n * BN;
       mbar_wait_sleep(&tfull[acc], aph);
@@ -218,6 +288,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           uint32_t r[32];
           tmem_ld32(taddr + c * 32, r);
           tmem_wait_ld();
+          if (c == BN / 32 - 1) release_tmem(acc);
           float u[32];
 #pragma unroll
           for (int j = 0; j < 32; ++j) u[j] = __uint_as_float(r[j]) * ep.scale_log2;
@@ -249,9 +320,6 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             trun = fmaf(e, d, trun);
           }
         }
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&tempty[acc]);
         if (row_ok) {
           constexpr float LN2 = 0.69314718055994530942f;
           ep.partials[static_cast<int64_t>(n) * ep.rows + row] = make_float4(mrun * LN2, srun, trun * LN2, zt);
@@ -278,11 +346,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             tmem_ld32(taddr + c * 64, r0);
             tmem_ld32(taddr + c * 64 + 32, r1);
             tmem_wait_ld();
-            if (c == BN / COLS - 1) {
-              tc_fence_before();
-              __syncwarp();
-              if (lane == 0) mbar_arrive(&tempty[acc]);
-            }
+            if (c == BN / COLS - 1) release_tmem(acc);
 #pragma unroll
             for (int j = 0; j < 16; ++j) {
               float v0 = __uint_as_float(r0[2 * j]), v1 = __uint_as_float(r0[2 * j + 1]);
@@ -305,23 +369,19 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             uint32_t r0[32];
             tmem_ld32(taddr + c * 32, r0);
             tmem_wait_ld();
-            if (c == BN / COLS - 1) {
-              tc_fence_before();
-              __syncwarp();
-              if (lane == 0) mbar_arrive(&tempty[acc]);
-            }
+            if (c == BN / COLS - 1) release_tmem(acc);
 #pragma unroll
             for (int j = 0; j < 32; ++j) w[j] = r0[j];
           }
           const uint32_t buf = buf0 + (chunk_ctr & 1) * EPI_BUF_BYTES;
           if (lane == 0) bulk_wait_read<1>();
           __syncwarp();
-          stage_row(buf, lane, w, 0);
+          stage_row(buf, lane, w);
           fence_async_smem();
           __syncwarp();
           if (lane == 0) {
             const int c0 = n0 + c * COLS;
-            const int c1 = m * BM + q * 32;
+            const int c1 = m * TL::TILE_M + rank * 128 + q * 32;
             if constexpr (MODE == EPI_F32_ADD)
               tma_reduce_add_2d(&tmC, sEpi + (buf - smem_u32(sEpi)), c0, c1);
             else
@@ -336,10 +396,17 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     }
     if (lane == 0) bulk_wait_all();
   }
-  __syncthreads();
+  tc_fence_before();
+  if constexpr (CG == 2)
+    cluster_sync();
+  else
+    __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc(tmem_base, 512);
+    if constexpr (CG == 2)
+      tmem_dealloc2(tmem_base, 512);
+    else
+      tmem_dealloc(tmem_base, 512);
   }
 }
 
