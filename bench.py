@@ -217,12 +217,13 @@ def main_ours(args):
     vocab_par = name == "glm64k" and world > 1
     mode = "vocab" if vocab_par else "dp"
     H, Vt = wl.hidden, wl.vocab
-    T = wl.tokens if (vocab_par or world == 1 or name != "stress") else wl.tokens // wl.n_ranks
     if name == "stress":
-        T = wl.tokens // wl.n_ranks          # 16k tokens per rank, one group per rank
-        wl_rank = synth.Workload("stress-rank", 1, wl.group_size, wl.rollout_len, H, Vt, delta_sigma=wl.delta_sigma,
-                                 spike_rate=wl.spike_rate)
+        # 16k tokens and one G=16 prompt group per rank (the guard and advantages stay local)
+        T = wl.tokens // wl.n_ranks
+        wl_rank = synth.Workload("stress-rank", 1, wl.group_size, wl.rollout_len, H, Vt,
+                                 delta_sigma=wl.delta_sigma, spike_rate=wl.spike_rate)
     else:
+        T = wl.tokens
         wl_rank = wl
     if vocab_par:
         assert Vt % world == 0
@@ -263,50 +264,46 @@ def main_ours(args):
     infer = torch.where(b["spikes"], torch.zeros_like(infer), infer).contiguous()
     del logp_ref
 
+    from paper_2512_16144_b200 import parallel
+    phases = parallel.LibrlPhases()
     adv = torch.empty(R, **f32)
     report = rl.new_report(dev)
     logprob = torch.empty(T, **f32)
     lse = torch.empty(T, **f32)
     coef = torch.empty(T, **f32)
     dw = torch.empty(V_local, H, **f32)
-    chunk = 16384 if T > 16384 else 0
+    # dU in 16k-row chunks: keeps K5/K6's per-wave working set inside L2 (the K = T
+    # reduction of K6 at 64k rows loses ~20% to HBM re-reads otherwise)
+    chunk = 0 if T <= 16384 else 16384
     if vocab_par:
-        ws = rl.alloc_workspace(rl.rl_workspace_bytes(shape, R, chunk), dev)
-        parts = torch.empty(world, T, 4, **f32)
-        dh = torch.empty(T, H, **f32)
-        lossws = rl.alloc_workspace(48 * R, dev)
+        engine = parallel.VocabParallelPolicyLoss(phases, T=T, H=H, V_global=Vt, num_rollouts=R,
+                                                  group_size=wl_rank.group_size, loss_denominator=D,
+                                                  dz_chunk_rows=chunk, device=dev)
+        ws = engine.ws
+        dh = engine.d_hidden
+    elif world > 1:
+        engine = parallel.DataParallelPolicyLoss(phases, T=T, H=H, V=Vt, num_rollouts=R,
+                                                 group_size=wl_rank.group_size, loss_denominator=D, device=dev)
+        ws = engine.ws
+        dh = engine.d_hidden
     else:
+        engine = None
         ws = rl.alloc_workspace(rl.rl_workspace_bytes(shape, R, chunk), dev)
         dh = torch.empty(T, H, dtype=torch.bfloat16, device=dev)
     torch.cuda.synchronize()
 
     launches = [0]
+    hidden, w_loc = b["hidden"], b["w"]
 
     def step():
-        n = 0
-        rl.rl_group_advantages(rewards, wl_rank.group_size, adv)
-        n += rl.rl_last_launch_count()
-        if vocab_par:
-            rl.rl_fwd_partials(shape, b["hidden"], b["w"], targets, parts[rank], workspace=ws)
-            n += rl.rl_last_launch_count()
-            dist.all_gather_into_tensor(parts, parts[rank].contiguous())
-            rl.rl_merge_partials(parts, world, T, logprob, None, lse)
-            n += rl.rl_last_launch_count()
-            rl.rl_loss_coef(params, T, Vt, logprob, infer, targets, adv, offsets, loss_mask, coef, report=report,
-                            workspace=lossws)
-            n += rl.rl_last_launch_count()
-            rl.rl_bwd(shape, b["hidden"], b["w"], targets, lse, coef, d_hidden_f32=dh, d_w_vocab=dw,
-                      dz_chunk_rows=chunk, workspace=ws)
-            n += rl.rl_last_launch_count()
-            dist.all_reduce(dh)
+        phases.launches = 0
+        if engine is not None:
+            engine.step(hidden, w_loc, targets, infer, rewards, offsets, loss_mask, dw)
         else:
-            rl.rl_policy_loss_fwd_bwd(shape, params, b["hidden"], b["w"], targets, infer, adv, offsets, loss_mask,
-                                      report=report, logprob=logprob, lse=lse, coef=coef, d_hidden=dh,
-                                      d_w_vocab=dw, workspace=ws)
-            n += rl.rl_last_launch_count()
-            if world > 1:
-                dist.all_reduce(dw)
-        launches[0] = n
+            phases.group_advantages(rewards, wl_rank.group_size, adv)
+            phases.full_step(shape, params, hidden, w_loc, targets, infer, adv, offsets, loss_mask, report=report,
+                             logprob=logprob, lse=lse, coef=coef, d_hidden=dh, d_w_vocab=dw, workspace=ws)
+        launches[0] = phases.launches
 
     for _ in range(args.warmup):
         step()
@@ -378,6 +375,8 @@ def main_ours(args):
         opin = torch.from_numpy(b["offsets"]).pin_memory()
         mpin = torch.from_numpy(b["loss_mask"]).pin_memory()
         del ws
+        if engine is not None:
+            engine.ws = None
         wsh = rl.alloc_workspace(rl.rl_workspace_bytes_hostio(shape, R), dev)
 
         def hstep():

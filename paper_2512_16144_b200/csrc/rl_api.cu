@@ -518,8 +518,8 @@ rl_status rl_logprob_fwd(const rl_lm_shape* shape, const uint16_t* hidden, const
       return fail(RL_ERR_ALIGNMENT, "hidden, w_vocab and workspace must be 16-byte aligned");
   }
   const WsLayout L = ws_layout(shape, 1, 0);
-  if (shape->T > 0 && (!workspace || workspace_bytes < L.end))
-    return fail(RL_ERR_WORKSPACE, "workspace needs %zu bytes, got %zu", L.end, workspace_bytes);
+  if (shape->T > 0 && (!workspace || workspace_bytes < L.dz))
+    return fail(RL_ERR_WORKSPACE, "workspace needs %zu bytes, got %zu", L.dz, workspace_bytes);
   DevInfo d;
   RL_TRY(device_info(d));
   return forward_impl(shape, hidden, w_vocab, targets, logprob, entropy, lse, nullptr,
@@ -540,8 +540,8 @@ rl_status rl_fwd_partials(const rl_lm_shape* shape, const uint16_t* hidden, cons
       return fail(RL_ERR_ALIGNMENT, "hidden, w_vocab, partials and workspace must be 16-byte aligned");
   }
   const WsLayout L = ws_layout(shape, 1, 0);
-  if (shape->T > 0 && (!workspace || workspace_bytes < L.end))
-    return fail(RL_ERR_WORKSPACE, "workspace needs %zu bytes, got %zu", L.end, workspace_bytes);
+  if (shape->T > 0 && (!workspace || workspace_bytes < L.dz))
+    return fail(RL_ERR_WORKSPACE, "workspace needs %zu bytes, got %zu", L.dz, workspace_bytes);
   DevInfo d;
   RL_TRY(device_info(d));
   return forward_impl(shape, hidden, w_vocab, targets, nullptr, nullptr, nullptr, reinterpret_cast<float4*>(partials),

@@ -1,0 +1,174 @@
+"""Multi-process (world size 2, gloo, CPU) checks of the N > 1 host logic in
+paper_2512_16144_b200/parallel.py: vocab sharding, rank-ordered partial gather
+and merge, redundant S3, dH partial reduction, DP with a global denominator and
+the dW reduction. The arithmetic is supplied by `OraclePhases`, a test double
+built from the fp64 oracle, so the composition is checked on any machine; the
+GPU path runs the same classes with librl's phases (bench.py, N > 1)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import oracle
+import synth
+from paper_2512_16144_b200 import parallel
+
+WORLD = 2
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+class OraclePhases:
+    """librl's split-phase signatures implemented with oracle functions (CPU)."""
+
+    def group_advantages(self, rewards, G, adv):
+        adv.copy_(torch.from_numpy(oracle.group_advantages(rewards.double().numpy().reshape(-1, G)).reshape(-1)))
+
+    def fwd_partials(self, shape, hidden, w_shard, targets, partials, workspace=None):
+        Z = oracle.lm_logits(hidden.double().numpy(), w_shard.double().numpy(), shape.inv_temperature)
+        m, s, u, zt = oracle.shard_stats(Z, targets.long().numpy(), shape.vocab_offset)
+        partials.copy_(torch.from_numpy(np.stack([m, s, u, zt], axis=1)))
+
+    def merge_partials(self, parts, n_parts, T, logprob, entropy, lse):
+        p = parts.double().numpy()
+        l, e, zt = oracle.merge_shard_stats([tuple(p[j, :, c] for c in range(4)) for j in range(n_parts)])
+        logprob.copy_(torch.from_numpy(zt - l))
+        entropy.copy_(torch.from_numpy(e))
+        lse.copy_(torch.from_numpy(l))
+
+    def loss_coef(self, params, T, V_global, logprob, infer, targets, adv, offsets, loss_mask, coef, keep, guarded,
+                  report, workspace=None):
+        rep = oracle.icepop_loss(logprob.double().numpy(), infer.double().numpy(), adv.double().numpy(),
+                                 offsets.numpy(), loss_mask.numpy(), params.alpha, params.beta,
+                                 params.guard_threshold, params.loss_denominator, targets.long().numpy(), V_global)
+        coef.copy_(torch.from_numpy(rep.coef))
+        keep.copy_(torch.from_numpy(rep.keep.astype(np.uint8)))
+        guarded.copy_(torch.from_numpy(rep.guarded.astype(np.uint8)))
+        self.loss = rep.loss
+
+    def bwd(self, shape, hidden, w_shard, targets, lse, coef, d_hidden_f32, d_w_vocab, dz_chunk_rows=0,
+            workspace=None):
+        h, W = hidden.double().numpy(), w_shard.double().numpy()
+        invT = shape.inv_temperature
+        Z = oracle.lm_logits(h, W, invT)
+        P = np.exp(Z - lse.double().numpy()[:, None])
+        local = targets.long().numpy() - shape.vocab_offset
+        inside = (local >= 0) & (local < W.shape[0])
+        P[np.nonzero(inside)[0], local[inside]] -= 1.0
+        dU = (coef.double().numpy() * invT)[:, None] * P
+        d_hidden_f32.copy_(torch.from_numpy(dU @ W))
+        d_w_vocab.copy_(torch.from_numpy(dU.T @ h))
+
+    def full_step(self, shape, params, hidden, w, targets, infer, adv, offsets, loss_mask, *, report, logprob,
+                  entropy=None, lse=None, coef=None, keep=None, guarded=None, d_hidden=None, d_w_vocab=None,
+                  workspace=None):
+        res = oracle.policy_loss_fwd_bwd(hidden.double().numpy(), w.double().numpy(), targets.long().numpy(),
+                                         infer.double().numpy(), None, offsets.numpy(), loss_mask.numpy(),
+                                         alpha=params.alpha, beta=params.beta,
+                                         guard_threshold=params.guard_threshold,
+                                         loss_denominator=params.loss_denominator,
+                                         inv_temperature=shape.inv_temperature, rollout_adv=adv.double().numpy())
+        logprob.copy_(torch.from_numpy(res.logp))
+        d_hidden.copy_(torch.from_numpy(res.d_hidden))
+        d_w_vocab.copy_(torch.from_numpy(res.d_w_vocab))
+        self.loss = res.report.loss
+
+
+WL = synth.Workload("dist", 2, 4, 12, 32, 96, ragged=True, prompt_frac=0.2, delta_sigma=0.8, spike_rate=0.02)
+
+
+def _batch():
+    b = synth.make_batch(WL, 11)
+    h64, w64 = oracle.bf16_to_f64(b.hidden), oracle.bf16_to_f64(b.w_vocab)
+    lp, _, _ = oracle.log_softmax_stats(oracle.lm_logits(h64, w64), b.targets)
+    infer = synth.compose_infer_logprobs(lp, b.delta_noise, b.spikes)
+    return b, h64, w64, infer
+
+
+def _bf16(bits):
+    return torch.from_numpy(bits.view(np.int16).copy()).view(torch.bfloat16)
+
+
+def _vocab_worker(rank, port, out_dir):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=WORLD)
+    b, h64, w64, infer = _batch()
+    vp = parallel.VocabParallelPolicyLoss(OraclePhases(), T=b.T, H=b.H, V_global=b.V, num_rollouts=len(b.rewards.reshape(-1)),
+                                          group_size=WL.group_size, loss_denominator=b.loss_denominator,
+                                          device="cpu", workspace=False)
+    lo, hi = vp.vocab_offset, vp.vocab_offset + vp.V_local
+    dw = torch.empty(vp.V_local, b.H, dtype=torch.float64)
+    for name in ("parts", "d_hidden", "logprob", "entropy", "lse", "coef", "adv"):
+        setattr(vp, name, getattr(vp, name).double())
+    dh = vp.step(_bf16(b.hidden), _bf16(b.w_vocab[lo:hi]), torch.from_numpy(b.targets), torch.from_numpy(infer),
+                 torch.from_numpy(b.rewards.reshape(-1)), torch.from_numpy(b.rollout_offsets),
+                 torch.from_numpy(b.loss_mask), dw)
+    np.savez(os.path.join(out_dir, f"vp{rank}.npz"), dh=dh.numpy(), dw=dw.numpy(), logprob=vp.logprob.numpy(),
+             coef=vp.coef.numpy(), lo=lo, hi=hi)
+    dist.destroy_process_group()
+
+
+def _dp_worker(rank, port, out_dir):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=WORLD)
+    b, h64, w64, infer = _batch()
+    # rank r takes prompt group r (whole rollouts, so the guard stays local)
+    G = WL.group_size
+    r0, r1 = rank * G, (rank + 1) * G
+    t0, t1 = int(b.rollout_offsets[r0]), int(b.rollout_offsets[r1])
+    lm = torch.from_numpy(b.loss_mask[t0:t1].copy())
+    D = parallel.DataParallelPolicyLoss.global_denominator(lm)
+    dp = parallel.DataParallelPolicyLoss(OraclePhases(), T=t1 - t0, H=b.H, V=b.V, num_rollouts=G, group_size=G,
+                                         loss_denominator=D, device="cpu", d_hidden_dtype=torch.float64,
+                                         workspace=False)
+    for name in ("logprob", "entropy", "lse", "coef", "adv"):
+        setattr(dp, name, getattr(dp, name).double())
+    dw = torch.empty(b.V, b.H, dtype=torch.float64)
+    offs = torch.from_numpy((b.rollout_offsets[r0:r1 + 1] - t0).astype(np.int32))
+    dp.step(_bf16(b.hidden[t0:t1]), _bf16(b.w_vocab), torch.from_numpy(b.targets[t0:t1].copy()),
+            torch.from_numpy(infer[t0:t1].copy()), torch.from_numpy(b.rewards[rank].copy()), offs, lm, dw)
+    loss = torch.tensor([dp.ph.loss], dtype=torch.float64)
+    dist.all_reduce(loss)
+    np.savez(os.path.join(out_dir, f"dp{rank}.npz"), dh=dp.d_hidden.numpy(), dw=dw.numpy(), t0=t0, t1=t1,
+             loss=loss.numpy(), D=D)
+    dist.destroy_process_group()
+
+
+def _reference():
+    b, h64, w64, infer = _batch()
+    return b, oracle.policy_loss_fwd_bwd(h64, w64, b.targets, infer.astype(np.float64), b.rewards,
+                                         b.rollout_offsets, b.loss_mask)
+
+
+def test_vocab_parallel_composition(tmp_path):
+    mp.start_processes(_vocab_worker, args=(_free_port(), str(tmp_path)), nprocs=WORLD, start_method="spawn")
+    b, ref = _reference()
+    outs = [np.load(tmp_path / f"vp{r}.npz") for r in range(WORLD)]
+    for o in outs:   # S2/S3 are identical on every rank; dH is the reduced sum
+        np.testing.assert_allclose(o["logprob"], ref.logp, atol=1e-6)
+        np.testing.assert_allclose(o["coef"], ref.report.coef, atol=1e-9)
+        np.testing.assert_allclose(o["dh"], ref.d_hidden, atol=1e-9)
+    dw = np.concatenate([o["dw"] for o in outs])
+    np.testing.assert_allclose(dw, ref.d_w_vocab, atol=1e-9)
+    assert [int(o["lo"]) for o in outs] == [0, b.V // 2]
+
+
+def test_data_parallel_composition(tmp_path):
+    mp.start_processes(_dp_worker, args=(_free_port(), str(tmp_path)), nprocs=WORLD, start_method="spawn")
+    b, ref = _reference()
+    outs = [np.load(tmp_path / f"dp{r}.npz") for r in range(WORLD)]
+    for o in outs:
+        assert float(o["D"]) == b.loss_denominator            # global D, reading R5
+        np.testing.assert_allclose(o["dw"], ref.d_w_vocab, atol=1e-12)   # all-reduced dW
+        np.testing.assert_allclose(o["dh"], ref.d_hidden[int(o["t0"]):int(o["t1"])], atol=1e-12)
+        assert float(o["loss"][0]) == pytest.approx(ref.report.loss, abs=1e-12)
