@@ -196,6 +196,23 @@ rl_status rl_bwd(const rl_lm_shape* shape, const uint16_t* hidden, const uint16_
                  float* d_hidden_f32, float* d_w_vocab, int32_t accumulate_dw,
                  int64_t dz_chunk_rows, void* workspace, size_t workspace_bytes, void* stream);
 
+/* rl_bwd with a phase selection and an SM budget:
+ *   phases  = OR of RL_BWD_DU (K4: recompute dU into the workspace), RL_BWD_DW
+ *             (K6: d_w_vocab) and RL_BWD_DH (K5: d_hidden); they run in the order
+ *             DU, DW, DH. Calling DW and/or DH without DU reuses the dU left in the
+ *             workspace by an earlier call with the same arguments; that requires a
+ *             single dU chunk (dz_chunk_rows = 0 or >= T), else INVALID_ARGUMENT.
+ *   max_sms = 0 for the whole GPU, else the persistent GEMM grids use at most
+ *             this many SMs (leaving the rest to a concurrent collective). */
+#define RL_BWD_DU 1
+#define RL_BWD_DW 2
+#define RL_BWD_DH 4
+#define RL_BWD_ALL 7
+rl_status rl_bwd_ex(const rl_lm_shape* shape, const uint16_t* hidden, const uint16_t* w_vocab,
+                    const int32_t* targets, const float* lse, const float* coef, uint16_t* d_hidden,
+                    float* d_hidden_f32, float* d_w_vocab, int32_t accumulate_dw, int64_t dz_chunk_rows,
+                    int32_t phases, int32_t max_sms, void* workspace, size_t workspace_bytes, void* stream);
+
 /* ------------------------------------------------------------ utilities */
 /* Workspace needed by rl_logprob_fwd / rl_policy_loss_fwd_bwd / the split
  * phases for this shape. dz_chunk_rows = rows of the bf16 dU buffer (0 = T). */

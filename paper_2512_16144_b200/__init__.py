@@ -87,6 +87,8 @@ _SIGS = {
                                     _P, _P, _P, _P, _P, _P, _P, ctypes.c_size_t, _P]),
     "rl_bwd": (ctypes.c_int, [ctypes.POINTER(rl_lm_shape), _P, _P, _P, _P, _P, _P, _P, _P, ctypes.c_int32,
                               ctypes.c_int64, _P, ctypes.c_size_t, _P]),
+    "rl_bwd_ex": (ctypes.c_int, [ctypes.POINTER(rl_lm_shape), _P, _P, _P, _P, _P, _P, _P, _P, ctypes.c_int32,
+                                 ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, _P, ctypes.c_size_t, _P]),
     "rl_workspace_bytes": (ctypes.c_size_t, [ctypes.POINTER(rl_lm_shape), ctypes.c_int32, ctypes.c_int64]),
     "rl_workspace_bytes_hostio": (ctypes.c_size_t, [ctypes.POINTER(rl_lm_shape), ctypes.c_int32]),
     "rl_default_dz_chunk_rows": (ctypes.c_int64, [ctypes.POINTER(rl_lm_shape)]),
@@ -285,6 +287,21 @@ def rl_profile_read(cap: int = 4096) -> list:
     buf = (rl_kernel_time * cap)()
     n = load_library().rl_profile_read(ctypes.cast(buf, ctypes.c_void_p), cap)
     return [(KERNEL_NAMES.get(buf[i].kernel, str(buf[i].kernel)), float(buf[i].ms)) for i in range(min(n, cap))]
+
+
+RL_BWD_DU, RL_BWD_DW, RL_BWD_DH, RL_BWD_ALL = 1, 2, 4, 7
+
+
+def rl_bwd_ex(shape: rl_lm_shape, hidden, w_vocab, targets, lse, coef, d_hidden=None, d_hidden_f32=None,
+              d_w_vocab=None, accumulate_dw=False, dz_chunk_rows=0, phases=RL_BWD_ALL, max_sms=0, workspace=None,
+              stream=None):
+    """S4-S6 with a phase mask (RL_BWD_DU | RL_BWD_DW | RL_BWD_DH) and an SM budget."""
+    ws = workspace if workspace is not None else alloc_workspace(
+        rl_workspace_bytes(shape, 1, dz_chunk_rows), w_vocab.device)
+    _check(load_library().rl_bwd_ex(ctypes.byref(shape), _ptr(hidden), _ptr(w_vocab), _ptr(targets), _ptr(lse),
+                                    _ptr(coef), _ptr(d_hidden), _ptr(d_hidden_f32), _ptr(d_w_vocab),
+                                    1 if accumulate_dw else 0, int(dz_chunk_rows), int(phases), int(max_sms),
+                                    _ptr(ws), ws.numel(), _stream(stream)))
 
 
 def rl_last_launch_count() -> int:

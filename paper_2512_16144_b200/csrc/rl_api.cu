@@ -160,6 +160,45 @@ int cta_group() {
   return cg;
 }
 
+// Raster group (in m-blocks) per GEMM: tiles walk n inside groups of this many
+// m-blocks. Defaults chosen from the sweep in DESIGN.md §5; RL_GROUP_M_<K>
+// overrides (K in FWD, DZ, DH, DW) for measurements.
+int group_m_for(int kid, int dflt) {
+  static int cache[16];
+  static bool init[16] = {};
+  if (!init[kid]) {
+    const char* names[16] = {nullptr, "RL_GROUP_M_FWD", nullptr, nullptr, nullptr, "RL_GROUP_M_DZ",
+                             "RL_GROUP_M_DH", "RL_GROUP_M_DW"};
+    const char* e = names[kid] ? getenv(names[kid]) : nullptr;
+    cache[kid] = (e && atoi(e) > 0) ? atoi(e) : dflt;
+    init[kid] = true;
+  }
+  return cache[kid];
+}
+
+// Soft k-barrier between producers (see EpiParams::sync_*): every RL_SYNC_EVERY
+// k-blocks (default 32; 0 = off), at most RL_SYNC_SLACK sync points of lead
+// (default 2). Keeping the CTAs that share operands inside one L2 window cuts
+// K5/K6 DRAM reads by ~1/3 and lets the power-capped clock rise (~6% per step,
+// profiles/r01/). Correctness never depends on it (the wait is bounded).
+int sync_every_for(int kid) {
+  static int every = [] {
+    const char* e = getenv("RL_SYNC_EVERY");
+    return e ? atoi(e) : 32;
+  }();
+  (void)kid;
+  return every;
+}
+int sync_slack() {
+  static int slack = [] {
+    const char* e = getenv("RL_SYNC_SLACK");
+    return e ? atoi(e) : 2;
+  }();
+  return slack;
+}
+constexpr int kMaxSyncPoints = 1 << 16;
+thread_local uint32_t* g_sync_ctr = nullptr;  // set per call from the workspace
+
 template <int CG>
 constexpr int stages_for() {
   return CG == 2 ? 6 : 4;
@@ -185,6 +224,19 @@ rl_status launch_gemm_cg(int kid, const CUtensorMap& a, const CUtensorMap& b, co
   if (sh.k_blocks == 0) return fail(RL_ERR_SHAPE, "GEMM with K = 0");
   const int64_t tiles = static_cast<int64_t>(sh.m_blocks) * sh.n_blocks;
   const int units = static_cast<int>(tiles < sms / CG ? tiles : sms / CG);
+  rl::EpiParams ep2 = ep;
+  ep2.sync_every = 0;
+  if (g_sync_ctr && sync_every_for(kid) > 0) {
+    const int64_t max_tiles = (tiles + units - 1) / units;
+    const int64_t max_sync = (max_tiles * sh.k_blocks - 1) / sync_every_for(kid);
+    if (max_sync > 0 && max_sync < kMaxSyncPoints) {
+      RL_CUDA(cudaMemsetAsync(g_sync_ctr, 0, static_cast<size_t>(max_sync + 1) * 4, st));
+      ep2.sync_ctr = g_sync_ctr;
+      ep2.sync_every = sync_every_for(kid);
+      ep2.sync_slack = sync_slack();
+      ep2.max_sync = static_cast<int>(max_sync);
+    }
+  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(units * CG);
   cfg.blockDim = dim3(rl::GEMM_THREADS);
@@ -199,7 +251,7 @@ rl_status launch_gemm_cg(int kid, const CUtensorMap& a, const CUtensorMap& b, co
   cfg.numAttrs = 1;
   {
     ProfScope ps(kid, st);
-    RL_CUDA(cudaLaunchKernelEx(&cfg, kern, a, b, c, sh, ep));
+    RL_CUDA(cudaLaunchKernelEx(&cfg, kern, a, b, c, sh, ep2));
   }
   RL_CHECK_LAUNCH();
   return RL_OK;
@@ -230,7 +282,7 @@ struct Carve {
 };
 
 struct WsLayout {
-  size_t partials, lse, coef, rp, dz, end;
+  size_t partials, lse, coef, rp, sync, dz, end;
   int64_t n_tiles_v, ldz, chunk;
 };
 
@@ -247,6 +299,7 @@ WsLayout ws_layout(const rl_lm_shape* s, int32_t R, int64_t chunk_rows) {
   w.lse = c.take(static_cast<size_t>(T) * 4);
   w.coef = c.take(static_cast<size_t>(T) * 4);
   w.rp = c.take(static_cast<size_t>(R > 0 ? R : 1) * sizeof(rl::RolloutPartial));
+  w.sync = c.take(static_cast<size_t>(kMaxSyncPoints) * 4);
   w.dz = c.take(static_cast<size_t>(w.chunk) * w.ldz * 2);
   w.end = align_up(c.off, 1024);
   return w;
@@ -307,7 +360,8 @@ rl_status forward_impl(const rl_lm_shape* s, const uint16_t* hidden, const uint1
   ep.vocab_offset = s->vocab_offset;
   float4* parts = reinterpret_cast<float4*>(ws + L.partials);
   ep.partials = parts;
-  RL_TRY((launch_gemm<rl::EPI_LSE, false, false>(RL_K_FWD_GEMM, ta, tb, ta, T, s->V_local, s->H, 16, ep, sms, st)));
+  g_sync_ctr = reinterpret_cast<uint32_t*>(ws + L.sync);
+  RL_TRY((launch_gemm<rl::EPI_LSE, false, false>(RL_K_FWD_GEMM, ta, tb, ta, T, s->V_local, s->H, group_m_for(RL_K_FWD_GEMM, 16), ep, sms, st)));
   const int blocks = static_cast<int>((T + 63) / 64);
   {
     ProfScope ps(RL_K_MERGE, st);
@@ -354,9 +408,11 @@ rl_status loss_impl(const rl_loss_params* p, int64_t T, int64_t V_global, const 
 }
 
 // K4 -> K5 -> K6 per chunk of rows.
+// K4 -> K6 -> K5 per chunk of rows (dW first, so a caller can overlap its
+// reduction with dH). `phases` selects which run (RL_BWD_* bits).
 rl_status bwd_impl(const rl_lm_shape* s, const uint16_t* hidden, const uint16_t* w, const int32_t* targets,
                    const float* lse, const float* coef, uint16_t* dh, float* dh32, float* dw, int accumulate_dw,
-                   uint8_t* ws, const WsLayout& L, int sms, cudaStream_t st) {
+                   uint8_t* ws, const WsLayout& L, int sms, cudaStream_t st, int phases = RL_BWD_ALL) {
   const int64_t T = s->T, H = s->H, V = s->V_local;
   if (T == 0) {
     if (dw && !accumulate_dw) RL_CUDA(cudaMemsetAsync(dw, 0, static_cast<size_t>(V) * H * 4, st));
@@ -364,6 +420,7 @@ rl_status bwd_impl(const rl_lm_shape* s, const uint16_t* hidden, const uint16_t*
   }
   uint16_t* dz = reinterpret_cast<uint16_t*>(ws + L.dz);
   const int64_t chunk = L.chunk;
+  g_sync_ctr = reinterpret_cast<uint32_t*>(ws + L.sync);
   CUtensorMap t_h_k, t_w_k, t_dz_st, t_dz_k, t_w_mn, t_dh, t_dz_mn, t_h_mn, t_dw;
   RL_TRY(make_map(&t_w_k, w, false, H, V, H, 64, rl::BN / cta_group()));
   RL_TRY(make_map(&t_w_mn, w, false, H, V, H, 64, 64));
@@ -383,32 +440,33 @@ rl_status bwd_impl(const rl_lm_shape* s, const uint16_t* hidden, const uint16_t*
     ep.vocab_offset = s->vocab_offset;
     ep.lse = lse + c0;
     ep.coef = coef + c0;
-    RL_TRY((launch_gemm<rl::EPI_DZ, false, false>(RL_K_DZ_GEMM, t_h_k, t_w_k, t_dz_st, rows, V, H, 16, ep, sms, st)));
-    // K5: dH chunk = dU W
-    if (dh || dh32) {
-      RL_TRY(make_map(&t_dz_k, dz, false, V, rows, L.ldz, 64, kARows));
-      rl::EpiParams e5 = {};
-      e5.rows = rows;
-      e5.cols = H;
-      if (dh) {
-        RL_TRY(make_map(&t_dh, dh + c0 * H, false, H, rows, H, 64, 32));
-        RL_TRY((launch_gemm<rl::EPI_BF16, false, true>(RL_K_DH_GEMM, t_dz_k, t_w_mn, t_dh, rows, H, V, 8, e5, sms, st)));
-      } else {
-        RL_TRY(make_map(&t_dh, dh32 + c0 * H, true, H, rows, H, 32, 32));
-        RL_TRY((launch_gemm<rl::EPI_F32, false, true>(RL_K_DH_GEMM, t_dz_k, t_w_mn, t_dh, rows, H, V, 8, e5, sms, st)));
-      }
-    }
+    if (phases & RL_BWD_DU)
+      RL_TRY((launch_gemm<rl::EPI_DZ, false, false>(RL_K_DZ_GEMM, t_h_k, t_w_k, t_dz_st, rows, V, H, group_m_for(RL_K_DZ_GEMM, 16), ep, sms, st)));
     // K6: dW (+)= dU^T h
-    if (dw) {
+    if ((phases & RL_BWD_DW) && dw) {
       RL_TRY(make_map(&t_dz_mn, dz, false, V, rows, L.ldz, 64, 64));
       RL_TRY(make_map(&t_h_mn, hc, false, H, rows, H, 64, 64));
       rl::EpiParams e6 = {};
       e6.rows = V;
       e6.cols = H;
       if (c0 == 0 && !accumulate_dw) {
-        RL_TRY((launch_gemm<rl::EPI_F32, true, true>(RL_K_DW_GEMM, t_dz_mn, t_h_mn, t_dw, V, H, rows, 8, e6, sms, st)));
+        RL_TRY((launch_gemm<rl::EPI_F32, true, true>(RL_K_DW_GEMM, t_dz_mn, t_h_mn, t_dw, V, H, rows, group_m_for(RL_K_DW_GEMM, 8), e6, sms, st)));
       } else {
-        RL_TRY((launch_gemm<rl::EPI_F32_ADD, true, true>(RL_K_DW_GEMM, t_dz_mn, t_h_mn, t_dw, V, H, rows, 8, e6, sms, st)));
+        RL_TRY((launch_gemm<rl::EPI_F32_ADD, true, true>(RL_K_DW_GEMM, t_dz_mn, t_h_mn, t_dw, V, H, rows, group_m_for(RL_K_DW_GEMM, 8), e6, sms, st)));
+      }
+    }
+    // K5: dH chunk = dU W
+    if ((phases & RL_BWD_DH) && (dh || dh32)) {
+      RL_TRY(make_map(&t_dz_k, dz, false, V, rows, L.ldz, 64, kARows));
+      rl::EpiParams e5 = {};
+      e5.rows = rows;
+      e5.cols = H;
+      if (dh) {
+        RL_TRY(make_map(&t_dh, dh + c0 * H, false, H, rows, H, 64, 32));
+        RL_TRY((launch_gemm<rl::EPI_BF16, false, true>(RL_K_DH_GEMM, t_dz_k, t_w_mn, t_dh, rows, H, V, group_m_for(RL_K_DH_GEMM, 8), e5, sms, st)));
+      } else {
+        RL_TRY(make_map(&t_dh, dh32 + c0 * H, true, H, rows, H, 32, 32));
+        RL_TRY((launch_gemm<rl::EPI_F32, false, true>(RL_K_DH_GEMM, t_dz_k, t_w_mn, t_dh, rows, H, V, group_m_for(RL_K_DH_GEMM, 8), e5, sms, st)));
       }
     }
   }
@@ -598,7 +656,17 @@ rl_status rl_bwd(const rl_lm_shape* shape, const uint16_t* hidden, const uint16_
                  const float* lse, const float* coef, uint16_t* d_hidden, float* d_hidden_f32, float* d_w_vocab,
                  int32_t accumulate_dw, int64_t dz_chunk_rows, void* workspace, size_t workspace_bytes,
                  void* stream) {
+  return rl_bwd_ex(shape, hidden, w_vocab, targets, lse, coef, d_hidden, d_hidden_f32, d_w_vocab, accumulate_dw,
+                   dz_chunk_rows, RL_BWD_ALL, 0, workspace, workspace_bytes, stream);
+}
+
+rl_status rl_bwd_ex(const rl_lm_shape* shape, const uint16_t* hidden, const uint16_t* w_vocab,
+                    const int32_t* targets, const float* lse, const float* coef, uint16_t* d_hidden,
+                    float* d_hidden_f32, float* d_w_vocab, int32_t accumulate_dw, int64_t dz_chunk_rows,
+                    int32_t phases, int32_t max_sms, void* workspace, size_t workspace_bytes, void* stream) {
   g_launches = 0;
+  if (phases <= 0 || phases > RL_BWD_ALL) return fail(RL_ERR_INVALID_ARGUMENT, "phases must be a non-empty RL_BWD_* mask");
+  if (max_sms < 0) return fail(RL_ERR_INVALID_ARGUMENT, "max_sms must be >= 0");
   RL_TRY(check_shape(shape));
   if (d_hidden && d_hidden_f32) return fail(RL_ERR_INVALID_ARGUMENT, "pass d_hidden or d_hidden_f32, not both");
   RL_NONNULL(w_vocab);
@@ -614,10 +682,14 @@ rl_status rl_bwd(const rl_lm_shape* shape, const uint16_t* hidden, const uint16_
   const WsLayout L = ws_layout(shape, 1, dz_chunk_rows);
   if (shape->T > 0 && (!workspace || workspace_bytes < L.end))
     return fail(RL_ERR_WORKSPACE, "workspace needs %zu bytes, got %zu", L.end, workspace_bytes);
+  if (phases != RL_BWD_ALL && L.chunk < shape->T)
+    return fail(RL_ERR_INVALID_ARGUMENT, "partial backward phases need one dU chunk (dz_chunk_rows = 0 or >= T)");
   DevInfo d;
   RL_TRY(device_info(d));
+  int sms = d.sms;
+  if (max_sms > 0 && max_sms < sms) sms = max_sms < 2 ? 2 : max_sms;
   return bwd_impl(shape, hidden, w_vocab, targets, lse, coef, d_hidden, d_hidden_f32, d_w_vocab, accumulate_dw,
-                  static_cast<uint8_t*>(workspace), L, d.sms, static_cast<cudaStream_t>(stream));
+                  static_cast<uint8_t*>(workspace), L, sms, static_cast<cudaStream_t>(stream), phases);
 }
 
 static rl_status step_impl(const rl_lm_shape* shape, const rl_loss_params* params, const uint16_t* hidden,
@@ -746,3 +818,26 @@ rl_status rl_policy_loss_fwd_bwd_hostio(const rl_lm_shape* shape, const rl_loss_
 }
 
 }  // extern "C"
+
+// Diagnostics (not part of rl.h): how many clusters of `cluster` CTAs of the
+// forward GEMM (CG=2 smem footprint) can be co-resident on this device.
+extern "C" int32_t rl_debug_max_active_clusters(int32_t cluster) {
+  auto kern = rl::gemm_kernel<rl::EPI_LSE, false, false, 2, 6>;
+  constexpr int smem = rl::gemm_smem_bytes<2, 6>();
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) return -1;
+  if (cluster > 8) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(cluster * 64);
+  cfg.blockDim = dim3(rl::GEMM_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = cluster;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess) return -2;
+  return n;
+}

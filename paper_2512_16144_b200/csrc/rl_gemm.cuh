@@ -64,7 +64,23 @@ struct EpiParams {
   float4* partials;        // EPI_LSE: [n_blocks][rows]
   const float* lse;        // EPI_DZ:  [rows]
   const float* coef;       // EPI_DZ:  [rows]
+  // soft k-barrier (locality): producers of all CTAs arrive on sync_ctr[p] every
+  // sync_every k-blocks and do not run more than sync_slack points ahead of the
+  // slowest CTA, so CTAs sharing operands stay inside one L2 window. 0 = off.
+  uint32_t* sync_ctr;      // [max_sync + 1], zeroed before the launch
+  int sync_every;
+  int sync_slack;
+  int max_sync;            // highest sync point any CTA reaches
 };
+
+__device__ __forceinline__ void red_release_add(uint32_t* p, uint32_t v) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
 
 __device__ __forceinline__ void tile_coords(int tile, const GemmShape& sh, int& m, int& n) {
   const int per_group = sh.group_m * sh.n_blocks;
@@ -147,12 +163,29 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     // registers); one elected lane issues the TMA copies.
     int s = 0;
     uint32_t ph = 0;
+    int gk = 0;            // k-blocks issued by this CTA so far (all tiles)
+    int last_sync = 0;
     for (int tile = unit; tile < total; tile += n_units) {
       int m, n;
       tile_coords(tile, sh, m, n);
       const int a_row = m * TL::TILE_M + rank * TL::A_ROWS;
       const int b_row = n * BN + rank * TL::B_ROWS;
-      for (int kb = 0; kb < sh.k_blocks; ++kb) {
+      for (int kb = 0; kb < sh.k_blocks; ++kb, ++gk) {
+        if (ep.sync_every > 0 && gk > 0 && gk % ep.sync_every == 0) {
+          const int p = gk / ep.sync_every;
+          if (lane == 0) {
+            red_release_add(ep.sync_ctr + p, 1u);
+            if (p > ep.sync_slack) {
+              // a locality hint, never a dependency: give up after ~2^17 cycles so a
+              // CTA that cannot become resident (shared GPU) cannot stall the others
+              const uint32_t* c = ep.sync_ctr + (p - ep.sync_slack);
+              const long long t0 = clock64();
+              while (ld_acquire(c) < gridDim.x && clock64() - t0 < (1ll << 17)) __nanosleep(64);
+            }
+          }
+          __syncwarp();
+          last_sync = p;
+        }
         mbar_wait_sleep(&empty[s], ph ^ 1);
         if (elect_one()) {
           if (leader) mbar_expect_tx(&full[s], CG * TL::STAGE);
@@ -196,6 +229,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         }
       }
     }
+    // arrive on the sync points this CTA never reaches (it had fewer tiles)
+    if (ep.sync_every > 0 && lane == 0)
+      for (int p = last_sync + 1; p <= ep.max_sync; ++p) red_release_add(ep.sync_ctr + p, 1u);
   } else if (warp == 1) {
     // ----------------------------------------------------------- MMA issuer
     if (leader) {
