@@ -214,6 +214,18 @@ def main_ours(args):
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     name, wl = workload_for(args, world)
+    if args.collective == "auto":
+        args.collective = "nccl"
+        if world > 1:
+            import torch.distributed._symmetric_memory as symm_mem
+            try:
+                probe = symm_mem.empty(1024, dtype=torch.float32, device=dev)
+                ok = torch.tensor([1 if symm_mem.rendezvous(probe, dist.group.WORLD.group_name).multicast_ptr
+                                   else 0], device=dev)
+                dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+                args.collective = "nvls" if ok.item() else "nccl"
+            except Exception:  # noqa: BLE001 - no symmetric memory / multicast here: NCCL
+                args.collective = "nccl"
     vocab_par = name == "glm64k" and world > 1
     mode = "vocab" if vocab_par else "dp"
     H, Vt = wl.hidden, wl.vocab
@@ -276,14 +288,17 @@ def main_ours(args):
     # reduction of K6 at 64k rows loses ~20% to HBM re-reads otherwise)
     chunk = 0 if T <= 16384 else 16384
     if vocab_par:
+        nv = args.collective == "nvls"
         engine = parallel.VocabParallelPolicyLoss(phases, T=T, H=H, V_global=Vt, num_rollouts=R,
                                                   group_size=wl_rank.group_size, loss_denominator=D,
-                                                  dz_chunk_rows=chunk, device=dev)
+                                                  dz_chunk_rows=0 if nv else chunk, device=dev, nvls=nv)
         ws = engine.ws
         dh = engine.d_hidden
     elif world > 1:
         engine = parallel.DataParallelPolicyLoss(phases, T=T, H=H, V=Vt, num_rollouts=R,
-                                                 group_size=wl_rank.group_size, loss_denominator=D, device=dev)
+                                                 group_size=wl_rank.group_size, loss_denominator=D, device=dev,
+                                                 overlap=args.overlap, comm_sms=args.comm_sms,
+                                                 nvls=args.collective == "nvls")
         ws = engine.ws
         dh = engine.d_hidden
     else:
@@ -379,7 +394,15 @@ def main_ours(args):
             engine.ws = None
         wsh = rl.alloc_workspace(rl.rl_workspace_bytes_hostio(shape, R), dev)
 
+        nvls_dp = engine is not None and getattr(engine, "nvls", None) is not None
+
         def hstep():
+            if nvls_dp:
+                rl.rl_policy_loss_fwd_bwd_hostio(shape, params, wl_rank.group_size, hpin, b["w"], tpin, ipin, rpin,
+                                                 opin, mpin, report=report, d_hidden=dh, d_w_vocab=engine.nvls.buf,
+                                                 d_w_vocab_nvls=engine.nvls.descriptor(), workspace=wsh)
+                engine.nvls.barrier()
+                return
             rl.rl_policy_loss_fwd_bwd_hostio(shape, params, wl_rank.group_size, hpin, b["w"], tpin, ipin, rpin, opin,
                                              mpin, report=report, d_hidden=dh, d_w_vocab=dw, workspace=wsh)
             if world > 1:
@@ -409,8 +432,13 @@ def main_ours(args):
                "group_size": wl_rank.group_size, "parallelism": f"{mode}{world}",
                "l2": "inputs exceed L2 (W %.2f GB, hidden %.0f MB > 126 MB); no flush needed" % (
                    V_local * H * 2 / 1e9, T * H * 2 / 1e6),
-               "dz_chunk_rows": chunk or T, "collectives": (["all_gather partials", "all_reduce dH fp32"] if vocab_par
-                                                             else (["all_reduce dW fp32"] if world > 1 else []))}
+               "dz_chunk_rows": (T if (vocab_par and args.collective == "nvls") else (chunk or T)),
+               "collectives": ([] if world == 1 else
+                               (["all_gather partials (NCCL)", "dH fp32 all-reduce " +
+                                 ("fused in K5 epilogue (NVLS multimem)" if args.collective == "nvls" else "(NCCL)")]
+                                if vocab_par else
+                                ["dW fp32 all-reduce " + ("fused in K6 epilogue (NVLS multimem)"
+                                                          if args.collective == "nvls" else "(NCCL)")]))}
         out = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
                "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,
                "scaling": "strong" if vocab_par else "weak", "vs_baseline": None, "dtype": "bf16",
@@ -436,7 +464,12 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
-    ap.add_argument("--ref-tokens", type=int, default=32)
+    ap.add_argument("--ref-tokens", type=int, default=128)
+    ap.add_argument("--overlap", action="store_true", help="DP + NCCL: all-reduce dW on a side stream under K5")
+    ap.add_argument("--collective", default="auto", choices=["auto", "nccl", "nvls"],
+                    help="nvls: the dW (DP) / dH (vocab-parallel) all-reduce is fused into the GEMM epilogue "
+                         "over NVLink multicast; auto = nvls when the GPUs support multicast, else NCCL")
+    ap.add_argument("--comm-sms", type=int, default=24, help="DP overlap: SMs left to NCCL while K5 runs")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

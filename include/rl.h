@@ -94,6 +94,27 @@ typedef struct rl_loss_report {
   uint32_t bad_offsets;      /* 1 if rollout_offsets is not 0 = o_0 <= ... <= o_R = T  */
 } rl_loss_report;
 
+/* Fused cross-rank reduction of an fp32 output over an NVLink multicast group
+ * (NVLS), done inside the producing GEMM's epilogue: every rank stores its own
+ * contribution into its replica of a symmetric buffer (the usual output pointer),
+ * publishes a per-slab flag, and the rank owning each tile sums that slab over
+ * all replicas with multimem.ld_reduce and writes the sum to all of them with
+ * multimem.st. After the call, and after a cross-rank barrier the caller runs on
+ * the same stream, every replica holds the sum over ranks (an all-reduce).
+ * Requirements: the output pointer is this rank's view of the symmetric buffer
+ * whose multicast VA is `multicast`; each flag array holds rl_nvls_flag_count()
+ * uint32 entries, zeroed once at allocation; `epoch` increases on every call;
+ * all ranks make the same call with the same shapes. */
+#define RL_NVLS_MAX_RANKS 8
+typedef struct rl_nvls_reduce {
+  void* multicast;                    /* multicast VA of the symmetric fp32 output buffer  */
+  uint32_t* flags[RL_NVLS_MAX_RANKS]; /* every rank's flag array (peer VAs); [rank] = local */
+  int32_t rank;                       /* this rank in the multicast group                  */
+  int32_t world;                      /* ranks in the group, 2..RL_NVLS_MAX_RANKS          */
+  uint32_t epoch;                     /* > every epoch used before with these flags        */
+  int32_t lag;                        /* tiles between a slab's store and its reduction; 0 = 2 */
+} rl_nvls_reduce;
+
 /* Outputs of rl_policy_loss_fwd_bwd. Optional pointers may be NULL. */
 typedef struct rl_loss_outputs {
   rl_loss_report* report;  /* [1] device, required                                     */
@@ -108,6 +129,9 @@ typedef struct rl_loss_outputs {
   float* d_w_vocab;        /* [V_local, H] fp32 d loss / d W_vocab; or NULL             */
   int32_t accumulate_dw;   /* 0: d_w_vocab is overwritten; 1: the gradient is added     */
   int32_t _pad;
+  const rl_nvls_reduce* d_w_vocab_nvls; /* non-NULL: d_w_vocab is all-reduced in the dW
+                             GEMM epilogue over NVLS (data-parallel ranks); needs
+                             accumulate_dw = 0 and one dU chunk                          */
 } rl_loss_outputs;
 
 /* ---------------------------------------------------------------- S0 */
@@ -203,7 +227,9 @@ rl_status rl_bwd(const rl_lm_shape* shape, const uint16_t* hidden, const uint16_
  *             workspace by an earlier call with the same arguments; that requires a
  *             single dU chunk (dz_chunk_rows = 0 or >= T), else INVALID_ARGUMENT.
  *   max_sms = 0 for the whole GPU, else the persistent GEMM grids use at most
- *             this many SMs (leaving the rest to a concurrent collective). */
+ *             this many SMs (leaving the rest to a concurrent collective).
+ *   dw_nvls / dh_nvls = NULL, or all-reduce d_w_vocab / d_hidden_f32 over an NVLS
+ *             group inside the K6 / K5 epilogue (see rl_nvls_reduce; one dU chunk). */
 #define RL_BWD_DU 1
 #define RL_BWD_DW 2
 #define RL_BWD_DH 4
@@ -211,7 +237,12 @@ rl_status rl_bwd(const rl_lm_shape* shape, const uint16_t* hidden, const uint16_
 rl_status rl_bwd_ex(const rl_lm_shape* shape, const uint16_t* hidden, const uint16_t* w_vocab,
                     const int32_t* targets, const float* lse, const float* coef, uint16_t* d_hidden,
                     float* d_hidden_f32, float* d_w_vocab, int32_t accumulate_dw, int64_t dz_chunk_rows,
-                    int32_t phases, int32_t max_sms, void* workspace, size_t workspace_bytes, void* stream);
+                    int32_t phases, int32_t max_sms, const rl_nvls_reduce* dw_nvls,
+                    const rl_nvls_reduce* dh_nvls, void* workspace, size_t workspace_bytes, void* stream);
+
+/* Flag entries an rl_nvls_reduce needs for d_w_vocab (which = 0) or for
+ * d_hidden_f32 (which = 1) of this shape. */
+int64_t rl_nvls_flag_count(const rl_lm_shape* shape, int32_t which);
 
 /* ------------------------------------------------------------ utilities */
 /* Workspace needed by rl_logprob_fwd / rl_policy_loss_fwd_bwd / the split

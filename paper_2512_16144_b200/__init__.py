@@ -52,12 +52,22 @@ class rl_loss_report(ctypes.Structure):
         return {name: getattr(self, name) for name, _ in self._fields_}
 
 
+NVLS_MAX_RANKS = 8
+
+
+class rl_nvls_reduce(ctypes.Structure):
+    _fields_ = [("multicast", ctypes.c_void_p), ("flags", ctypes.c_void_p * NVLS_MAX_RANKS),
+                ("rank", ctypes.c_int32), ("world", ctypes.c_int32), ("epoch", ctypes.c_uint32),
+                ("lag", ctypes.c_int32)]
+
+
 class rl_loss_outputs(ctypes.Structure):
     _fields_ = [("report", ctypes.c_void_p), ("logprob", ctypes.c_void_p), ("entropy", ctypes.c_void_p),
                 ("lse", ctypes.c_void_p), ("coef", ctypes.c_void_p), ("token_keep", ctypes.c_void_p),
                 ("rollout_guarded", ctypes.c_void_p), ("d_hidden", ctypes.c_void_p),
                 ("d_hidden_f32", ctypes.c_void_p), ("d_w_vocab", ctypes.c_void_p),
-                ("accumulate_dw", ctypes.c_int32), ("_pad", ctypes.c_int32)]
+                ("accumulate_dw", ctypes.c_int32), ("_pad", ctypes.c_int32),
+                ("d_w_vocab_nvls", ctypes.POINTER(rl_nvls_reduce))]
 
 
 class rl_kernel_time(ctypes.Structure):
@@ -88,7 +98,9 @@ _SIGS = {
     "rl_bwd": (ctypes.c_int, [ctypes.POINTER(rl_lm_shape), _P, _P, _P, _P, _P, _P, _P, _P, ctypes.c_int32,
                               ctypes.c_int64, _P, ctypes.c_size_t, _P]),
     "rl_bwd_ex": (ctypes.c_int, [ctypes.POINTER(rl_lm_shape), _P, _P, _P, _P, _P, _P, _P, _P, ctypes.c_int32,
-                                 ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, _P, ctypes.c_size_t, _P]),
+                                 ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(rl_nvls_reduce),
+                                 ctypes.POINTER(rl_nvls_reduce), _P, ctypes.c_size_t, _P]),
+    "rl_nvls_flag_count": (ctypes.c_int64, [ctypes.POINTER(rl_lm_shape), ctypes.c_int32]),
     "rl_workspace_bytes": (ctypes.c_size_t, [ctypes.POINTER(rl_lm_shape), ctypes.c_int32, ctypes.c_int64]),
     "rl_workspace_bytes_hostio": (ctypes.c_size_t, [ctypes.POINTER(rl_lm_shape), ctypes.c_int32]),
     "rl_default_dz_chunk_rows": (ctypes.c_int64, [ctypes.POINTER(rl_lm_shape)]),
@@ -195,21 +207,25 @@ def rl_logprob_fwd(shape: rl_lm_shape, hidden, w_vocab, targets, logprob, entrop
 
 
 def _outputs(report, logprob, entropy=None, lse=None, coef=None, token_keep=None, rollout_guarded=None,
-             d_hidden=None, d_hidden_f32=None, d_w_vocab=None, accumulate_dw=False) -> rl_loss_outputs:
+             d_hidden=None, d_hidden_f32=None, d_w_vocab=None, accumulate_dw=False,
+             d_w_vocab_nvls=None) -> rl_loss_outputs:
     return rl_loss_outputs(_ptr(report), _ptr(logprob), _ptr(entropy), _ptr(lse), _ptr(coef), _ptr(token_keep),
                            _ptr(rollout_guarded), _ptr(d_hidden), _ptr(d_hidden_f32), _ptr(d_w_vocab),
-                           1 if accumulate_dw else 0, 0)
+                           1 if accumulate_dw else 0, 0,
+                           ctypes.pointer(d_w_vocab_nvls) if d_w_vocab_nvls is not None else None)
 
 
 def rl_policy_loss_fwd_bwd(shape: rl_lm_shape, params: rl_loss_params, hidden, w_vocab, targets, infer_logprobs,
                            rollout_adv, rollout_offsets, loss_mask=None, *, report, logprob, entropy=None,
                            lse=None, coef=None, token_keep=None, rollout_guarded=None, d_hidden=None,
-                           d_hidden_f32=None, d_w_vocab=None, accumulate_dw=False, workspace=None, stream=None):
-    """S0..S6 on one rank (see include/rl.h). `report` is a [48] uint8 CUDA tensor."""
+                           d_hidden_f32=None, d_w_vocab=None, accumulate_dw=False, d_w_vocab_nvls=None,
+                           workspace=None, stream=None):
+    """S0..S6 on one rank (see include/rl.h). `report` is a [48] uint8 CUDA tensor.
+    `d_w_vocab_nvls` (rl_nvls_reduce) all-reduces d_w_vocab over NVLS in the K6 epilogue."""
     ws = workspace if workspace is not None else alloc_workspace(
         rl_workspace_bytes(shape, params.num_rollouts), w_vocab.device)
     out = _outputs(report, logprob, entropy, lse, coef, token_keep, rollout_guarded, d_hidden, d_hidden_f32,
-                   d_w_vocab, accumulate_dw)
+                   d_w_vocab, accumulate_dw, d_w_vocab_nvls)
     _check(load_library().rl_policy_loss_fwd_bwd(
         ctypes.byref(shape), ctypes.byref(params), _ptr(_bf16(hidden, "hidden")), _ptr(_bf16(w_vocab, "w_vocab")),
         _ptr(targets), _ptr(infer_logprobs), _ptr(rollout_adv), _ptr(rollout_offsets), _ptr(loss_mask),
@@ -219,7 +235,7 @@ def rl_policy_loss_fwd_bwd(shape: rl_lm_shape, params: rl_loss_params, hidden, w
 def rl_policy_loss_fwd_bwd_hostio(shape: rl_lm_shape, params: rl_loss_params, group_size: int, hidden_host,
                                   w_vocab, targets_host, infer_host, rewards_host, offsets_host,
                                   loss_mask_host=None, *, report, d_hidden=None, d_hidden_f32=None,
-                                  d_w_vocab=None, accumulate_dw=False, workspace=None,
+                                  d_w_vocab=None, accumulate_dw=False, d_w_vocab_nvls=None, workspace=None,
                                   stream=None) -> rl_loss_report:
     """The same step with per-step inputs in (pinned) host tensors; returns the report."""
     ws = workspace if workspace is not None else alloc_workspace(
@@ -233,7 +249,7 @@ def rl_policy_loss_fwd_bwd_hostio(shape: rl_lm_shape, params: rl_loss_params, gr
         return ctypes.c_void_p(t.data_ptr())
 
     out = _outputs(report, None, d_hidden=d_hidden, d_hidden_f32=d_hidden_f32, d_w_vocab=d_w_vocab,
-                   accumulate_dw=accumulate_dw)
+                   accumulate_dw=accumulate_dw, d_w_vocab_nvls=d_w_vocab_nvls)
     rep = rl_loss_report()
     _check(load_library().rl_policy_loss_fwd_bwd_hostio(
         ctypes.byref(shape), ctypes.byref(params), int(group_size), hp(hidden_host), _ptr(w_vocab),
@@ -293,15 +309,22 @@ RL_BWD_DU, RL_BWD_DW, RL_BWD_DH, RL_BWD_ALL = 1, 2, 4, 7
 
 
 def rl_bwd_ex(shape: rl_lm_shape, hidden, w_vocab, targets, lse, coef, d_hidden=None, d_hidden_f32=None,
-              d_w_vocab=None, accumulate_dw=False, dz_chunk_rows=0, phases=RL_BWD_ALL, max_sms=0, workspace=None,
-              stream=None):
+              d_w_vocab=None, accumulate_dw=False, dz_chunk_rows=0, phases=RL_BWD_ALL, max_sms=0, dw_nvls=None,
+              dh_nvls=None, workspace=None, stream=None):
     """S4-S6 with a phase mask (RL_BWD_DU | RL_BWD_DW | RL_BWD_DH) and an SM budget."""
     ws = workspace if workspace is not None else alloc_workspace(
         rl_workspace_bytes(shape, 1, dz_chunk_rows), w_vocab.device)
     _check(load_library().rl_bwd_ex(ctypes.byref(shape), _ptr(hidden), _ptr(w_vocab), _ptr(targets), _ptr(lse),
                                     _ptr(coef), _ptr(d_hidden), _ptr(d_hidden_f32), _ptr(d_w_vocab),
                                     1 if accumulate_dw else 0, int(dz_chunk_rows), int(phases), int(max_sms),
+                                    ctypes.pointer(dw_nvls) if dw_nvls is not None else None,
+                                    ctypes.pointer(dh_nvls) if dh_nvls is not None else None,
                                     _ptr(ws), ws.numel(), _stream(stream)))
+
+
+def rl_nvls_flag_count(shape: rl_lm_shape, which: int) -> int:
+    """Flag entries for an NVLS reduction of d_w_vocab (0) or d_hidden_f32 (1)."""
+    return int(load_library().rl_nvls_flag_count(ctypes.byref(shape), int(which)))
 
 
 def rl_last_launch_count() -> int:

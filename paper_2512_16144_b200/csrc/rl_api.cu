@@ -408,11 +408,35 @@ rl_status loss_impl(const rl_loss_params* p, int64_t T, int64_t V_global, const 
 }
 
 // K4 -> K5 -> K6 per chunk of rows.
+// Fill the NVLS fields of an epilogue from the caller's descriptor; the
+// multicast VA is offset like the local output pointer `local`.
+void set_nvls(rl::EpiParams& e, const rl_nvls_reduce* n, const float* local) {
+  (void)local;
+  e.nvls_mc = static_cast<float*>(n->multicast);
+  for (int r = 0; r < rl::NVLS_MAX_RANKS; ++r) e.nvls_flags[r] = n->flags[r];
+  e.nvls_rank = n->rank;
+  e.nvls_world = n->world;
+  e.nvls_epoch = n->epoch;
+  e.nvls_lag = n->lag > 0 ? n->lag : 2;
+}
+
+rl_status check_nvls(const rl_nvls_reduce* n, const char* what) {
+  if (!n) return RL_OK;
+  if (!n->multicast) return fail(RL_ERR_INVALID_ARGUMENT, "%s: multicast VA is NULL", what);
+  if (n->world < 2 || n->world > RL_NVLS_MAX_RANKS || n->rank < 0 || n->rank >= n->world)
+    return fail(RL_ERR_INVALID_ARGUMENT, "%s: need 2 <= world <= %d and 0 <= rank < world", what, RL_NVLS_MAX_RANKS);
+  for (int r = 0; r < n->world; ++r)
+    if (!n->flags[r]) return fail(RL_ERR_INVALID_ARGUMENT, "%s: flags[%d] is NULL", what, r);
+  if (n->epoch == 0) return fail(RL_ERR_INVALID_ARGUMENT, "%s: epoch must be > 0 (flags start at 0)", what);
+  return RL_OK;
+}
+
 // K4 -> K6 -> K5 per chunk of rows (dW first, so a caller can overlap its
 // reduction with dH). `phases` selects which run (RL_BWD_* bits).
 rl_status bwd_impl(const rl_lm_shape* s, const uint16_t* hidden, const uint16_t* w, const int32_t* targets,
                    const float* lse, const float* coef, uint16_t* dh, float* dh32, float* dw, int accumulate_dw,
-                   uint8_t* ws, const WsLayout& L, int sms, cudaStream_t st, int phases = RL_BWD_ALL) {
+                   uint8_t* ws, const WsLayout& L, int sms, cudaStream_t st, int phases = RL_BWD_ALL,
+                   const rl_nvls_reduce* dw_nvls = nullptr, const rl_nvls_reduce* dh_nvls = nullptr) {
   const int64_t T = s->T, H = s->H, V = s->V_local;
   if (T == 0) {
     if (dw && !accumulate_dw) RL_CUDA(cudaMemsetAsync(dw, 0, static_cast<size_t>(V) * H * 4, st));
@@ -449,7 +473,11 @@ rl_status bwd_impl(const rl_lm_shape* s, const uint16_t* hidden, const uint16_t*
       rl::EpiParams e6 = {};
       e6.rows = V;
       e6.cols = H;
-      if (c0 == 0 && !accumulate_dw) {
+      if (dw_nvls) {
+        set_nvls(e6, dw_nvls, dw);
+        RL_TRY((launch_gemm<rl::EPI_F32_NVLS, true, true>(RL_K_DW_GEMM, t_dz_mn, t_h_mn, t_dw, V, H, rows,
+                                                            group_m_for(RL_K_DW_GEMM, 8), e6, sms, st)));
+      } else if (c0 == 0 && !accumulate_dw) {
         RL_TRY((launch_gemm<rl::EPI_F32, true, true>(RL_K_DW_GEMM, t_dz_mn, t_h_mn, t_dw, V, H, rows, group_m_for(RL_K_DW_GEMM, 8), e6, sms, st)));
       } else {
         RL_TRY((launch_gemm<rl::EPI_F32_ADD, true, true>(RL_K_DW_GEMM, t_dz_mn, t_h_mn, t_dw, V, H, rows, group_m_for(RL_K_DW_GEMM, 8), e6, sms, st)));
@@ -466,6 +494,11 @@ rl_status bwd_impl(const rl_lm_shape* s, const uint16_t* hidden, const uint16_t*
         RL_TRY((launch_gemm<rl::EPI_BF16, false, true>(RL_K_DH_GEMM, t_dz_k, t_w_mn, t_dh, rows, H, V, group_m_for(RL_K_DH_GEMM, 8), e5, sms, st)));
       } else {
         RL_TRY(make_map(&t_dh, dh32 + c0 * H, true, H, rows, H, 32, 32));
+        if (dh_nvls) {
+          set_nvls(e5, dh_nvls, dh32 + c0 * H);
+          RL_TRY((launch_gemm<rl::EPI_F32_NVLS, false, true>(RL_K_DH_GEMM, t_dz_k, t_w_mn, t_dh, rows, H, V,
+                                                               group_m_for(RL_K_DH_GEMM, 8), e5, sms, st)));
+        } else
         RL_TRY((launch_gemm<rl::EPI_F32, false, true>(RL_K_DH_GEMM, t_dz_k, t_w_mn, t_dh, rows, H, V, group_m_for(RL_K_DH_GEMM, 8), e5, sms, st)));
       }
     }
@@ -516,6 +549,14 @@ int32_t rl_profile_read(rl_kernel_time* out, int32_t cap) {
 }
 
 int64_t rl_default_dz_chunk_rows(const rl_lm_shape* shape) { return shape ? shape->T : 0; }
+
+int64_t rl_nvls_flag_count(const rl_lm_shape* shape, int32_t which) {
+  if (!shape) return 0;
+  // slabs = tiles x 8 (2 CTAs x 4 epilogue warps), counted with the smaller
+  // (128-row) tiles so the bound holds for either CTA-group variant
+  const int64_t M = which == 0 ? shape->V_local : shape->T;
+  return ((M + 127) / 128) * ((shape->H + rl::BN - 1) / rl::BN) * 8;
+}
 
 size_t rl_workspace_bytes(const rl_lm_shape* shape, int32_t num_rollouts, int64_t dz_chunk_rows) {
   if (check_shape(shape) != RL_OK) return 0;
@@ -657,14 +698,19 @@ rl_status rl_bwd(const rl_lm_shape* shape, const uint16_t* hidden, const uint16_
                  int32_t accumulate_dw, int64_t dz_chunk_rows, void* workspace, size_t workspace_bytes,
                  void* stream) {
   return rl_bwd_ex(shape, hidden, w_vocab, targets, lse, coef, d_hidden, d_hidden_f32, d_w_vocab, accumulate_dw,
-                   dz_chunk_rows, RL_BWD_ALL, 0, workspace, workspace_bytes, stream);
+                   dz_chunk_rows, RL_BWD_ALL, 0, nullptr, nullptr, workspace, workspace_bytes, stream);
 }
 
 rl_status rl_bwd_ex(const rl_lm_shape* shape, const uint16_t* hidden, const uint16_t* w_vocab,
                     const int32_t* targets, const float* lse, const float* coef, uint16_t* d_hidden,
                     float* d_hidden_f32, float* d_w_vocab, int32_t accumulate_dw, int64_t dz_chunk_rows,
-                    int32_t phases, int32_t max_sms, void* workspace, size_t workspace_bytes, void* stream) {
+                    int32_t phases, int32_t max_sms, const rl_nvls_reduce* dw_nvls,
+                    const rl_nvls_reduce* dh_nvls, void* workspace, size_t workspace_bytes, void* stream) {
   g_launches = 0;
+  RL_TRY(check_nvls(dw_nvls, "dw_nvls"));
+  RL_TRY(check_nvls(dh_nvls, "dh_nvls"));
+  if (dw_nvls && accumulate_dw) return fail(RL_ERR_INVALID_ARGUMENT, "dw_nvls needs accumulate_dw = 0");
+  if (dh_nvls && !d_hidden_f32) return fail(RL_ERR_INVALID_ARGUMENT, "dh_nvls reduces d_hidden_f32");
   if (phases <= 0 || phases > RL_BWD_ALL) return fail(RL_ERR_INVALID_ARGUMENT, "phases must be a non-empty RL_BWD_* mask");
   if (max_sms < 0) return fail(RL_ERR_INVALID_ARGUMENT, "max_sms must be >= 0");
   RL_TRY(check_shape(shape));
@@ -684,12 +730,15 @@ rl_status rl_bwd_ex(const rl_lm_shape* shape, const uint16_t* hidden, const uint
     return fail(RL_ERR_WORKSPACE, "workspace needs %zu bytes, got %zu", L.end, workspace_bytes);
   if (phases != RL_BWD_ALL && L.chunk < shape->T)
     return fail(RL_ERR_INVALID_ARGUMENT, "partial backward phases need one dU chunk (dz_chunk_rows = 0 or >= T)");
+  if ((dw_nvls || dh_nvls) && L.chunk < shape->T)
+    return fail(RL_ERR_INVALID_ARGUMENT, "NVLS reduction needs one dU chunk (dz_chunk_rows = 0 or >= T)");
   DevInfo d;
   RL_TRY(device_info(d));
   int sms = d.sms;
   if (max_sms > 0 && max_sms < sms) sms = max_sms < 2 ? 2 : max_sms;
   return bwd_impl(shape, hidden, w_vocab, targets, lse, coef, d_hidden, d_hidden_f32, d_w_vocab, accumulate_dw,
-                  static_cast<uint8_t*>(workspace), L, sms, static_cast<cudaStream_t>(stream), phases);
+                  static_cast<uint8_t*>(workspace), L, sms, static_cast<cudaStream_t>(stream), phases, dw_nvls,
+                  dh_nvls);
 }
 
 static rl_status step_impl(const rl_lm_shape* shape, const rl_loss_params* params, const uint16_t* hidden,
@@ -705,7 +754,7 @@ static rl_status step_impl(const rl_lm_shape* shape, const rl_loss_params* param
                    reinterpret_cast<rl::RolloutPartial*>(ws + L.rp), st));
   const int mid = g_launches;
   RL_TRY(bwd_impl(shape, hidden, w_vocab, targets, lse, coef, out->d_hidden, out->d_hidden_f32, out->d_w_vocab,
-                  out->accumulate_dw, ws, L, sms, st));
+                  out->accumulate_dw, ws, L, sms, st, RL_BWD_ALL, out->d_w_vocab_nvls, nullptr));
   (void)fwd;
   (void)mid;
   return RL_OK;
@@ -724,6 +773,9 @@ static rl_status check_step_args(const rl_lm_shape* shape, const rl_loss_params*
   if (!aligned16(w_vocab) || !aligned16(out->d_hidden) || !aligned16(out->d_hidden_f32) || !aligned16(out->d_w_vocab))
     return fail(RL_ERR_ALIGNMENT, "matrix pointers must be 16-byte aligned");
   if (need_logprob && shape->T > 0) RL_NONNULL(out->logprob);
+  RL_TRY(check_nvls(out->d_w_vocab_nvls, "d_w_vocab_nvls"));
+  if (out->d_w_vocab_nvls && (out->accumulate_dw || !out->d_w_vocab))
+    return fail(RL_ERR_INVALID_ARGUMENT, "d_w_vocab_nvls needs d_w_vocab and accumulate_dw = 0");
   return RL_OK;
 }
 

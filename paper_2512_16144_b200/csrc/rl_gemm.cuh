@@ -31,7 +31,9 @@ constexpr int EPI_BUF_BYTES = 32 * 128;  // one warp's 32-row x 128-byte store c
 constexpr int EPI_BYTES = 4 * 2 * EPI_BUF_BYTES;
 constexpr int BAR_BYTES = 256;
 
-enum EpiMode { EPI_LSE = 0, EPI_DZ = 1, EPI_BF16 = 2, EPI_F32 = 3, EPI_F32_ADD = 4 };
+enum EpiMode { EPI_LSE = 0, EPI_DZ = 1, EPI_BF16 = 2, EPI_F32 = 3, EPI_F32_ADD = 4, EPI_F32_NVLS = 5 };
+
+constexpr int NVLS_MAX_RANKS = 8;
 
 template <int CG>
 struct Tiling {
@@ -71,6 +73,15 @@ struct EpiParams {
   int sync_every;
   int sync_slack;
   int max_sync;            // highest sync point any CTA reaches
+  // EPI_F32_NVLS: D is also reduced over the ranks of an NVLink multicast group.
+  // Every warp stores its 32-row slab locally (TMA), then publishes flag[slab] =
+  // epoch; the rank owning the tile (tile % world) later sums the slab over all
+  // replicas with multimem.ld_reduce and writes the sum to all with multimem.st.
+  float* nvls_mc;                          // multicast VA of D ([rows][cols], fp32)
+  uint32_t* nvls_flags[NVLS_MAX_RANKS];    // every rank's flag array ([rank] is local)
+  int nvls_rank, nvls_world;
+  uint32_t nvls_epoch;
+  int nvls_lag;                            // reduce the slab finished this many tiles ago
 };
 
 __device__ __forceinline__ void red_release_add(uint32_t* p, uint32_t v) {
@@ -98,6 +109,51 @@ __device__ __forceinline__ void stage_row(uint32_t buf, int row, const uint32_t 
   for (int j = 0; j < 8; ++j) {
     const uint32_t addr = buf + row * 128 + ((j ^ (row & 7)) << 4);
     st_shared_v4(addr, w[4 * j], w[4 * j + 1], w[4 * j + 2], w[4 * j + 3]);
+  }
+}
+
+// Slab = 32 accumulator rows of one tile owned by one epilogue warp.
+__device__ __forceinline__ int nvls_slab(int tile, uint32_t rank, int q) { return tile * 8 + rank * 4 + q; }
+
+// Owner-side reduction of one slab over the multicast group (see EpiParams::nvls_*).
+template <int TILE_M>
+__device__ __noinline__ void nvls_reduce_slab_impl(const EpiParams& ep, const GemmShape& sh, int tile, uint32_t rank,
+                                                   int q, int lane) {
+  if (tile % ep.nvls_world != ep.nvls_rank) return;
+  const int slab = nvls_slab(tile, rank, q);
+  if (lane < ep.nvls_world) {
+    const uint32_t* f = ep.nvls_flags[lane] + slab;
+    const long long t0 = clock64();
+    while (ld_acquire_sys(f) != ep.nvls_epoch) {
+      __nanosleep(128);
+      if (clock64() - t0 > (1ll << 36)) __trap();
+    }
+  }
+  __syncwarp();
+  int m, n;
+  tile_coords(tile, sh, m, n);
+  const int64_t r0 = static_cast<int64_t>(m) * TILE_M + rank * 128 + q * 32;
+  const int64_t c0 = static_cast<int64_t>(n) * BN;
+  const int64_t rleft = ep.rows - r0, cleft = ep.cols - c0;
+  const int rmax = rleft < 32 ? static_cast<int>(rleft) : 32;
+  const int cmax = cleft < BN ? static_cast<int>(cleft) : BN;
+  // lane l covers columns 4l..4l+3 and 128+4l..: 2 x 16 B per row, 8 rows in flight
+  for (int rb = 0; rb < rmax; rb += 8) {
+    float v[8][2][4];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int c = h * 128 + lane * 4;
+        if (rb + i < rmax && c < cmax) mc_ld_reduce_v4(ep.nvls_mc + (r0 + rb + i) * ep.cols + c0 + c, v[i][h]);
+      }
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int c = h * 128 + lane * 4;
+        if (rb + i < rmax && c < cmax) mc_st_v4(ep.nvls_mc + (r0 + rb + i) * ep.cols + c0 + c, v[i][h]);
+      }
   }
 }
 
@@ -291,6 +347,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     int acc = 0;
     uint32_t aph = 0;
     int chunk_ctr = 0;
+    int it = 0;  // tile iteration of this CTA
+    auto nvls_reduce_slab = [&](const EpiParams& e, const GemmShape& g, int t, uint32_t r, int qq, int l) {
+      nvls_reduce_slab_impl<TL::TILE_M>(e, g, t, r, qq, l);
+    };
     auto release_tmem = [&](int a) {
       tc_fence_before();
       __syncwarp();
@@ -426,9 +486,26 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           }
           ++chunk_ctr;
         }
+        if constexpr (MODE == EPI_F32_NVLS) {
+          // publish this warp's slab once its stores are globally visible
+          if (lane == 0) {
+            bulk_wait_all();
+            fence_async_global();
+            fence_sys();
+            st_release_sys(ep.nvls_flags[ep.nvls_rank] + nvls_slab(tile, rank, q), ep.nvls_epoch);
+          }
+          __syncwarp();
+          if (it >= ep.nvls_lag) nvls_reduce_slab(ep, sh, unit + (it - ep.nvls_lag) * n_units, rank, q, lane);
+        }
       }
+      ++it;
       acc ^= 1;
       if (acc == 0) aph ^= 1;
+    }
+    if constexpr (MODE == EPI_F32_NVLS) {
+      for (int j = it - ep.nvls_lag < 0 ? 0 : it - ep.nvls_lag; j < it; ++j)
+        nvls_reduce_slab(ep, sh, unit + j * n_units, rank, q, lane);
+      fence_sys();
     }
     if (lane == 0) bulk_wait_all();
   }

@@ -18,8 +18,44 @@ from __future__ import annotations
 import torch
 import torch.distributed as dist
 
-from . import (make_params, make_shape, rl_bwd, rl_fwd_partials, rl_group_advantages, rl_last_launch_count,
-               rl_loss_coef, rl_merge_partials, rl_policy_loss_fwd_bwd, rl_workspace_bytes, alloc_workspace)
+from . import (RL_BWD_DH, RL_BWD_DU, RL_BWD_DW, alloc_workspace, make_params, make_shape, rl_bwd, rl_bwd_ex,
+               rl_fwd_partials, rl_group_advantages, rl_last_launch_count, rl_logprob_fwd, rl_loss_coef,
+               rl_merge_partials, rl_nvls_flag_count, rl_nvls_reduce, rl_policy_loss_fwd_bwd, rl_workspace_bytes)
+
+
+class NvlsReduction:
+    """A symmetric fp32 output buffer plus per-slab flags for librl's in-epilogue
+    NVLink-multicast all-reduce (rl_nvls_reduce), on torch symmetric memory.
+
+    Each call uses a fresh epoch; `barrier()` (on the current stream) completes the
+    exchange: after it every rank's `buf` holds the sum over ranks."""
+
+    def __init__(self, rows, cols, flag_count, group=None, device=None):
+        import torch.distributed._symmetric_memory as symm_mem
+        name = (group or dist.group.WORLD).group_name
+        self.buf = symm_mem.empty(rows, cols, dtype=torch.float32, device=device)
+        self.handle = symm_mem.rendezvous(self.buf, name)
+        if not self.handle.multicast_ptr:
+            raise RuntimeError("NVLink multicast (NVLS) is not available for this group")
+        self.flags = symm_mem.empty(max(1, flag_count), dtype=torch.int32, device=device)
+        self.flags.zero_()
+        self.flag_handle = symm_mem.rendezvous(self.flags, name)
+        self.rank, self.world = self.handle.rank, self.handle.world_size
+        self.epoch = 0
+        torch.cuda.synchronize(device)
+        self.handle.barrier(channel=0)
+
+    def descriptor(self, lag=2) -> rl_nvls_reduce:
+        self.epoch += 1
+        d = rl_nvls_reduce()
+        d.multicast = self.handle.multicast_ptr
+        for r in range(self.world):
+            d.flags[r] = self.flag_handle.buffer_ptrs[r]
+        d.rank, d.world, d.epoch, d.lag = self.rank, self.world, self.epoch, lag
+        return d
+
+    def barrier(self):
+        self.handle.barrier(channel=1)
 
 
 class LibrlPhases:
@@ -50,18 +86,32 @@ class LibrlPhases:
         self._count()
 
     def bwd(self, shape, hidden, w_shard, targets, lse, coef, d_hidden_f32, d_w_vocab, dz_chunk_rows=0,
-            workspace=None):
-        rl_bwd(shape, hidden, w_shard, targets, lse, coef, d_hidden_f32=d_hidden_f32, d_w_vocab=d_w_vocab,
-               dz_chunk_rows=dz_chunk_rows, workspace=workspace)
+            workspace=None, dh_nvls=None):
+        if dh_nvls is None:
+            rl_bwd(shape, hidden, w_shard, targets, lse, coef, d_hidden_f32=d_hidden_f32, d_w_vocab=d_w_vocab,
+                   dz_chunk_rows=dz_chunk_rows, workspace=workspace)
+        else:
+            rl_bwd_ex(shape, hidden, w_shard, targets, lse, coef, d_hidden_f32=d_hidden_f32, d_w_vocab=d_w_vocab,
+                      dz_chunk_rows=dz_chunk_rows, dh_nvls=dh_nvls, workspace=workspace)
+        self._count()
+
+    def logprob_fwd(self, shape, hidden, w, targets, logprob, entropy, lse, workspace=None):
+        rl_logprob_fwd(shape, hidden, w, targets, logprob, entropy, lse, workspace=workspace)
+        self._count()
+
+    def bwd_phases(self, shape, hidden, w, targets, lse, coef, d_hidden, d_w_vocab, phases, max_sms=0,
+                   workspace=None):
+        rl_bwd_ex(shape, hidden, w, targets, lse, coef, d_hidden=d_hidden, d_w_vocab=d_w_vocab, phases=phases,
+                  max_sms=max_sms, workspace=workspace)
         self._count()
 
     def full_step(self, shape, params, hidden, w, targets, infer, adv, offsets, loss_mask, *, report, logprob,
                   entropy=None, lse=None, coef=None, keep=None, guarded=None, d_hidden=None, d_w_vocab=None,
-                  workspace=None):
+                  d_w_vocab_nvls=None, workspace=None):
         rl_policy_loss_fwd_bwd(shape, params, hidden, w, targets, infer, adv, offsets, loss_mask, report=report,
                                logprob=logprob, entropy=entropy, lse=lse, coef=coef, token_keep=keep,
                                rollout_guarded=guarded, d_hidden=d_hidden, d_w_vocab=d_w_vocab,
-                               workspace=workspace)
+                               d_w_vocab_nvls=d_w_vocab_nvls, workspace=workspace)
         self._count()
 
 
@@ -78,7 +128,7 @@ class VocabParallelPolicyLoss:
 
     def __init__(self, phases, *, T, H, V_global, num_rollouts, group_size, loss_denominator, group=None,
                  inv_temperature=1.0, alpha=0.5, beta=5.0, guard=1e-5, dz_chunk_rows=0, device=None,
-                 workspace=True):
+                 workspace=True, nvls=False):
         self.ph = phases
         self.group = group
         self.world = dist.get_world_size(group)
@@ -102,7 +152,15 @@ class VocabParallelPolicyLoss:
         self.guarded = torch.empty(num_rollouts, dtype=torch.uint8, device=dev)
         self.adv = torch.empty(num_rollouts, **f32)
         self.report = torch.zeros(48, dtype=torch.uint8, device=dev)
-        self.d_hidden = torch.empty(T, H, **f32)
+        # nvls: dH partials are all-reduced inside the K5 epilogue (NVLink multicast)
+        self.nvls = None
+        if nvls:
+            if dz_chunk_rows and dz_chunk_rows < T:
+                raise ValueError("the NVLS dH reduction needs one dU chunk (dz_chunk_rows = 0)")
+            self.nvls = NvlsReduction(T, H, rl_nvls_flag_count(self.shape, 1), group, dev)
+            self.d_hidden = self.nvls.buf
+        else:
+            self.d_hidden = torch.empty(T, H, **f32)
         self.ws = self.loss_ws = None
         if workspace:
             self.ws = alloc_workspace(rl_workspace_bytes(self.shape, num_rollouts, dz_chunk_rows), dev)
@@ -116,6 +174,11 @@ class VocabParallelPolicyLoss:
         ph.merge_partials(self.parts, self.world, self.T, self.logprob, self.entropy, self.lse)
         ph.loss_coef(self.params, self.T, self.V_global, self.logprob, infer, targets, self.adv, offsets,
                      loss_mask, self.coef, self.keep, self.guarded, self.report, workspace=self.loss_ws)
+        if self.nvls is not None:
+            ph.bwd(self.shape, hidden, w_shard, targets, self.lse, self.coef, self.d_hidden, d_w_vocab,
+                   dz_chunk_rows=self.chunk, workspace=self.ws, dh_nvls=self.nvls.descriptor())
+            self.nvls.barrier()                                   # exchange 2, fused into K5's epilogue
+            return self.d_hidden
         ph.bwd(self.shape, hidden, w_shard, targets, self.lse, self.coef, self.d_hidden, d_w_vocab,
                dz_chunk_rows=self.chunk, workspace=self.ws)
         dist.all_reduce(self.d_hidden, group=self.group)                                  # exchange 2
@@ -127,8 +190,15 @@ class DataParallelPolicyLoss:
 
     def __init__(self, phases, *, T, H, V, num_rollouts, group_size, loss_denominator, group=None,
                  inv_temperature=1.0, alpha=0.5, beta=5.0, guard=1e-5, device=None, d_hidden_dtype=torch.bfloat16,
-                 workspace=True):
+                 workspace=True, overlap=False, comm_sms=24, nvls=False):
         self.ph = phases
+        # overlap: the dW all-reduce (NCCL, side stream) runs concurrently with K5,
+        # which then uses all but `comm_sms` SMs (NCCL's NVLS channels need SMs).
+        self.overlap = overlap
+        self.comm = torch.cuda.Stream(device=device) if overlap else None
+        if overlap:
+            n_sms = torch.cuda.get_device_properties(device).multi_processor_count
+            self.dh_sms = max(2, (n_sms - comm_sms) // 2 * 2)
         self.group = group
         self.world = dist.get_world_size(group)
         self.T, self.H, self.V, self.R, self.G = T, H, V, num_rollouts, group_size
@@ -146,6 +216,10 @@ class DataParallelPolicyLoss:
         self.report = torch.zeros(48, dtype=torch.uint8, device=dev)
         self.d_hidden = torch.empty(T, H, dtype=d_hidden_dtype, device=dev)
         self.ws = alloc_workspace(rl_workspace_bytes(self.shape, num_rollouts), dev) if workspace else None
+        self.loss_ws = alloc_workspace(48 * max(1, num_rollouts), dev) if workspace else None
+        # nvls: dW is all-reduced inside the K6 epilogue (NVLink multicast); the
+        # step then returns the symmetric buffer that holds the sum.
+        self.nvls = NvlsReduction(V, H, rl_nvls_flag_count(self.shape, 0), group, dev) if nvls else None
 
     @staticmethod
     def global_denominator(loss_mask: torch.Tensor, group=None) -> float:
@@ -154,12 +228,35 @@ class DataParallelPolicyLoss:
         dist.all_reduce(t, group=group)
         return float(t.item())
 
-    def step(self, hidden, w, targets, infer, rewards, offsets, loss_mask, d_w_vocab):
+    def step(self, hidden, w, targets, infer, rewards, offsets, loss_mask, d_w_vocab=None):
         ph = self.ph
         ph.group_advantages(rewards, self.G, self.adv)
-        ph.full_step(self.shape, self.params, hidden, w, targets, infer, self.adv, offsets, loss_mask,
-                     report=self.report, logprob=self.logprob, entropy=self.entropy, lse=self.lse, coef=self.coef,
-                     keep=self.keep, guarded=self.guarded, d_hidden=self.d_hidden, d_w_vocab=d_w_vocab,
-                     workspace=self.ws)
-        dist.all_reduce(d_w_vocab, group=self.group)                                      # the exchange
+        if self.nvls is not None:
+            ph.full_step(self.shape, self.params, hidden, w, targets, infer, self.adv, offsets, loss_mask,
+                         report=self.report, logprob=self.logprob, entropy=self.entropy, lse=self.lse,
+                         coef=self.coef, keep=self.keep, guarded=self.guarded, d_hidden=self.d_hidden,
+                         d_w_vocab=self.nvls.buf, d_w_vocab_nvls=self.nvls.descriptor(), workspace=self.ws)
+            self.nvls.barrier()                                   # the exchange, fused into K6's epilogue
+            return self.nvls.buf
+        if not self.overlap:
+            ph.full_step(self.shape, self.params, hidden, w, targets, infer, self.adv, offsets, loss_mask,
+                         report=self.report, logprob=self.logprob, entropy=self.entropy, lse=self.lse,
+                         coef=self.coef, keep=self.keep, guarded=self.guarded, d_hidden=self.d_hidden,
+                         d_w_vocab=d_w_vocab, workspace=self.ws)
+            dist.all_reduce(d_w_vocab, group=self.group)                                  # the exchange
+            return d_w_vocab
+        # S1..S3, then K4 (dU) and K6 (dW); the dW all-reduce runs on a side stream
+        # while K5 (dH) uses the SMs NCCL leaves free.
+        ph.logprob_fwd(self.shape, hidden, w, targets, self.logprob, self.entropy, self.lse, workspace=self.ws)
+        ph.loss_coef(self.params, self.T, self.V, self.logprob, infer, targets, self.adv, offsets, loss_mask,
+                     self.coef, self.keep, self.guarded, self.report, workspace=self.loss_ws)
+        ph.bwd_phases(self.shape, hidden, w, targets, self.lse, self.coef, self.d_hidden, d_w_vocab,
+                      RL_BWD_DU | RL_BWD_DW, workspace=self.ws)
+        main = torch.cuda.current_stream()
+        self.comm.wait_stream(main)
+        with torch.cuda.stream(self.comm):
+            dist.all_reduce(d_w_vocab, group=self.group)                                  # the exchange
+        ph.bwd_phases(self.shape, hidden, w, targets, self.lse, self.coef, self.d_hidden, d_w_vocab, RL_BWD_DH,
+                      max_sms=self.dh_sms, workspace=self.ws)
+        main.wait_stream(self.comm)
         return d_w_vocab

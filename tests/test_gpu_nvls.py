@@ -1,0 +1,82 @@
+"""The in-epilogue NVLink-multicast all-reduce (rl_nvls_reduce) against NCCL on
+2 GPUs (`-m gpu`; skipped with fewer than 2 devices). DP: dW summed over ranks;
+vocab-parallel: dH partials summed over ranks. Both must equal the NCCL
+all-reduce of the same per-rank results up to fp32 summation order."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+if not torch.cuda.is_available() or torch.cuda.device_count() < 2:  # pragma: no cover
+    pytest.skip("needs 2 GPUs", allow_module_level=True)
+
+import torch.distributed as dist  # noqa: E402
+import torch.multiprocessing as mp  # noqa: E402
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, port, out_dir, mode):
+    import synth
+    from paper_2512_16144_b200 import parallel
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(rank)
+    dev = torch.device("cuda", rank)
+    dist.init_process_group("nccl", rank=rank, world_size=2, device_id=dev)
+    wl = synth.Workload("nv", 1, 4, 150, 512, 3000, ragged=True, delta_sigma=0.5)
+    T = wl.tokens
+    res = {}
+    infer = None
+    for nv in (False, False, True):
+        if mode == "dp":
+            b = synth.make_batch_device(wl, 50 + rank, device=dev, tokens=T)
+        else:
+            Vl = wl.vocab // 2
+            b = synth.make_batch_device(wl, 50, device=dev, tokens=T, vocab=Vl, vocab_offset=rank * Vl,
+                                        vocab_total=wl.vocab)
+        offs = torch.from_numpy(b["offsets"]).to(dev)
+        lm = torch.from_numpy(b["loss_mask"]).to(dev)
+        rw = torch.from_numpy(b["rewards"]).to(dev)
+        inf = infer if infer is not None else torch.full((T,), -1.0, device=dev)
+        if mode == "dp":
+            D = parallel.DataParallelPolicyLoss.global_denominator(lm)
+            eng = parallel.DataParallelPolicyLoss(parallel.LibrlPhases(), T=T, H=wl.hidden, V=wl.vocab,
+                                                  num_rollouts=wl.num_rollouts, group_size=wl.group_size,
+                                                  loss_denominator=D, device=dev, nvls=nv)
+            dw = torch.empty(wl.vocab, wl.hidden, device=dev)
+            out = eng.step(b["hidden"], b["w"], b["targets"], inf, rw, offs, lm, None if nv else dw)
+        else:
+            eng = parallel.VocabParallelPolicyLoss(parallel.LibrlPhases(), T=T, H=wl.hidden, V_global=wl.vocab,
+                                                   num_rollouts=wl.num_rollouts, group_size=wl.group_size,
+                                                   loss_denominator=float(T), device=dev, nvls=nv)
+            dw = torch.empty(eng.V_local, wl.hidden, device=dev)
+            out = eng.step(b["hidden"], b["w"], b["targets"], inf, rw, offs, lm, dw)
+        torch.cuda.synchronize()
+        if infer is None:   # first pass: stored log-probs = own log-probs minus the drawn mismatch
+            infer = torch.clamp(eng.logprob - b["delta"], max=0.0).contiguous()
+            continue
+        res["nvls" if nv else "nccl"] = out.cpu().numpy().copy()
+    np.savez(os.path.join(out_dir, f"{mode}{rank}.npz"), **res)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("mode", ["dp", "vocab"])
+def test_nvls_matches_nccl(tmp_path, mode):
+    mp.start_processes(_worker, args=(_port(), str(tmp_path), mode), nprocs=2, start_method="spawn")
+    for r in range(2):
+        d = np.load(tmp_path / f"{mode}{r}.npz")
+        a, b = d["nvls"], d["nccl"]
+        assert np.abs(b).max() > 0
+        np.testing.assert_allclose(a, b, rtol=1e-5, atol=1e-6 * np.abs(b).max())
+    d0, d1 = np.load(tmp_path / f"{mode}0.npz"), np.load(tmp_path / f"{mode}1.npz")
+    assert np.array_equal(d0["nvls"], d1["nvls"])   # one reduced value, written to every replica
