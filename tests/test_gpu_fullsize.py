@@ -96,3 +96,124 @@ def test_glm16k_sampled_rollouts():
     assert not dh[torch.from_numpy(other).to(dev)].float().abs().max().item()
     dw_h = dw.cpu().numpy().astype(np.float64)
     assert harness.rel_fro(dw_h, ref.d_w_vocab) <= harness.GRAD_RTOL
+
+
+def _sampled_reference(b, rows, infer, adv, D, inv_temperature=1.0):
+    """Oracle on a set of sampled rows (loss mask 1 only there): rollout structure
+    re-based to the sampled rows, so the guard sees exactly the sampled tokens."""
+    rollout_of = np.repeat(np.arange(len(b.rollout_offsets) - 1), np.diff(b.rollout_offsets))
+    counts = np.bincount(rollout_of[rows], minlength=len(b.rollout_offsets) - 1)
+    sub_off = np.concatenate([[0], np.cumsum(counts)])
+    h64 = oracle.bf16_to_f64(b.hidden[rows])
+    w64 = oracle.bf16_to_f64(b.w_vocab)
+    return oracle.policy_loss_fwd_bwd(h64, w64, b.targets[rows], infer[rows].astype(np.float64), None, sub_off,
+                                      None, loss_denominator=D, rollout_adv=adv.astype(np.float64),
+                                      inv_temperature=inv_temperature)
+
+
+def _sample_rows(b, n, seed):
+    rows = np.sort(np.random.default_rng(seed).choice(b.T, size=n, replace=False))
+    return rows
+
+
+def _infer_for(b, rows):
+    h64 = oracle.bf16_to_f64(b.hidden[rows])
+    w64 = oracle.bf16_to_f64(b.w_vocab)
+    lp, _, _ = oracle.log_softmax_stats(oracle.lm_logits(h64, w64), b.targets[rows])
+    infer = np.full(b.T, -5.0, dtype=np.float32)
+    infer[rows] = synth.compose_infer_logprobs(lp, b.delta_noise[rows] * 3.0, b.spikes[rows])
+    return infer
+
+
+def test_small_config_chunked_backward_sampled_rows():
+    """BASELINE 'small dense' (T = 131072, H = 2048, V = 32000) with the bench's
+    16k-row dU chunks (8 chunks; dW accumulated by TMA reduce-add)."""
+    wl = synth.CONFIGS["small"]
+    b = synth.make_batch(wl, 4)
+    T, H, V = b.T, b.H, b.V
+    rows = _sample_rows(b, 1536, 4)
+    infer = _infer_for(b, rows)
+    lm = np.zeros(T, np.uint8)
+    lm[rows] = 1
+    adv = oracle.group_advantages(b.rewards).reshape(-1).astype(np.float32)
+    D = float(len(rows))
+    ref = _sampled_reference(b, rows, infer, adv, D)
+    dev = "cuda"
+    bf = lambda x: torch.from_numpy(x.view(np.int16).copy()).view(torch.bfloat16).to(dev)  # noqa: E731
+    hidden, w = bf(b.hidden), bf(b.w_vocab)
+    tg = torch.from_numpy(b.targets).to(dev)
+    shape = rl.make_shape(T, H, V)
+    lp, ent, lse = (torch.empty(T, device=dev) for _ in range(3))
+    ws = rl.alloc_workspace(rl.rl_workspace_bytes(shape, len(adv), 16384), dev)
+    rl.rl_logprob_fwd(shape, hidden, w, tg, lp, ent, lse, workspace=ws)
+    coef = torch.empty(T, device=dev)
+    keep = torch.empty(T, dtype=torch.uint8, device=dev)
+    guarded = torch.empty(len(adv), dtype=torch.uint8, device=dev)
+    report = rl.new_report(dev)
+    rl.rl_loss_coef(rl.make_params(len(adv), D), T, V, lp, torch.from_numpy(infer).to(dev), tg,
+                    torch.from_numpy(adv).to(dev), torch.from_numpy(b.rollout_offsets).to(dev),
+                    torch.from_numpy(lm).to(dev), coef, keep, guarded, report=report)
+    dh = torch.empty(T, H, dtype=torch.bfloat16, device=dev)
+    dw = torch.empty(V, H, device=dev)
+    rl.rl_bwd(shape, hidden, w, tg, lse, coef, d_hidden=dh, d_w_vocab=dw, dz_chunk_rows=16384, workspace=ws)
+    torch.cuda.synchronize()
+    assert np.max(np.abs(lp.cpu().numpy()[rows] - ref.logp)) <= harness.LOGP_TOL
+    assert np.max(np.abs(ent.cpu().numpy()[rows] - ref.entropy)) <= harness.LOGP_TOL
+    rep = rl.read_report(report).as_dict()
+    assert abs(rep["loss"] - ref.report.loss) <= harness.LOSS_TOL
+    assert harness.rel_fro(dh.float().cpu().numpy()[rows].astype(np.float64), ref.d_hidden) <= harness.GRAD_RTOL
+    assert harness.rel_fro(dw.cpu().numpy().astype(np.float64), ref.d_w_vocab) <= harness.GRAD_RTOL
+
+
+def test_glm64k_vocab_parallel_emulated_sampled_rows():
+    """BASELINE 'GLM-4.5-Air long-context' (T = 65536, V = 151552) as 2 vocab
+    shards through the split-phase ABI on one GPU (what each rank of the N = 2
+    vocab-parallel run executes, in sequence), sampled rows checked vs the oracle."""
+    wl = synth.CONFIGS["glm64k"]
+    b = synth.make_batch(wl, 5)
+    T, H, V = b.T, b.H, b.V
+    rows = _sample_rows(b, 512, 5)
+    infer = _infer_for(b, rows)
+    lm = np.zeros(T, np.uint8)
+    lm[rows] = 1
+    adv = oracle.group_advantages(b.rewards).reshape(-1).astype(np.float32)
+    D = float(len(rows))
+    ref = _sampled_reference(b, rows, infer, adv, D)
+    dev = "cuda"
+    bf = lambda x: torch.from_numpy(x.view(np.int16).copy()).view(torch.bfloat16).to(dev)  # noqa: E731
+    hidden = bf(b.hidden)
+    tg = torch.from_numpy(b.targets).to(dev)
+    n = 2
+    Vl = V // n
+    parts = torch.empty(n, T, 4, device=dev)
+    shards = [bf(b.w_vocab[j * Vl:(j + 1) * Vl]) for j in range(n)]
+    ws = None
+    for j in range(n):
+        shp = rl.make_shape(T, H, Vl, j * Vl, V)
+        ws = ws if ws is not None else rl.alloc_workspace(rl.rl_workspace_bytes(shp, len(adv), 16384), dev)
+        rl.rl_fwd_partials(shp, hidden, shards[j], tg, parts[j], workspace=ws)
+    lp, ent, lse = (torch.empty(T, device=dev) for _ in range(3))
+    rl.rl_merge_partials(parts, n, T, lp, ent, lse)
+    coef = torch.empty(T, device=dev)
+    report = rl.new_report(dev)
+    rl.rl_loss_coef(rl.make_params(len(adv), D), T, V, lp, torch.from_numpy(infer).to(dev), tg,
+                    torch.from_numpy(adv).to(dev), torch.from_numpy(b.rollout_offsets).to(dev),
+                    torch.from_numpy(lm).to(dev), coef, report=report)
+    dh = torch.zeros(T, H, device=dev)
+    dws = []
+    for j in range(n):
+        shp = rl.make_shape(T, H, Vl, j * Vl, V)
+        dhp = torch.empty(T, H, device=dev)
+        dw = torch.empty(Vl, H, device=dev)
+        rl.rl_bwd(shp, hidden, shards[j], tg, lse, coef, d_hidden_f32=dhp, d_w_vocab=dw, dz_chunk_rows=16384,
+                  workspace=ws)
+        dh += dhp
+        dws.append(dw)
+    torch.cuda.synchronize()
+    assert np.max(np.abs(lp.cpu().numpy()[rows] - ref.logp)) <= harness.LOGP_TOL
+    assert np.max(np.abs(ent.cpu().numpy()[rows] - ref.entropy)) <= harness.LOGP_TOL
+    rep = rl.read_report(report).as_dict()
+    assert abs(rep["loss"] - ref.report.loss) <= harness.LOSS_TOL
+    assert harness.rel_fro(dh.cpu().numpy()[rows].astype(np.float64), ref.d_hidden) <= harness.GRAD_RTOL
+    dw_all = torch.cat(dws).cpu().numpy().astype(np.float64)
+    assert harness.rel_fro(dw_all, ref.d_w_vocab) <= harness.GRAD_RTOL
