@@ -258,3 +258,41 @@ def test_host_validation_errors():
                           torch.zeros(10, dtype=torch.int32, device="cuda"), torch.empty(10, device="cuda"),
                           workspace=torch.empty(16, dtype=torch.uint8, device="cuda"))
     assert e.value.status == 5
+
+
+def test_no_out_of_bounds_writes_guard_bands():
+    """compute-sanitizer is unavailable on the GPU pool, so every output (and the
+    workspace) sits inside a larger buffer whose margins hold a sentinel; ragged
+    T, V, H exercise every tail path. Any byte written outside the tensors fails."""
+    c = harness.make_case(RAGGED, 12, tokens=333, vocab=1000, hidden=200)
+    d = harness.to_device(c)
+    b = c.batch
+    T, H, V, R = b.T, b.H, b.V, len(c.adv)
+    G = 4096   # guard elements on each side (16 KB of fp32)
+
+    def guarded(n, dtype):
+        buf = torch.full((n + 2 * G,), 0, dtype=dtype, device="cuda")
+        buf.view(torch.uint8).fill_(0xA5)
+        return buf, buf[G:G + n]
+
+    bufs = {}
+    f32 = torch.float32
+    for name, n, dt in (("logprob", T, f32), ("entropy", T, f32), ("lse", T, f32), ("coef", T, f32),
+                        ("keep", T, torch.uint8), ("guarded", R, torch.uint8), ("report", 48, torch.uint8),
+                        ("dh", T * H, torch.bfloat16), ("dw", V * H, f32)):
+        bufs[name] = guarded(n, dt)
+    shape = rl.make_shape(T, H, V)
+    params = rl.make_params(R, b.loss_denominator)
+    wsn = rl.rl_workspace_bytes(shape, R)
+    wbuf, ws = guarded(wsn + (16 - wsn % 16) % 16, torch.uint8)
+    v = {k: x[1] for k, x in bufs.items()}
+    rl.rl_policy_loss_fwd_bwd(shape, params, d["hidden"], d["w"], d["targets"], d["infer"], d["adv"], d["offsets"],
+                              d["loss_mask"], report=v["report"], logprob=v["logprob"], entropy=v["entropy"],
+                              lse=v["lse"], coef=v["coef"], token_keep=v["keep"], rollout_guarded=v["guarded"],
+                              d_hidden=v["dh"].view(T, H), d_w_vocab=v["dw"].view(V, H), workspace=ws)
+    torch.cuda.synchronize()
+    for name, (buf, _) in list(bufs.items()) + [("workspace", (wbuf, None))]:
+        raw = buf.view(torch.uint8)
+        esz = buf.element_size()
+        head, tail = raw[: G * esz], raw[raw.numel() - G * esz:]
+        assert bool((head == 0xA5).all()) and bool((tail == 0xA5).all()), f"write outside {name}"
