@@ -506,6 +506,36 @@ rl_status bwd_impl(const rl_lm_shape* s, const uint16_t* hidden, const uint16_t*
   return RL_OK;
 }
 
+// Side stream + events of the host-I/O call (per host thread and device).
+struct HostioStreams {
+  int dev = -1;
+  cudaStream_t copy = nullptr;
+  cudaEvent_t start = nullptr;
+  std::vector<cudaEvent_t> slab;
+  rl_status ensure(int n) {
+    int d = 0;
+    RL_CUDA(cudaGetDevice(&d));
+    if (d != dev) {
+      copy = nullptr;
+      start = nullptr;
+      slab.clear();
+      dev = d;
+    }
+    if (!copy) RL_CUDA(cudaStreamCreateWithFlags(&copy, cudaStreamNonBlocking));
+    if (!start) RL_CUDA(cudaEventCreateWithFlags(&start, cudaEventDisableTiming));
+    while (static_cast<int>(slab.size()) < n) {
+      cudaEvent_t e;
+      RL_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      slab.push_back(e);
+    }
+    return RL_OK;
+  }
+};
+HostioStreams& hostio_streams() {
+  thread_local HostioStreams h;
+  return h;
+}
+
 }  // namespace
 
 // =================================================================== C ABI
@@ -741,13 +771,28 @@ rl_status rl_bwd_ex(const rl_lm_shape* shape, const uint16_t* hidden, const uint
                   dh_nvls);
 }
 
+// The whole step. With slab_events, the forward runs slab by slab (slab_rows
+// rows each), each launch first waiting for its slab's event (the host-I/O
+// call records one per H2D slab copy), so the hidden-state upload overlaps K1.
 static rl_status step_impl(const rl_lm_shape* shape, const rl_loss_params* params, const uint16_t* hidden,
                            const uint16_t* w_vocab, const int32_t* targets, const float* infer_logprobs,
                            const float* rollout_adv, const int32_t* rollout_offsets, const uint8_t* loss_mask,
-                           const rl_loss_outputs* out, uint8_t* ws, const WsLayout& L, int sms, cudaStream_t st) {
+                           const rl_loss_outputs* out, uint8_t* ws, const WsLayout& L, int sms, cudaStream_t st,
+                           const cudaEvent_t* slab_events = nullptr, int64_t slab_rows = 0) {
   float* lse = out->lse ? out->lse : reinterpret_cast<float*>(ws + L.lse);
   float* coef = out->coef ? out->coef : reinterpret_cast<float*>(ws + L.coef);
-  RL_TRY(forward_impl(shape, hidden, w_vocab, targets, out->logprob, out->entropy, lse, nullptr, ws, L, sms, st));
+  if (slab_events && slab_rows > 0 && shape->T > 0) {
+    int j = 0;
+    for (int64_t r0 = 0; r0 < shape->T; r0 += slab_rows, ++j) {
+      rl_lm_shape sub = *shape;
+      sub.T = (shape->T - r0 < slab_rows) ? shape->T - r0 : slab_rows;
+      RL_CUDA(cudaStreamWaitEvent(st, slab_events[j], 0));
+      RL_TRY(forward_impl(&sub, hidden + r0 * shape->H, w_vocab, targets + r0, out->logprob + r0,
+                          out->entropy ? out->entropy + r0 : nullptr, lse + r0, nullptr, ws, L, sms, st));
+    }
+  } else {
+    RL_TRY(forward_impl(shape, hidden, w_vocab, targets, out->logprob, out->entropy, lse, nullptr, ws, L, sms, st));
+  }
   const int fwd = g_launches;
   RL_TRY(loss_impl(params, shape->T, shape->V_global, out->logprob, infer_logprobs, targets, rollout_adv,
                    rollout_offsets, loss_mask, coef, out->token_keep, out->rollout_guarded, out->report,
@@ -843,8 +888,21 @@ rl_status rl_policy_loss_fwd_bwd_hostio(const rl_lm_shape* shape, const rl_loss_
   int32_t* d_off = reinterpret_cast<int32_t*>(ws + c.take((R + 1) * 4));
   uint8_t* d_lm = ws + c.take(T);
   float* d_lp = reinterpret_cast<float*>(ws + c.take(T * 4));
+  // hidden rows go up in slabs on a side stream; the forward starts on slab 0
+  // while the rest is in flight (the small per-token vectors go first on `st`)
+  const int64_t slab = 4096;
+  const int n_slabs = static_cast<int>((T + slab - 1) / slab);
+  HostioStreams& hs = hostio_streams();
+  RL_TRY(hs.ensure(n_slabs));
   if (T > 0) {
-    RL_CUDA(cudaMemcpyAsync(d_hidden_in, hidden_host, T * shape->H * 2, cudaMemcpyHostToDevice, st));
+    RL_CUDA(cudaEventRecord(hs.start, st));
+    RL_CUDA(cudaStreamWaitEvent(hs.copy, hs.start, 0));
+    for (int j = 0; j < n_slabs; ++j) {
+      const int64_t r0 = j * slab, rows = (T - r0 < slab) ? T - r0 : slab;
+      RL_CUDA(cudaMemcpyAsync(d_hidden_in + r0 * shape->H, hidden_host + r0 * shape->H, rows * shape->H * 2,
+                              cudaMemcpyHostToDevice, hs.copy));
+      RL_CUDA(cudaEventRecord(hs.slab[j], hs.copy));
+    }
     RL_CUDA(cudaMemcpyAsync(d_tg, targets_host, T * 4, cudaMemcpyHostToDevice, st));
     RL_CUDA(cudaMemcpyAsync(d_inf, infer_host, T * 4, cudaMemcpyHostToDevice, st));
     if (loss_mask_host) RL_CUDA(cudaMemcpyAsync(d_lm, loss_mask_host, T, cudaMemcpyHostToDevice, st));
@@ -861,7 +919,8 @@ rl_status rl_policy_loss_fwd_bwd_hostio(const rl_lm_shape* shape, const rl_loss_
   if (!o.logprob) o.logprob = d_lp;
   const int before = g_launches;
   rl_status s = step_impl(shape, params, d_hidden_in, w_vocab, d_tg, d_inf, d_adv, d_off,
-                          loss_mask_host ? d_lm : nullptr, &o, ws, L, d.sms, st);
+                          loss_mask_host ? d_lm : nullptr, &o, ws, L, d.sms, st, T > 0 ? hs.slab.data() : nullptr,
+                          slab);
   (void)before;
   if (s != RL_OK) return s;
   RL_CUDA(cudaMemcpyAsync(report_host, out->report, sizeof(rl_loss_report), cudaMemcpyDeviceToHost, st));
