@@ -69,13 +69,25 @@ typedef struct rl_lm_shape {
   int32_t _pad;
 } rl_lm_shape;
 
+/* Loss variants. All share the backward: each only changes
+ * coef_t = -d loss / d logp_t and the loss value (R16, R17).
+ *   RL_LOSS_ICEPOP  Eq.1 + Eq.2: token ratio masked outside [alpha, beta] (the paper)
+ *   RL_LOSS_CISPO   ratio clipped to [alpha, beta], as a stop-gradient weight on
+ *                   log pi (CISPO, contrasted with IcePop at PAPER.md L472)
+ *   RL_LOSS_GSPO    sequence-level ratio s_i = exp(mean_t log k_t), PPO-style clip of s_i
+ *                   to [alpha, beta] (GSPO, Fig. 8); D is then the
+ *                   caller's sequence count */
+typedef enum rl_loss_variant { RL_LOSS_ICEPOP = 0, RL_LOSS_CISPO = 1, RL_LOSS_GSPO = 2 } rl_loss_variant;
+
 /* Loss hyper-parameters. */
 typedef struct rl_loss_params {
-  float alpha;             /* Eq.2 lower bound, 0 < alpha <= 1                        */
-  float beta;              /* Eq.2 upper bound, beta >= 1 (closed interval, R4)       */
-  float guard_threshold;   /* rollout masked iff min_t k_t < guard (strict, R4); 0 off */
-  int32_t num_rollouts;    /* R = number of packed rollouts on this rank (>= 1)       */
-  double loss_denominator; /* D = sum_i |y_i| over the GLOBAL step batch, > 0 (R5)     */
+  float alpha;             /* Eq.2 lower bound, 0 < alpha <= 1 (clip low for CISPO/GSPO) */
+  float beta;              /* Eq.2 upper bound, beta >= 1, closed interval (R4)           */
+  float guard_threshold;   /* rollout masked iff min_t k_t < guard (strict, R4); 0 off    */
+  int32_t num_rollouts;    /* R = number of packed rollouts on this rank (>= 1)          */
+  double loss_denominator; /* D = sum_i |y_i| over the GLOBAL step batch, > 0 (R5)        */
+  int32_t variant;         /* rl_loss_variant; 0 = the paper's IcePop objective           */
+  int32_t _pad;
 } rl_loss_params;
 
 /* Device-resident loss report (SPEC LossReport + counters). Written, not

@@ -180,6 +180,90 @@ def icepop_loss(logp: np.ndarray, infer_logprobs: np.ndarray, rollout_adv: np.nd
     )
 
 
+# ------------------------------------------------------- loss variants (§8 f2)
+def _segments(offsets, T):
+    R = len(offsets) - 1
+    return R, np.repeat(np.arange(R), np.diff(np.asarray(offsets, dtype=np.int64)))
+
+
+def cispo_loss(logp, infer_logprobs, rollout_adv, offsets, loss_mask, clip_low, clip_high, guard_threshold,
+               loss_denominator, targets=None, vocab=None) -> LossReport:
+    """CISPO (MiniMax-M1, cited at PAPER.md L472: "similar to CISPO ... we use masking
+    instead of clipping"; reading R16): the ratio is clipped, not masked, and enters as a
+    stop-gradient weight on log pi_train:
+
+      J      = 1/D sum_t valid_t (1 - g_i) sg(clip(k_t, lo, hi)) A_i logp_t
+      coef_t = valid_t (1 - g_i) clip(k_t, lo, hi) A_i / D          (d(-J)/d logp_t = -coef_t)
+      loss   = -sum_t coef_t logp_t
+    The rollout guard of L472 still applies (guard_threshold = 0 disables it).
+    masked_low / masked_high count tokens whose ratio was clipped."""
+    T = len(logp)
+    base = icepop_loss(logp, infer_logprobs, rollout_adv, offsets, loss_mask, 0.0, np.inf, guard_threshold,
+                       loss_denominator, targets, vocab)
+    if base.bad_offsets:
+        return base
+    R, rollout_of = _segments(offsets, T)
+    k = base.ratio
+    valid = base.valid
+    keep = valid & ~base.guarded[rollout_of]
+    w = np.clip(k, clip_low, clip_high)
+    coef = np.where(keep, w * np.asarray(rollout_adv, np.float64)[rollout_of] / loss_denominator, 0.0)
+    loss = -float((coef * np.where(keep, logp, 0.0)).sum())
+    return dataclasses.replace(base, loss=loss, coef=coef, keep=keep,
+                               masked_low=int((valid & (k < clip_low)).sum()),
+                               masked_high=int((valid & (k > clip_high)).sum()),
+                               kept_tokens=int(keep.sum()))
+
+
+def gspo_loss(logp, infer_logprobs, rollout_adv, offsets, loss_mask, clip_low, clip_high, guard_threshold,
+              loss_denominator, targets=None, vocab=None) -> LossReport:
+    """GSPO (Qwen, the sequence-level objective of PAPER.md Fig. 8; reading R17):
+
+      s_i    = exp( (1/n_i) sum_{t in i, valid} (logp_t - infer_t) )      (n_i valid tokens)
+      J      = 1/D sum_i [n_i > 0] (1 - g_i) min(s_i A_i, clip(s_i, lo, hi) A_i)
+      coef_t = valid_t (1 - g_i) u_i s_i A_i / (n_i D),  u_i = 1 unless the min picks the
+               clipped term (A_i > 0 and s_i > hi, or A_i < 0 and s_i < lo), then 0
+      loss   = -J
+    (d s_i / d logp_t = s_i / n_i, so d(-J)/d logp_t = -coef_t.) D is the caller's
+    denominator (the GSPO paper averages over sequences: pass the rollout count).
+    masked_low / masked_high count tokens of rollouts whose gradient the clip removed."""
+    T = len(logp)
+    base = icepop_loss(logp, infer_logprobs, rollout_adv, offsets, loss_mask, 0.0, np.inf, guard_threshold,
+                       loss_denominator, targets, vocab)
+    if base.bad_offsets:
+        return base
+    R, rollout_of = _segments(offsets, T)
+    A = np.asarray(rollout_adv, np.float64)
+    valid = base.valid
+    with np.errstate(invalid="ignore"):
+        logratio = np.where(valid, np.asarray(logp, np.float64) - np.asarray(infer_logprobs, np.float64), 0.0)
+    n = np.bincount(rollout_of, weights=valid.astype(np.float64), minlength=R)
+    sum_lr = np.bincount(rollout_of, weights=logratio, minlength=R)
+    s = np.exp(np.divide(sum_lr, n, out=np.zeros(R), where=n > 0))
+    live = (n > 0) & ~base.guarded
+    clipped_hi = (A > 0) & (s > clip_high)
+    clipped_lo = (A < 0) & (s < clip_low)
+    u = live & ~clipped_hi & ~clipped_lo
+    J = np.where(live, np.minimum(s * A, np.clip(s, clip_low, clip_high) * A), 0.0).sum() / loss_denominator
+    per_rollout = np.where(u, s * A / np.where(n > 0, n, 1.0) / loss_denominator, 0.0)
+    keep = valid & u[rollout_of]
+    coef = np.where(keep, per_rollout[rollout_of], 0.0)
+    return dataclasses.replace(base, loss=-float(J), coef=coef, keep=keep,
+                               masked_low=int((valid & (live & clipped_lo)[rollout_of]).sum()),
+                               masked_high=int((valid & (live & clipped_hi)[rollout_of]).sum()),
+                               kept_tokens=int(keep.sum()))
+
+
+LOSS_VARIANTS = {"icepop": 0, "cispo": 1, "gspo": 2}
+
+
+def variant_loss(variant, *args, **kw) -> LossReport:
+    """Dispatch by name: icepop (Eq.1/Eq.2, alpha/beta = mask bounds), cispo or gspo
+    (alpha/beta = clip bounds)."""
+    fn = {"icepop": icepop_loss, "cispo": cispo_loss, "gspo": gspo_loss}[variant]
+    return fn(*args, **kw)
+
+
 # ------------------------------------------------------------------- backward
 def icepop_backward(Z: np.ndarray, lse: np.ndarray, targets: np.ndarray, coef: np.ndarray,
                     hidden: np.ndarray, w_vocab: np.ndarray, inv_temperature: float = 1.0):
@@ -211,7 +295,7 @@ class StepResult:
 def policy_loss_fwd_bwd(hidden, w_vocab, targets, infer_logprobs, rewards, offsets,
                         loss_mask=None, *, alpha=0.5, beta=5.0, guard_threshold=1e-5,
                         loss_denominator=None, inv_temperature=1.0, backward=True,
-                        rollout_adv=None) -> StepResult:
+                        rollout_adv=None, variant="icepop") -> StepResult:
     """The whole north-star step on one rank: S0 (advantages), S1-S2 (logits,
     log-softmax stats), S3 (Eq.1/Eq.2/guard), S4-S6 (backward). `hidden` and
     `w_vocab` are fp64 arrays (use bf16_to_f64 on bit patterns); `rewards` is
@@ -224,8 +308,8 @@ def policy_loss_fwd_bwd(hidden, w_vocab, targets, infer_logprobs, rewards, offse
     V = w_vocab.shape[0]
     safe_t = np.where((targets >= 0) & (targets < V), targets, 0)
     logp, ent, lse = log_softmax_stats(Z, safe_t)
-    rep = icepop_loss(logp, infer_logprobs, A, offsets, lm, alpha, beta, guard_threshold,
-                      D, targets=targets, vocab=V)
+    rep = variant_loss(variant, logp, infer_logprobs, A, offsets, lm, alpha, beta, guard_threshold,
+                       D, targets=targets, vocab=V)
     dH = dW = None
     if backward:
         _, dH, dW = icepop_backward(Z, lse, safe_t, rep.coef, hidden, w_vocab, inv_temperature)

@@ -38,7 +38,11 @@ class rl_lm_shape(ctypes.Structure):
 
 class rl_loss_params(ctypes.Structure):
     _fields_ = [("alpha", ctypes.c_float), ("beta", ctypes.c_float), ("guard_threshold", ctypes.c_float),
-                ("num_rollouts", ctypes.c_int32), ("loss_denominator", ctypes.c_double)]
+                ("num_rollouts", ctypes.c_int32), ("loss_denominator", ctypes.c_double),
+                ("variant", ctypes.c_int32), ("_pad", ctypes.c_int32)]
+
+
+LOSS_VARIANTS = {"icepop": 0, "cispo": 1, "gspo": 2}   # rl_loss_variant
 
 
 class rl_loss_report(ctypes.Structure):
@@ -160,9 +164,11 @@ def make_shape(T, H, V_local, vocab_offset=0, V_global=None, inv_temperature=1.0
                        int(V_local + vocab_offset if V_global is None else V_global), float(inv_temperature), 0)
 
 
-def make_params(num_rollouts, loss_denominator, alpha=ALPHA, beta=BETA, guard_threshold=GUARD) -> rl_loss_params:
+def make_params(num_rollouts, loss_denominator, alpha=ALPHA, beta=BETA, guard_threshold=GUARD,
+                variant="icepop") -> rl_loss_params:
+    v = LOSS_VARIANTS[variant] if isinstance(variant, str) else int(variant)
     return rl_loss_params(float(alpha), float(beta), float(guard_threshold), int(num_rollouts),
-                          float(loss_denominator))
+                          float(loss_denominator), v, 0)
 
 
 def _bf16(t: torch.Tensor | None, name: str) -> torch.Tensor | None:

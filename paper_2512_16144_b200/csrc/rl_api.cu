@@ -329,6 +329,8 @@ rl_status check_params(const rl_loss_params* p) {
   if (!(p->loss_denominator > 0.0) || !isfinite(p->loss_denominator))
     return fail(RL_ERR_INVALID_ARGUMENT, "loss_denominator must be finite and > 0");
   if (p->num_rollouts < 1) return fail(RL_ERR_INVALID_ARGUMENT, "num_rollouts must be >= 1");
+  if (p->variant < RL_LOSS_ICEPOP || p->variant > RL_LOSS_GSPO)
+    return fail(RL_ERR_INVALID_ARGUMENT, "unknown loss variant %d", p->variant);
   return RL_OK;
 }
 
@@ -377,6 +379,7 @@ rl_status loss_impl(const rl_loss_params* p, int64_t T, int64_t V_global, const 
                     float* coef, uint8_t* keep, uint8_t* guarded, rl_loss_report* rep, rl::RolloutPartial* rp,
                     cudaStream_t st) {
   rl::LossArgs a;
+  a.variant = p->variant;
   a.alpha = p->alpha;
   a.beta = p->beta;
   a.guard = p->guard_threshold;

@@ -101,6 +101,7 @@ __device__ __forceinline__ T block_reduce_sum(T v, T* sh) {
 }
 
 struct LossArgs {
+  int variant;  // rl_loss_variant
   float alpha, beta, guard;
   double inv_D;
   int R;
@@ -149,7 +150,10 @@ __global__ void __launch_bounds__(256) loss_coef_kernel(const LossArgs a) {
   const int64_t t0 = a.offsets[i], t1 = a.offsets[i + 1];
   const double A = static_cast<double>(a.adv[i]);
 
+  // pass 1: guard min over valid tokens (and, for GSPO, the mean log-ratio)
   float kmin = INFINITY;
+  double lr_sum = 0.0;
+  uint32_t n_valid = 0;
   for (int64_t t = t0 + threadIdx.x; t < t1; t += blockDim.x) {
     const bool lm = a.loss_mask ? (a.loss_mask[t] != 0) : true;
     const float inf = a.infer[t];
@@ -159,7 +163,12 @@ __global__ void __launch_bounds__(256) loss_coef_kernel(const LossArgs a) {
       const int32_t y = a.targets[t];
       tg = y >= 0 && static_cast<int64_t>(y) < a.V_global;
     }
-    if (lm && fin && tg) kmin = fminf(kmin, expf(a.logprob[t] - inf));
+    if (lm && fin && tg) {
+      const float d = a.logprob[t] - inf;
+      kmin = fminf(kmin, expf(d));
+      lr_sum += static_cast<double>(d);
+      ++n_valid;
+    }
   }
   // block min (fixed tree)
   shf[threadIdx.x] = kmin;
@@ -170,7 +179,27 @@ __global__ void __launch_bounds__(256) loss_coef_kernel(const LossArgs a) {
   }
   const bool g = shf[0] < a.guard;
   __syncthreads();
+  // GSPO: s_i, the liveness and clip gate of the rollout (identical in every thread)
+  float s_seq = 1.f, gspo_w = 0.f;
+  bool gspo_live = false, gspo_clip_lo = false, gspo_clip_hi = false, gspo_u = false;
+  double gspo_J = 0.0;
+  if (a.variant == RL_LOSS_GSPO) {
+    const double lr = block_reduce_sum(lr_sum, shd);
+    const uint32_t n = block_reduce_sum(n_valid, shu);
+    gspo_live = n > 0 && !g;
+    s_seq = n > 0 ? static_cast<float>(exp(lr / n)) : 1.f;
+    gspo_clip_hi = gspo_live && A > 0.0 && s_seq > a.beta;
+    gspo_clip_lo = gspo_live && A < 0.0 && s_seq < a.alpha;
+    gspo_u = gspo_live && !gspo_clip_hi && !gspo_clip_lo;
+    gspo_w = gspo_u ? static_cast<float>(static_cast<double>(s_seq) * A / n * a.inv_D) : 0.f;
+    if (gspo_live) {
+      const double sc = fmin(fmax(static_cast<double>(s_seq), static_cast<double>(a.alpha)),
+                             static_cast<double>(a.beta));
+      gspo_J = fmin(static_cast<double>(s_seq) * A, sc * A) * a.inv_D;
+    }
+  }
 
+  // pass 2: gate, coefficient, counters
   double loss = 0.0, kl = 0.0;
   uint32_t kept = 0, low = 0, high = 0, gtok = 0, nonfin = 0, badtgt = 0;
   for (int64_t t = t0 + threadIdx.x; t < t1; t += blockDim.x) {
@@ -186,19 +215,36 @@ __global__ void __launch_bounds__(256) loss_coef_kernel(const LossArgs a) {
     float c = 0.f;
     bool kp = false;
     if (valid) {
-      const float d = a.logprob[t] - inf;
+      const float lp = a.logprob[t];
+      const float d = lp - inf;
       const float k = expf(d);
-      low += (k < a.alpha);
-      high += (k > a.beta);
       gtok += g;
       kl += static_cast<double>(k) - static_cast<double>(d) - 1.0;
-      kp = (k >= a.alpha) && (k <= a.beta) && !g;
-      if (kp) {
-        const double cd = static_cast<double>(k) * A * a.inv_D;
-        c = static_cast<float>(cd);
-        loss += cd;
-        ++kept;
+      if (a.variant == RL_LOSS_ICEPOP) {
+        low += (k < a.alpha);
+        high += (k > a.beta);
+        kp = (k >= a.alpha) && (k <= a.beta) && !g;
+        if (kp) {
+          const double cd = static_cast<double>(k) * A * a.inv_D;
+          c = static_cast<float>(cd);
+          loss += cd;
+        }
+      } else if (a.variant == RL_LOSS_CISPO) {
+        low += (k < a.alpha);
+        high += (k > a.beta);
+        kp = !g;
+        if (kp) {
+          const double cd = static_cast<double>(fminf(fmaxf(k, a.alpha), a.beta)) * A * a.inv_D;
+          c = static_cast<float>(cd);
+          loss += cd * static_cast<double>(lp);   // -loss = sum coef * logp
+        }
+      } else {  // GSPO
+        low += gspo_clip_lo;
+        high += gspo_clip_hi;
+        kp = gspo_u;
+        c = gspo_w;
       }
+      kept += kp;
     } else if (lm) {
       nonfin += !fin;
       badtgt += (fin && !tg);
@@ -206,6 +252,7 @@ __global__ void __launch_bounds__(256) loss_coef_kernel(const LossArgs a) {
     a.coef[t] = c;
     if (a.keep) a.keep[t] = kp ? 1 : 0;
   }
+  if (a.variant == RL_LOSS_GSPO) loss = (threadIdx.x == 0) ? gspo_J : 0.0;
   RolloutPartial p;
   p.loss = block_reduce_sum(loss, shd);
   p.kl = block_reduce_sum(kl, shd);

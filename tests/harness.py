@@ -29,6 +29,7 @@ class Case:
     alpha: float = synth.ALPHA
     beta: float = synth.BETA
     guard: float = synth.GUARD
+    variant: str = "icepop"
 
 
 def make_case(wl: synth.Workload, seed=0, *, tokens=None, vocab=None, hidden=None, inv_temperature=1.0,
@@ -50,10 +51,22 @@ def run_oracle(c: Case, backward=True, loss_denominator=None):
         c.h64, c.w64, b.targets, c.infer.astype(np.float64), None, b.rollout_offsets, b.loss_mask,
         alpha=c.alpha, beta=c.beta, guard_threshold=c.guard,
         loss_denominator=b.loss_denominator if loss_denominator is None else loss_denominator,
-        inv_temperature=c.inv_temperature, backward=backward, rollout_adv=c.adv.astype(np.float64))
+        inv_temperature=c.inv_temperature, backward=backward, rollout_adv=c.adv.astype(np.float64),
+        variant=c.variant)
 
 
 def band_tokens(c: Case, ref) -> np.ndarray:
+    if c.variant == "gspo":
+        # the gate is per rollout: s_i = exp(mean log k) within 1e-4 of a clip bound
+        b = c.batch
+        v = ref.report.valid
+        R = len(b.rollout_offsets) - 1
+        rollout_of = np.repeat(np.arange(R), np.diff(b.rollout_offsets))
+        lr = np.where(v, ref.logp - c.infer.astype(np.float64), 0.0)
+        n = np.bincount(rollout_of, weights=v.astype(float), minlength=R)
+        s = np.exp(np.bincount(rollout_of, weights=lr, minlength=R) / np.maximum(n, 1))
+        near = (np.abs(s - c.alpha) <= BAND) | (np.abs(s - c.beta) <= BAND)
+        return v & near[rollout_of]
     k = ref.report.ratio
     v = ref.report.valid
     near = (np.abs(k - c.alpha) <= BAND) | (np.abs(k - c.beta) <= BAND)
@@ -150,7 +163,7 @@ def run_gpu_step(c: Case, *, dh_f32=False, accumulate_dw=False, dw_init=None, us
     T, H, V, R = b.T, b.H, b.V, len(c.adv)
     shape = rl.make_shape(T, H, V, 0, V, c.inv_temperature)
     params = rl.make_params(R, b.loss_denominator if loss_denominator is None else loss_denominator,
-                            c.alpha, c.beta, c.guard)
+                            c.alpha, c.beta, c.guard, c.variant)
     f32 = dict(dtype=torch.float32, device=device)
     out = dict(logprob=torch.empty(T, **f32), entropy=torch.empty(T, **f32), lse=torch.empty(T, **f32),
                coef=torch.empty(T, **f32), keep=torch.empty(T, dtype=torch.uint8, device=device),

@@ -34,7 +34,7 @@ def test_every_declared_symbol_is_exported(lib):
 
 def test_struct_layouts_match_header(lib):
     assert ctypes.sizeof(rl.rl_lm_shape) == 48
-    assert ctypes.sizeof(rl.rl_loss_params) == 24
+    assert ctypes.sizeof(rl.rl_loss_params) == 32
     assert ctypes.sizeof(rl.rl_loss_report) == 48
     assert ctypes.sizeof(rl.rl_loss_outputs) == 96
     assert ctypes.sizeof(rl.rl_nvls_reduce) == 88

@@ -296,3 +296,17 @@ def test_no_out_of_bounds_writes_guard_bands():
         esz = buf.element_size()
         head, tail = raw[: G * esz], raw[raw.numel() - G * esz:]
         assert bool((head == 0xA5).all()) and bool((tail == 0xA5).all()), f"write outside {name}"
+
+
+@pytest.mark.parametrize("variant,lo,hi", [("cispo", 0.8, 1.25), ("gspo", 0.9, 1.1), ("gspo", 0.5, 2.0)])
+def test_loss_variants_vs_oracle(variant, lo, hi):
+    """CISPO and GSPO coefficients (S3 only; same backward kernels)."""
+    c = harness.make_case(RAGGED, 13, tokens=333, vocab=1000, hidden=200)
+    c.variant, c.alpha, c.beta = variant, lo, hi
+    D = float(len(c.adv)) if variant == "gspo" else c.batch.loss_denominator
+    ref = harness.run_oracle(c, loss_denominator=D)
+    gpu = harness.run_gpu_step(c, loss_denominator=D)
+    err = harness.compare(c, ref, gpu)
+    if hi - lo < 0.5:
+        assert ref.report.masked_low + ref.report.masked_high > 0      # the clip is exercised
+    print(variant, err)
