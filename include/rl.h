@@ -256,6 +256,28 @@ rl_status rl_bwd_ex(const rl_lm_shape* shape, const uint16_t* hidden, const uint
  * d_hidden_f32 (which = 1) of this shape. */
 int64_t rl_nvls_flag_count(const rl_lm_shape* shape, int32_t which);
 
+/* ------------------------------------------ Muon */
+/* Newton-Schulz orthogonalisation of an fp32 matrix G [M, N] (row-major, e.g.
+ * d_w_vocab), the step Muon applies to a gradient (§2.1.7;
+ * reading R18): X_0 = bf16(G / (||G||_F + 1e-7)), then `steps` quintic iterations
+ * (a, b, c) = (3.4445, -4.7750, 2.0315):
+ *   M >= N:  A = X^T X,  X <- X (a I + b A + c A^2)
+ *   M <  N:  A = X X^T,  X <- (a I + b A + c A^2) X
+ * Every product runs on the tcgen05 GEMMs (bf16 operands, fp32 accumulation).
+ * out: [M, N] bf16. M, N >= 1, N % 8 == 0, min(M, N) % 8 == 0, steps >= 1. */
+rl_status rl_newton_schulz(const float* g, int64_t M, int64_t N, int32_t steps, uint16_t* out, void* workspace,
+                           size_t workspace_bytes, void* stream);
+size_t rl_newton_schulz_workspace_bytes(int64_t M, int64_t N);
+
+/* One Muon update of an fp32 parameter matrix theta [M, N] (reading R18):
+ *   m <- mu m + g;  u = nesterov ? g + mu m : m;
+ *   theta <- theta (1 - lr wd) - lr sqrt(max(1, M/N)) NS_steps(u).
+ * momentum [M, N] fp32 is updated in place. Workspace: rl_muon_workspace_bytes. */
+rl_status rl_muon_step(float* theta, const float* grad, float* momentum, int64_t M, int64_t N, float lr, float mu,
+                       float weight_decay, int32_t nesterov, int32_t steps, void* workspace, size_t workspace_bytes,
+                       void* stream);
+size_t rl_muon_workspace_bytes(int64_t M, int64_t N);
+
 /* ------------------------------------------------------------ utilities */
 /* Workspace needed by rl_logprob_fwd / rl_policy_loss_fwd_bwd / the split
  * phases for this shape. dz_chunk_rows = rows of the bf16 dU buffer (0 = T). */
@@ -289,7 +311,9 @@ typedef enum rl_kernel_id {
   RL_K_DZ_GEMM = 5,    /* K4 S4 recompute + dU (tcgen05)         */
   RL_K_DH_GEMM = 6,    /* K5 S5 dH = dU W (tcgen05)              */
   RL_K_DW_GEMM = 7,    /* K6 S6 dW (+)= dU^T h (tcgen05)         */
-  RL_K_MEMSET = 8      /* zero fill of an empty batch's dW       */
+  RL_K_MEMSET = 8,     /* zero fill of an empty batch's dW       */
+  RL_K_NS_GEMM = 9,    /* Newton-Schulz / Muon GEMMs (tcgen05)   */
+  RL_K_NS_AUX = 10     /* Newton-Schulz / Muon SIMT kernels      */
 } rl_kernel_id;
 
 typedef struct rl_kernel_time {

@@ -79,7 +79,7 @@ class rl_kernel_time(ctypes.Structure):
 
 
 KERNEL_NAMES = {0: "K0_group_adv", 1: "K1_fwd_gemm_lse", 2: "K2_merge", 3: "K3_loss_coef", 4: "K3b_finalize",
-                5: "K4_bwd_dz_gemm", 6: "K5_dh_gemm", 7: "K6_dw_gemm", 8: "memset"}
+                5: "K4_bwd_dz_gemm", 6: "K5_dh_gemm", 7: "K6_dw_gemm", 8: "memset", 9: "NS_gemm", 10: "NS_aux"}
 
 REPORT_BYTES = ctypes.sizeof(rl_loss_report)
 assert REPORT_BYTES == 48
@@ -105,6 +105,12 @@ _SIGS = {
                                  ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(rl_nvls_reduce),
                                  ctypes.POINTER(rl_nvls_reduce), _P, ctypes.c_size_t, _P]),
     "rl_nvls_flag_count": (ctypes.c_int64, [ctypes.POINTER(rl_lm_shape), ctypes.c_int32]),
+    "rl_newton_schulz": (ctypes.c_int, [_P, ctypes.c_int64, ctypes.c_int64, ctypes.c_int32, _P, _P,
+                                        ctypes.c_size_t, _P]),
+    "rl_newton_schulz_workspace_bytes": (ctypes.c_size_t, [ctypes.c_int64, ctypes.c_int64]),
+    "rl_muon_step": (ctypes.c_int, [_P, _P, _P, ctypes.c_int64, ctypes.c_int64, ctypes.c_float, ctypes.c_float,
+                                    ctypes.c_float, ctypes.c_int32, ctypes.c_int32, _P, ctypes.c_size_t, _P]),
+    "rl_muon_workspace_bytes": (ctypes.c_size_t, [ctypes.c_int64, ctypes.c_int64]),
     "rl_workspace_bytes": (ctypes.c_size_t, [ctypes.POINTER(rl_lm_shape), ctypes.c_int32, ctypes.c_int64]),
     "rl_workspace_bytes_hostio": (ctypes.c_size_t, [ctypes.POINTER(rl_lm_shape), ctypes.c_int32]),
     "rl_default_dz_chunk_rows": (ctypes.c_int64, [ctypes.POINTER(rl_lm_shape)]),
@@ -331,6 +337,30 @@ def rl_bwd_ex(shape: rl_lm_shape, hidden, w_vocab, targets, lse, coef, d_hidden=
 def rl_nvls_flag_count(shape: rl_lm_shape, which: int) -> int:
     """Flag entries for an NVLS reduction of d_w_vocab (0) or d_hidden_f32 (1)."""
     return int(load_library().rl_nvls_flag_count(ctypes.byref(shape), int(which)))
+
+
+def rl_newton_schulz(g: torch.Tensor, steps: int = 5, out: torch.Tensor | None = None, workspace=None,
+                     stream=None) -> torch.Tensor:
+    """Muon's Newton-Schulz orthogonalisation of an fp32 [M, N] matrix -> bf16 [M, N]."""
+    M, N = g.shape
+    if out is None:
+        out = torch.empty(M, N, dtype=torch.bfloat16, device=g.device)
+    ws = workspace if workspace is not None else alloc_workspace(
+        load_library().rl_newton_schulz_workspace_bytes(M, N), g.device)
+    _check(load_library().rl_newton_schulz(_ptr(g), M, N, int(steps), _ptr(out), _ptr(ws), ws.numel(),
+                                           _stream(stream)))
+    return out
+
+
+def rl_muon_step(theta: torch.Tensor, grad: torch.Tensor, momentum: torch.Tensor, lr: float, mu: float = 0.95,
+                 weight_decay: float = 0.0, nesterov: bool = True, steps: int = 5, workspace=None, stream=None):
+    """One Muon update of an fp32 [M, N] parameter (theta and momentum in place)."""
+    M, N = theta.shape
+    ws = workspace if workspace is not None else alloc_workspace(load_library().rl_muon_workspace_bytes(M, N),
+                                                                 theta.device)
+    _check(load_library().rl_muon_step(_ptr(theta), _ptr(grad), _ptr(momentum), M, N, float(lr), float(mu),
+                                       float(weight_decay), 1 if nesterov else 0, int(steps), _ptr(ws), ws.numel(),
+                                       _stream(stream)))
 
 
 def rl_last_launch_count() -> int:

@@ -206,7 +206,8 @@ constexpr int stages_for() {
 
 template <int MODE, bool A_MN, bool B_MN, int CG>
 rl_status launch_gemm_cg(int kid, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c, int64_t M,
-                         int64_t N, int64_t K, int group_m, const rl::EpiParams& ep, int sms, cudaStream_t st) {
+                         int64_t N, int64_t K, int group_m, const rl::EpiParams& ep, int sms, cudaStream_t st,
+                         int k_splits = 1, int split_rows = 0) {
   constexpr int S = stages_for<CG>();
   auto kern = rl::gemm_kernel<MODE, A_MN, B_MN, CG, S>;
   constexpr int smem = rl::gemm_smem_bytes<CG, S>();
@@ -222,7 +223,14 @@ rl_status launch_gemm_cg(int kid, const CUtensorMap& a, const CUtensorMap& b, co
   sh.k_blocks = static_cast<int>((K + rl::BK - 1) / rl::BK);
   sh.group_m = group_m;
   if (sh.k_blocks == 0) return fail(RL_ERR_SHAPE, "GEMM with K = 0");
-  const int64_t tiles = static_cast<int64_t>(sh.m_blocks) * sh.n_blocks;
+  if (k_splits < 1) k_splits = 1;
+  if (k_splits > sh.k_blocks) k_splits = sh.k_blocks;
+  sh.k_per_split = (sh.k_blocks + k_splits - 1) / k_splits;
+  sh.k_splits = (sh.k_blocks + sh.k_per_split - 1) / sh.k_per_split;
+  sh.split_rows = split_rows;
+  if (sh.k_splits > 1 && (MODE == rl::EPI_LSE || MODE == rl::EPI_DZ || MODE == rl::EPI_F32_NVLS))
+    return fail(RL_ERR_UNSUPPORTED, "split-K needs a plain store epilogue");
+  const int64_t tiles = static_cast<int64_t>(sh.m_blocks) * sh.n_blocks * sh.k_splits;
   const int units = static_cast<int>(tiles < sms / CG ? tiles : sms / CG);
   rl::EpiParams ep2 = ep;
   ep2.sync_every = 0;
@@ -259,11 +267,12 @@ rl_status launch_gemm_cg(int kid, const CUtensorMap& a, const CUtensorMap& b, co
 
 template <int MODE, bool A_MN, bool B_MN>
 rl_status launch_gemm(int kid, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c, int64_t M, int64_t N,
-                      int64_t K, int group_m, const rl::EpiParams& ep, int sms, cudaStream_t st) {
+                      int64_t K, int group_m, const rl::EpiParams& ep, int sms, cudaStream_t st, int k_splits = 1,
+                      int split_rows = 0) {
   if (M <= 0 || N <= 0) return RL_OK;
   if (cta_group() == 2)
-    return launch_gemm_cg<MODE, A_MN, B_MN, 2>(kid, a, b, c, M, N, K, group_m, ep, sms, st);
-  return launch_gemm_cg<MODE, A_MN, B_MN, 1>(kid, a, b, c, M, N, K, group_m, ep, sms, st);
+    return launch_gemm_cg<MODE, A_MN, B_MN, 2>(kid, a, b, c, M, N, K, group_m, ep, sms, st, k_splits, split_rows);
+  return launch_gemm_cg<MODE, A_MN, B_MN, 1>(kid, a, b, c, M, N, K, group_m, ep, sms, st, k_splits, split_rows);
 }
 
 // Rows of A staged per CTA per tile (the TMA box height for A loads).
@@ -505,6 +514,124 @@ rl_status bwd_impl(const rl_lm_shape* s, const uint16_t* hidden, const uint16_t*
         RL_TRY((launch_gemm<rl::EPI_F32, false, true>(RL_K_DH_GEMM, t_dz_k, t_w_mn, t_dh, rows, H, V, group_m_for(RL_K_DH_GEMM, 8), e5, sms, st)));
       }
     }
+  }
+  return RL_OK;
+}
+
+// ------------------------------------------------------- Newton-Schulz (f3)
+struct NsLayout {
+  size_t xa, xb, g32, g16, g2, c16, parts, partials, sync, u, o, end;
+  int64_t K;
+  int splits;  // split-K of the Gram GEMM (its K x K output has few tiles)
+};
+constexpr int kNsMaxSplits = 8;
+constexpr int kNsPartials = 1184;
+
+NsLayout ns_layout(int64_t M, int64_t N, bool muon) {
+  NsLayout l;
+  Carve c;
+  const int64_t K = M < N ? M : N;
+  l.K = K;
+  l.xa = c.take(static_cast<size_t>(M) * N * 2);
+  l.xb = c.take(static_cast<size_t>(M) * N * 2);
+  l.g32 = c.take(static_cast<size_t>(K) * K * 4);
+  l.g16 = c.take(static_cast<size_t>(K) * K * 2);
+  l.g2 = c.take(static_cast<size_t>(K) * K * 4);
+  l.c16 = c.take(static_cast<size_t>(K) * K * 2);
+  // splits: enough Gram tiles for >= 8 waves of CTA pairs, each split >= 64 k-blocks
+  const int64_t tiles = ((K + 255) / 256) * ((K + 255) / 256);
+  const int64_t kdim = M < N ? N : M;
+  int sp = static_cast<int>((8 * 74 + tiles - 1) / tiles);
+  while (sp > 1 && (kdim / 64) / sp < 64) --sp;
+  l.splits = sp < 1 ? 1 : (sp > kNsMaxSplits ? kNsMaxSplits : sp);
+  l.parts = c.take(static_cast<size_t>(l.splits) * K * K * 4);
+  l.partials = c.take(kNsPartials * 8);
+  l.sync = c.take(static_cast<size_t>(kMaxSyncPoints) * 4);
+  l.u = muon ? c.take(static_cast<size_t>(M) * N * 4) : 0;
+  l.o = muon ? c.take(static_cast<size_t>(M) * N * 2) : 0;
+  l.end = align_up(c.off, 1024);
+  return l;
+}
+
+rl_status check_ns_shape(int64_t M, int64_t N, int32_t steps) {
+  if (M < 1 || N < 1 || M > (int64_t(1) << 31) - 1 || N > 65536) return fail(RL_ERR_SHAPE, "need 1 <= M and 1 <= N <= 65536");
+  const int64_t K = M < N ? M : N;
+  if (N % 8 != 0 || K % 8 != 0) return fail(RL_ERR_SHAPE, "N and min(M, N) must be multiples of 8");
+  if (K > 16384) return fail(RL_ERR_SHAPE, "min(M, N) > 16384 (the K x K Gram would not fit the design)");
+  if (steps < 1) return fail(RL_ERR_INVALID_ARGUMENT, "steps must be >= 1");
+  return RL_OK;
+}
+
+// X_0 from g (fp32) in l.xa, then `steps` iterations; the last one writes `out`.
+rl_status ns_impl(const float* g, int64_t M, int64_t N, int32_t steps, uint16_t* out, uint8_t* ws, const NsLayout& l,
+                  int sms, cudaStream_t st) {
+  constexpr float ca = 3.4445f, cb = -4.7750f, cc = 2.0315f;
+  const int64_t K = l.K, n = M * N;
+  const bool tall = M >= N;
+  uint16_t* xa = reinterpret_cast<uint16_t*>(ws + l.xa);
+  uint16_t* xb = reinterpret_cast<uint16_t*>(ws + l.xb);
+  float* g32 = reinterpret_cast<float*>(ws + l.g32);
+  uint16_t* g16 = reinterpret_cast<uint16_t*>(ws + l.g16);
+  float* g2 = reinterpret_cast<float*>(ws + l.g2);
+  uint16_t* c16 = reinterpret_cast<uint16_t*>(ws + l.c16);
+  double* partials = reinterpret_cast<double*>(ws + l.partials);
+  g_sync_ctr = reinterpret_cast<uint32_t*>(ws + l.sync);
+  const int eblocks = 8 * sms;
+  {
+    ProfScope ps(RL_K_NS_AUX, st);
+    rl::sumsq_partial_kernel<<<kNsPartials, 256, 0, st>>>(g, n, partials);
+  }
+  RL_CHECK_LAUNCH();
+  {
+    ProfScope ps(RL_K_NS_AUX, st);
+    rl::ns_prep_kernel<<<eblocks, 256, 0, st>>>(g, n, partials, kNsPartials, xa);
+  }
+  RL_CHECK_LAUNCH();
+  float* parts = reinterpret_cast<float*>(ws + l.parts);
+  CUtensorMap t_g32, t_g16k, t_g16m, t_g2, t_c16m, t_c16k;
+  RL_TRY(make_map(&t_g32, parts, true, K, K * l.splits, K, 32, 32));   // split s -> rows [s K, s K + K)
+  RL_TRY(make_map(&t_g16k, g16, false, K, K, K, 64, kARows));
+  RL_TRY(make_map(&t_g16m, g16, false, K, K, K, 64, 64));
+  RL_TRY(make_map(&t_g2, g2, true, K, K, K, 32, 32));
+  RL_TRY(make_map(&t_c16m, c16, false, K, K, K, 64, 64));
+  RL_TRY(make_map(&t_c16k, c16, false, K, K, K, 64, kARows));
+  rl::EpiParams e = {};
+  uint16_t* src = xa;
+  for (int j = 0; j < steps; ++j) {
+    uint16_t* dst = (j == steps - 1) ? out : (src == xa ? xb : xa);
+    CUtensorMap t_xk, t_xm, t_xb, t_out;
+    RL_TRY(make_map(&t_xk, src, false, N, M, N, 64, kARows));          // X K-major (rows of X)
+    RL_TRY(make_map(&t_xm, src, false, N, M, N, 64, 64));              // X MN-major
+    RL_TRY(make_map(&t_xb, src, false, N, M, N, 64, rl::BN / cta_group()));  // X as a K-major B
+    RL_TRY(make_map(&t_out, dst, false, N, M, N, 64, 32));
+    e.rows = K;
+    e.cols = K;
+    if (tall) {  // A = X^T X : [N x N], K-dim = M
+      RL_TRY((launch_gemm<rl::EPI_F32, true, true>(RL_K_NS_GEMM, t_xm, t_xm, t_g32, N, N, M, 8, e, sms, st,
+                                                   l.splits, static_cast<int>(K))));
+    } else {     // A = X X^T : [M x M], K-dim = N
+      RL_TRY((launch_gemm<rl::EPI_F32, false, false>(RL_K_NS_GEMM, t_xk, t_xb, t_g32, M, M, N, 8, e, sms, st,
+                                                     l.splits, static_cast<int>(K))));
+    }
+    {
+      ProfScope ps(RL_K_NS_AUX, st);
+      rl::split_reduce_cast_kernel<<<eblocks, 256, 0, st>>>(parts, l.splits, K * K, g32, g16);
+    }
+    RL_CHECK_LAUNCH();
+    RL_TRY((launch_gemm<rl::EPI_F32, false, true>(RL_K_NS_GEMM, t_g16k, t_g16m, t_g2, K, K, K, 8, e, sms, st)));
+    {
+      ProfScope ps(RL_K_NS_AUX, st);
+      rl::ns_poly_kernel<<<eblocks, 256, 0, st>>>(g32, g2, K, ca, cb, cc, c16);
+    }
+    RL_CHECK_LAUNCH();
+    e.rows = M;
+    e.cols = N;
+    if (tall) {  // X' = X C : [M x N], K-dim = N
+      RL_TRY((launch_gemm<rl::EPI_BF16, false, true>(RL_K_NS_GEMM, t_xk, t_c16m, t_out, M, N, N, 8, e, sms, st)));
+    } else {     // X' = C X : [M x N], K-dim = M
+      RL_TRY((launch_gemm<rl::EPI_BF16, false, true>(RL_K_NS_GEMM, t_c16k, t_xm, t_out, M, N, M, 8, e, sms, st)));
+    }
+    src = dst;
   }
   return RL_OK;
 }
@@ -928,6 +1055,71 @@ rl_status rl_policy_loss_fwd_bwd_hostio(const rl_lm_shape* shape, const rl_loss_
   if (s != RL_OK) return s;
   RL_CUDA(cudaMemcpyAsync(report_host, out->report, sizeof(rl_loss_report), cudaMemcpyDeviceToHost, st));
   RL_CUDA(cudaStreamSynchronize(st));
+  return RL_OK;
+}
+
+size_t rl_newton_schulz_workspace_bytes(int64_t M, int64_t N) {
+  if (check_ns_shape(M, N, 1) != RL_OK) return 0;
+  return ns_layout(M, N, false).end;
+}
+
+size_t rl_muon_workspace_bytes(int64_t M, int64_t N) {
+  if (check_ns_shape(M, N, 1) != RL_OK) return 0;
+  return ns_layout(M, N, true).end;
+}
+
+rl_status rl_newton_schulz(const float* g, int64_t M, int64_t N, int32_t steps, uint16_t* out, void* workspace,
+                           size_t workspace_bytes, void* stream) {
+  g_launches = 0;
+  RL_TRY(check_ns_shape(M, N, steps));
+  RL_NONNULL(g);
+  RL_NONNULL(out);
+  if (!aligned16(g) || !aligned16(out) || !aligned16(workspace))
+    return fail(RL_ERR_ALIGNMENT, "g, out and workspace must be 16-byte aligned");
+  const NsLayout l = ns_layout(M, N, false);
+  if (!workspace || workspace_bytes < l.end)
+    return fail(RL_ERR_WORKSPACE, "workspace needs %zu bytes, got %zu", l.end, workspace_bytes);
+  DevInfo d;
+  RL_TRY(device_info(d));
+  return ns_impl(g, M, N, steps, out, static_cast<uint8_t*>(workspace), l, d.sms, static_cast<cudaStream_t>(stream));
+}
+
+rl_status rl_muon_step(float* theta, const float* grad, float* momentum, int64_t M, int64_t N, float lr, float mu,
+                       float weight_decay, int32_t nesterov, int32_t steps, void* workspace, size_t workspace_bytes,
+                       void* stream) {
+  g_launches = 0;
+  RL_TRY(check_ns_shape(M, N, steps));
+  RL_NONNULL(theta);
+  RL_NONNULL(grad);
+  RL_NONNULL(momentum);
+  if (!aligned16(theta) || !aligned16(grad) || !aligned16(momentum) || !aligned16(workspace))
+    return fail(RL_ERR_ALIGNMENT, "theta, grad, momentum and workspace must be 16-byte aligned");
+  if (!isfinite(lr) || !isfinite(mu) || !isfinite(weight_decay))
+    return fail(RL_ERR_INVALID_ARGUMENT, "lr, mu and weight_decay must be finite");
+  const NsLayout l = ns_layout(M, N, true);
+  if (!workspace || workspace_bytes < l.end)
+    return fail(RL_ERR_WORKSPACE, "workspace needs %zu bytes, got %zu", l.end, workspace_bytes);
+  DevInfo d;
+  RL_TRY(device_info(d));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  uint8_t* ws = static_cast<uint8_t*>(workspace);
+  float* u = reinterpret_cast<float*>(ws + l.u);
+  uint16_t* o = reinterpret_cast<uint16_t*>(ws + l.o);
+  const int64_t n = M * N;
+  const int eblocks = 4 * d.sms;
+  {
+    ProfScope ps(RL_K_NS_AUX, st);
+    rl::muon_momentum_kernel<<<eblocks, 256, 0, st>>>(grad, momentum, u, n, mu, nesterov ? 1 : 0);
+  }
+  RL_CHECK_LAUNCH();
+  RL_TRY(ns_impl(u, M, N, steps, o, ws, l, d.sms, st));
+  const double scale = sqrt(M > N ? static_cast<double>(M) / N : 1.0);
+  {
+    ProfScope ps(RL_K_NS_AUX, st);
+    rl::muon_apply_kernel<<<eblocks, 256, 0, st>>>(theta, o, n, 1.f - lr * weight_decay,
+                                                   static_cast<float>(lr * scale));
+  }
+  RL_CHECK_LAUNCH();
   return RL_OK;
 }
 

@@ -53,7 +53,16 @@ constexpr int gemm_smem_bytes() {
 struct GemmShape {
   int m_blocks, n_blocks, k_blocks;  // m_blocks counts TILE_M-row tiles
   int group_m;                       // raster: tiles walk n inside groups of group_m m-blocks
+  int k_splits;                      // split-K: tile t covers k-blocks of split t / (m_blocks*n_blocks)
+  int k_per_split;                   // k-blocks per split
+  int split_rows;                    // store epilogues: split s writes rows offset by s*split_rows
 };
+
+__device__ __forceinline__ void tile_k_range(int tile, const GemmShape& sh, int& kb0, int& kb1) {
+  const int ks = tile / (sh.m_blocks * sh.n_blocks);
+  kb0 = ks * sh.k_per_split;
+  kb1 = min(sh.k_blocks, kb0 + sh.k_per_split);
+}
 
 struct EpiParams {
   int64_t rows;          // valid rows of D (M)
@@ -94,6 +103,7 @@ __device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
 }
 
 __device__ __forceinline__ void tile_coords(int tile, const GemmShape& sh, int& m, int& n) {
+  tile %= sh.m_blocks * sh.n_blocks;  // split-K: the split index is the outer coordinate
   const int per_group = sh.group_m * sh.n_blocks;
   const int g = tile / per_group;
   const int first_m = g * sh.group_m;
@@ -211,7 +221,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  const int total = sh.m_blocks * sh.n_blocks;
+  const int total = sh.m_blocks * sh.n_blocks * sh.k_splits;
 
   if (warp == 0) {
     // ------------------------------------------------------------- producer
@@ -226,7 +236,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       tile_coords(tile, sh, m, n);
       const int a_row = m * TL::TILE_M + rank * TL::A_ROWS;
       const int b_row = n * BN + rank * TL::B_ROWS;
-      for (int kb = 0; kb < sh.k_blocks; ++kb, ++gk) {
+      int kb0, kb1;
+      tile_k_range(tile, sh, kb0, kb1);
+      for (int kb = kb0; kb < kb1; ++kb, ++gk) {
         if (ep.sync_every > 0 && gk > 0 && gk % ep.sync_every == 0) {
           const int p = gk / ep.sync_every;
           if (lane == 0) {
@@ -301,7 +313,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         mbar_wait(&tempty[acc], aph ^ 1);
         tc_fence_after();
         const uint32_t d = tmem_base + acc * BN;
-        for (int kb = 0; kb < sh.k_blocks; ++kb) {
+        int kb0, kb1;
+        tile_k_range(tile, sh, kb0, kb1);
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&full[s], ph);
           tc_fence_after();
           if (elect_one()) {
@@ -312,9 +326,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
               const uint64_t ad = A_MN ? sw128_desc(a0 + k * 2048, 8192, 1024) : sw128_desc(a0 + k * 32, 16, 1024);
               const uint64_t bd = B_MN ? sw128_desc(b0 + k * 2048, 8192, 1024) : sw128_desc(b0 + k * 32, 16, 1024);
               if constexpr (CG == 2)
-                umma_bf16_pair(d, ad, bd, idesc, (kb | k) != 0);
+                umma_bf16_pair(d, ad, bd, idesc, (kb != kb0) || (k != 0));
               else
-                umma_bf16(d, ad, bd, idesc, (kb | k) != 0);
+                umma_bf16(d, ad, bd, idesc, (kb != kb0) || (k != 0));
             }
             if constexpr (CG == 2)
               umma_commit_pair(&empty[s], 0x3);
@@ -477,7 +491,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           __syncwarp();
           if (lane == 0) {
             const int c0 = n0 + c * COLS;
-            const int c1 = m * TL::TILE_M + rank * 128 + q * 32;
+            const int c1 = m * TL::TILE_M + rank * 128 + q * 32 + (tile / (sh.m_blocks * sh.n_blocks)) * sh.split_rows;
             if constexpr (MODE == EPI_F32_ADD)
               tma_reduce_add_2d(&tmC, sEpi + (buf - smem_u32(sEpi)), c0, c1);
             else

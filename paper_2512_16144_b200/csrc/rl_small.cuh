@@ -4,6 +4,7 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <math.h>
+#include <cuda_bf16.h>
 #include <stdint.h>
 
 #include "../../include/rl.h"
@@ -291,6 +292,104 @@ __global__ void loss_finalize_kernel(const RolloutPartial* __restrict__ rp, int 
   r.loss = -loss;
   r.mismatch_kl_sum = kl;
   *rep = r;
+}
+
+// ------------------------------------------------------- Newton-Schulz aux
+// Frobenius norm: per-block fp64 partial sums of squares (fixed order), then every
+// block of the cast kernel re-sums the partials in index order (deterministic).
+__global__ void sumsq_partial_kernel(const float* __restrict__ g, int64_t n, double* __restrict__ partials) {
+  __shared__ double sh[256];
+  // 128-bit loads, 4 independent fp32 squares per load folded into one fp64 accumulator
+  double acc = 0.0;
+  const int64_t n4 = n / 4;
+  const float4* g4 = reinterpret_cast<const float4*>(g);
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n4; i += stride) {
+    const float4 v = g4[i];
+    acc += static_cast<double>(v.x * v.x + v.y * v.y) + static_cast<double>(v.z * v.z + v.w * v.w);
+  }
+  for (int64_t i = n4 * 4 + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const double v = g[i];
+    acc += v * v;
+  }
+  const double tot = block_reduce_sum(acc, sh);
+  if (threadIdx.x == 0) partials[blockIdx.x] = tot;
+}
+
+__device__ __forceinline__ uint16_t f32_to_bf16_bits(float x) {
+  return __bfloat16_as_ushort(__float2bfloat16_rn(x));
+}
+
+// X_0 = bf16(g / (||g||_F + eps)); optionally u = g + mu*m first (Muon, fused).
+__global__ void ns_prep_kernel(const float* __restrict__ g, int64_t n, const double* __restrict__ partials,
+                               int nparts, uint16_t* __restrict__ x0) {
+  // every block re-sums the partials with the same fixed-order tree -> identical norms
+  __shared__ double sh[256];
+  double part = 0.0;
+  for (int i = threadIdx.x; i < nparts; i += blockDim.x) part += partials[i];
+  const double tot = block_reduce_sum(part, sh);
+  const float s = static_cast<float>(1.0 / (sqrt(tot) + 1e-7));
+  const int64_t n4 = n / 4;
+  const float4* g4 = reinterpret_cast<const float4*>(g);
+  uint2* x4 = reinterpret_cast<uint2*>(x0);
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n4; i += stride) {
+    const float4 v = g4[i];
+    uint2 o;
+    o.x = static_cast<uint32_t>(f32_to_bf16_bits(v.x * s)) | (static_cast<uint32_t>(f32_to_bf16_bits(v.y * s)) << 16);
+    o.y = static_cast<uint32_t>(f32_to_bf16_bits(v.z * s)) | (static_cast<uint32_t>(f32_to_bf16_bits(v.w * s)) << 16);
+    x4[i] = o;
+  }
+  for (int64_t i = n4 * 4 + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
+    x0[i] = f32_to_bf16_bits(g[i] * s);
+}
+
+__global__ void cast_bf16_kernel(const float* __restrict__ a, int64_t n, uint16_t* __restrict__ out) {
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    out[i] = f32_to_bf16_bits(a[i]);
+}
+
+// Split-K reduction in index order (deterministic): out32 = sum_s parts[s], out16 = bf16(out32).
+__global__ void split_reduce_cast_kernel(const float* __restrict__ parts, int splits, int64_t n,
+                                         float* __restrict__ out32, uint16_t* __restrict__ out16) {
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    float acc = parts[i];
+    for (int s = 1; s < splits; ++s) acc += parts[static_cast<int64_t>(s) * n + i];
+    out32[i] = acc;
+    out16[i] = f32_to_bf16_bits(acc);
+  }
+}
+
+// C = bf16(a I + b A + c A2) for K x K matrices.
+__global__ void ns_poly_kernel(const float* __restrict__ A, const float* __restrict__ A2, int64_t K, float ca,
+                               float cb, float cc, uint16_t* __restrict__ C) {
+  const int64_t n = K * K;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const float diag = (i / K == i % K) ? ca : 0.f;
+    C[i] = f32_to_bf16_bits(diag + cb * A[i] + cc * A2[i]);
+  }
+}
+
+// Muon momentum: m <- mu m + g; u = nesterov ? g + mu m : m (fp32, in place on m, u out).
+__global__ void muon_momentum_kernel(const float* __restrict__ g, float* __restrict__ m, float* __restrict__ u,
+                                     int64_t n, float mu, int nesterov) {
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const float mi = mu * m[i] + g[i];
+    m[i] = mi;
+    u[i] = nesterov ? g[i] + mu * mi : mi;
+  }
+}
+
+// theta <- theta (1 - lr wd) - lr * scale * O  (O bf16 from Newton-Schulz).
+__global__ void muon_apply_kernel(float* __restrict__ theta, const uint16_t* __restrict__ o, int64_t n, float decay,
+                                  float step) {
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    theta[i] = theta[i] * decay - step * __bfloat162float(__ushort_as_bfloat16(o[i]));
 }
 
 }  // namespace rl
