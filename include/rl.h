@@ -278,6 +278,18 @@ rl_status rl_muon_step(float* theta, const float* grad, float* momentum, int64_t
                        void* stream);
 size_t rl_muon_workspace_bytes(int64_t M, int64_t N);
 
+/* -------------------------------- MoE grouped GEMM */
+/* out[r, :] = a[r, :] . b[g]^T for every row r of group g = [offsets[g], offsets[g+1]):
+ * the torch._grouped_mm that PAPER.md Fig. 5 times for the MoE expert projections
+ * (§2.1.8; hidden 4096, MoE dim 1408 at the GLM-4.5-Air shape).
+ *   a: [rows, K] bf16 (tokens permuted so each expert's rows are contiguous)
+ *   b: [n_groups, N, K] bf16 (each expert's nn.Linear weight, no transpose)
+ *   offsets: [n_groups + 1] int32, DEVICE, non-decreasing, 0 .. rows (values are
+ *            clamped to that range on the device; they are not otherwise validated)
+ *   out: [rows, N] bf16.  K % 8 == 0, N % 32 == 0, 1 <= n_groups <= 1024. */
+rl_status rl_grouped_gemm(const uint16_t* a, const uint16_t* b, const int32_t* offsets, int32_t n_groups,
+                          int64_t rows, int64_t N, int64_t K, uint16_t* out, void* stream);
+
 /* ------------------------------------------------------------ utilities */
 /* Workspace needed by rl_logprob_fwd / rl_policy_loss_fwd_bwd / the split
  * phases for this shape. dz_chunk_rows = rows of the bf16 dU buffer (0 = T). */
@@ -313,7 +325,8 @@ typedef enum rl_kernel_id {
   RL_K_DW_GEMM = 7,    /* K6 S6 dW (+)= dU^T h (tcgen05)         */
   RL_K_MEMSET = 8,     /* zero fill of an empty batch's dW       */
   RL_K_NS_GEMM = 9,    /* Newton-Schulz / Muon GEMMs (tcgen05)   */
-  RL_K_NS_AUX = 10     /* Newton-Schulz / Muon SIMT kernels      */
+  RL_K_NS_AUX = 10,    /* Newton-Schulz / Muon SIMT kernels      */
+  RL_K_GROUPED_GEMM = 11 /* MoE grouped GEMM (tcgen05)           */
 } rl_kernel_id;
 
 typedef struct rl_kernel_time {

@@ -79,7 +79,8 @@ class rl_kernel_time(ctypes.Structure):
 
 
 KERNEL_NAMES = {0: "K0_group_adv", 1: "K1_fwd_gemm_lse", 2: "K2_merge", 3: "K3_loss_coef", 4: "K3b_finalize",
-                5: "K4_bwd_dz_gemm", 6: "K5_dh_gemm", 7: "K6_dw_gemm", 8: "memset", 9: "NS_gemm", 10: "NS_aux"}
+                5: "K4_bwd_dz_gemm", 6: "K5_dh_gemm", 7: "K6_dw_gemm", 8: "memset", 9: "NS_gemm", 10: "NS_aux",
+                11: "grouped_gemm"}
 
 REPORT_BYTES = ctypes.sizeof(rl_loss_report)
 assert REPORT_BYTES == 48
@@ -111,6 +112,8 @@ _SIGS = {
     "rl_muon_step": (ctypes.c_int, [_P, _P, _P, ctypes.c_int64, ctypes.c_int64, ctypes.c_float, ctypes.c_float,
                                     ctypes.c_float, ctypes.c_int32, ctypes.c_int32, _P, ctypes.c_size_t, _P]),
     "rl_muon_workspace_bytes": (ctypes.c_size_t, [ctypes.c_int64, ctypes.c_int64]),
+    "rl_grouped_gemm": (ctypes.c_int, [_P, _P, _P, ctypes.c_int32, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
+                                       _P, _P]),
     "rl_workspace_bytes": (ctypes.c_size_t, [ctypes.POINTER(rl_lm_shape), ctypes.c_int32, ctypes.c_int64]),
     "rl_workspace_bytes_hostio": (ctypes.c_size_t, [ctypes.POINTER(rl_lm_shape), ctypes.c_int32]),
     "rl_default_dz_chunk_rows": (ctypes.c_int64, [ctypes.POINTER(rl_lm_shape)]),
@@ -361,6 +364,20 @@ def rl_muon_step(theta: torch.Tensor, grad: torch.Tensor, momentum: torch.Tensor
     _check(load_library().rl_muon_step(_ptr(theta), _ptr(grad), _ptr(momentum), M, N, float(lr), float(mu),
                                        float(weight_decay), 1 if nesterov else 0, int(steps), _ptr(ws), ws.numel(),
                                        _stream(stream)))
+
+
+def rl_grouped_gemm(a: torch.Tensor, b: torch.Tensor, offsets: torch.Tensor, out: torch.Tensor | None = None,
+                    stream=None) -> torch.Tensor:
+    """MoE grouped GEMM: out[r] = a[r] @ b[g(r)].T with int32 group offsets [G+1] on the device."""
+    rows, K = a.shape
+    G, N, K2 = b.shape
+    if K2 != K or offsets.numel() != G + 1 or offsets.dtype != torch.int32:
+        raise RLError(2, "shapes: a [rows, K], b [G, N, K], offsets int32 [G + 1]")
+    if out is None:
+        out = torch.empty(rows, N, dtype=torch.bfloat16, device=a.device)
+    _check(load_library().rl_grouped_gemm(_ptr(_bf16(a, "a")), _ptr(_bf16(b, "b")), _ptr(offsets), G, rows, N, K,
+                                          _ptr(out), _stream(stream)))
+    return out
 
 
 def rl_last_launch_count() -> int:

@@ -275,6 +275,51 @@ rl_status launch_gemm(int kid, const CUtensorMap& a, const CUtensorMap& b, const
   return launch_gemm_cg<MODE, A_MN, B_MN, 1>(kid, a, b, c, M, N, K, group_m, ep, sms, st, k_splits, split_rows);
 }
 
+// Grouped GEMM (MoE experts): the tile count is only known on the device (it
+// depends on the group offsets), so the grid is sized from an upper bound.
+template <int CG>
+rl_status launch_grouped_cg(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c, int64_t rows,
+                            int64_t N, int64_t K, int n_groups, const rl::EpiParams& ep, int sms, cudaStream_t st) {
+  constexpr int S = CG == 2 ? 5 : 3;
+  auto kern = rl::gemm_kernel<rl::EPI_BF16_GROUPED, false, false, CG, S>;
+  constexpr int smem = rl::gemm_smem_bytes<CG, S, true>();
+  static bool attr_set = false;
+  if (!attr_set) {
+    RL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    attr_set = true;
+  }
+  using TL = rl::Tiling<CG>;
+  rl::GemmShape sh = {};
+  sh.n_blocks = static_cast<int>((N + rl::BN - 1) / rl::BN);
+  sh.m_blocks = static_cast<int>((rows + TL::TILE_M - 1) / TL::TILE_M) + n_groups;  // bound on group m-blocks
+  sh.k_blocks = static_cast<int>((K + rl::BK - 1) / rl::BK);
+  sh.group_m = 1;
+  sh.k_splits = 1;
+  sh.k_per_split = sh.k_blocks;
+  const int64_t tiles = static_cast<int64_t>(sh.m_blocks) * sh.n_blocks;
+  const int units = static_cast<int>(tiles < sms / CG ? tiles : sms / CG);
+  rl::EpiParams e = ep;
+  e.sync_every = 0;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(units * CG);
+  cfg.blockDim = dim3(rl::GEMM_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CG;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  {
+    ProfScope ps(RL_K_GROUPED_GEMM, st);
+    RL_CUDA(cudaLaunchKernelEx(&cfg, kern, a, b, c, sh, e));
+  }
+  RL_CHECK_LAUNCH();
+  return RL_OK;
+}
+
 // Rows of A staged per CTA per tile (the TMA box height for A loads).
 constexpr int kARows = 128;
 
@@ -1121,6 +1166,37 @@ rl_status rl_muon_step(float* theta, const float* grad, float* momentum, int64_t
   }
   RL_CHECK_LAUNCH();
   return RL_OK;
+}
+
+
+rl_status rl_grouped_gemm(const uint16_t* a, const uint16_t* b, const int32_t* offsets, int32_t n_groups, int64_t rows,
+                          int64_t N, int64_t K, uint16_t* out, void* stream) {
+  g_launches = 0;
+  if (n_groups < 1 || n_groups > rl::MAX_GROUPS) return fail(RL_ERR_SHAPE, "need 1 <= n_groups <= %d", rl::MAX_GROUPS);
+  if (rows < 0 || rows > (int64_t(1) << 31) - 1 || N < 32 || N % 32 != 0 || K < 8 || K % 8 != 0 ||
+      static_cast<int64_t>(n_groups) * N > (int64_t(1) << 31) - 1)
+    return fail(RL_ERR_SHAPE, "need rows >= 0, N a positive multiple of 32, K a positive multiple of 8");
+  if (rows == 0) return RL_OK;
+  RL_NONNULL(a);
+  RL_NONNULL(b);
+  RL_NONNULL(offsets);
+  RL_NONNULL(out);
+  if (!aligned16(a) || !aligned16(b) || !aligned16(out)) return fail(RL_ERR_ALIGNMENT, "a, b and out must be 16-byte aligned");
+  DevInfo d;
+  RL_TRY(device_info(d));
+  CUtensorMap ta, tb, tc;
+  RL_TRY(make_map(&ta, a, false, K, rows, K, 64, kARows));
+  RL_TRY(make_map(&tb, b, false, K, static_cast<int64_t>(n_groups) * N, K, 64, rl::BN / cta_group()));
+  RL_TRY(make_map(&tc, out, false, N, rows, N, 64, 32));
+  rl::EpiParams ep = {};
+  ep.rows = rows;
+  ep.cols = N;
+  ep.group_offsets = offsets;
+  ep.n_groups = n_groups;
+  ep.grouped_out = out;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (cta_group() == 2) return launch_grouped_cg<2>(ta, tb, tc, rows, N, K, n_groups, ep, d.sms, st);
+  return launch_grouped_cg<1>(ta, tb, tc, rows, N, K, n_groups, ep, d.sms, st);
 }
 
 }  // extern "C"

@@ -31,7 +31,16 @@ constexpr int EPI_BUF_BYTES = 32 * 128;  // one warp's 32-row x 128-byte store c
 constexpr int EPI_BYTES = 4 * 2 * EPI_BUF_BYTES;
 constexpr int BAR_BYTES = 256;
 
-enum EpiMode { EPI_LSE = 0, EPI_DZ = 1, EPI_BF16 = 2, EPI_F32 = 3, EPI_F32_ADD = 4, EPI_F32_NVLS = 5 };
+enum EpiMode {
+  EPI_LSE = 0,
+  EPI_DZ = 1,
+  EPI_BF16 = 2,
+  EPI_F32 = 3,
+  EPI_F32_ADD = 4,
+  EPI_F32_NVLS = 5,
+  EPI_BF16_GROUPED = 6  // grouped GEMM (MoE experts): row groups from device offsets, masked bf16 stores
+};
+constexpr int MAX_GROUPS = 1024;
 
 constexpr int NVLS_MAX_RANKS = 8;
 
@@ -45,9 +54,9 @@ struct Tiling {
   static constexpr int STAGE = A_STAGE + B_STAGE;
 };
 
-template <int CG, int STAGES>
+template <int CG, int STAGES, bool GROUPED = false>
 constexpr int gemm_smem_bytes() {
-  return 1024 + STAGES * Tiling<CG>::STAGE + EPI_BYTES + BAR_BYTES;
+  return 1024 + STAGES * Tiling<CG>::STAGE + EPI_BYTES + BAR_BYTES + (GROUPED ? (MAX_GROUPS + 1) * 4 : 0);
 }
 
 struct GemmShape {
@@ -86,6 +95,11 @@ struct EpiParams {
   // Every warp stores its 32-row slab locally (TMA), then publishes flag[slab] =
   // epoch; the rank owning the tile (tile % world) later sums the slab over all
   // replicas with multimem.ld_reduce and writes the sum to all with multimem.st.
+  // EPI_BF16_GROUPED: D rows [off[g], off[g+1]) = A rows of the group times B_g^T,
+  // B_g = rows [g * cols, (g + 1) * cols) of B; D is bf16 [rows][cols] at `grouped_out`.
+  const int32_t* group_offsets;            // [n_groups + 1], device
+  int n_groups;
+  uint16_t* grouped_out;
   float* nvls_mc;                          // multicast VA of D ([rows][cols], fp32)
   uint32_t* nvls_flags[NVLS_MAX_RANKS];    // every rank's flag array ([rank] is local)
   int nvls_rank, nvls_world;
@@ -120,6 +134,19 @@ __device__ __forceinline__ void stage_row(uint32_t buf, int row, const uint32_t 
     const uint32_t addr = buf + row * 128 + ((j ^ (row & 7)) << 4);
     st_shared_v4(addr, w[4 * j], w[4 * j + 1], w[4 * j + 2], w[4 * j + 3]);
   }
+}
+
+// Group row range, clamped to [0, rows] and to a non-decreasing sequence, so bad
+// offsets can skip work but never address memory outside A or D.
+__device__ __forceinline__ int grp_begin(const EpiParams& ep, int g) {
+  const int64_t v = ep.group_offsets[g];
+  return static_cast<int>(v < 0 ? 0 : (v > ep.rows ? ep.rows : v));
+}
+__device__ __forceinline__ int grp_end(const EpiParams& ep, int g) {
+  const int64_t v = ep.group_offsets[g + 1];
+  const int e = static_cast<int>(v < 0 ? 0 : (v > ep.rows ? ep.rows : v));
+  const int b = grp_begin(ep, g);
+  return e < b ? b : e;
 }
 
 // Slab = 32 accumulator rows of one tile owned by one epilogue warp.
@@ -182,6 +209,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  constexpr bool GROUPED = MODE == EPI_BF16_GROUPED;
+  int* s_prefix = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(full) + BAR_BYTES);  // GROUPED only
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -204,6 +233,19 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     tma_prefetch(&tmB);
     if (MODE != EPI_LSE) tma_prefetch(&tmC);
   }
+  if constexpr (GROUPED) {
+    // tiles per group: ceil(rows_g / TILE_M) * n_blocks (n fastest inside a group); the
+    // counts are loaded by all threads in parallel, then prefix-summed from smem
+    for (int g = threadIdx.x; g < ep.n_groups; g += blockDim.x) {
+      const int rows_g = grp_end(ep, g) - grp_begin(ep, g);
+      s_prefix[g + 1] = (rows_g + TL::TILE_M - 1) / TL::TILE_M * sh.n_blocks;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      s_prefix[0] = 0;
+      for (int g = 1; g <= ep.n_groups; ++g) s_prefix[g] += s_prefix[g - 1];
+    }
+  }
   if (warp == 1) {
     if constexpr (CG == 2) {
       tmem_alloc2(tmem_slot, 512);
@@ -221,7 +263,20 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  const int total = sh.m_blocks * sh.n_blocks * sh.k_splits;
+  const int total = GROUPED ? s_prefix[ep.n_groups] : sh.m_blocks * sh.n_blocks * sh.k_splits;
+  // grouped tiles -> (group, first A row, row end, n); otherwise the raster of tile_coords
+  auto group_tile = [&](int tile, int& g, int& row0, int& row_end, int& n) {
+    int lo = 0, hi = ep.n_groups - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (s_prefix[mid] <= tile) lo = mid; else hi = mid - 1;
+    }
+    g = lo;
+    const int local = tile - s_prefix[g];
+    row0 = grp_begin(ep, g) + (local / sh.n_blocks) * TL::TILE_M;
+    row_end = grp_end(ep, g);
+    n = local % sh.n_blocks;
+  };
 
   if (warp == 0) {
     // ------------------------------------------------------------- producer
@@ -232,12 +287,20 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     int gk = 0;            // k-blocks issued by this CTA so far (all tiles)
     int last_sync = 0;
     for (int tile = unit; tile < total; tile += n_units) {
-      int m, n;
-      tile_coords(tile, sh, m, n);
-      const int a_row = m * TL::TILE_M + rank * TL::A_ROWS;
-      const int b_row = n * BN + rank * TL::B_ROWS;
-      int kb0, kb1;
-      tile_k_range(tile, sh, kb0, kb1);
+      int m, n, a_row, b_row;
+      if constexpr (GROUPED) {
+        int g, row0, row_end;
+        group_tile(tile, g, row0, row_end, n);
+        a_row = row0 + rank * TL::A_ROWS;
+        b_row = static_cast<int>(g * ep.cols) + n * BN + rank * TL::B_ROWS;
+        (void)m;
+      } else {
+        tile_coords(tile, sh, m, n);
+        a_row = m * TL::TILE_M + rank * TL::A_ROWS;
+        b_row = n * BN + rank * TL::B_ROWS;
+      }
+      int kb0 = 0, kb1 = sh.k_blocks;
+      if constexpr (!GROUPED) tile_k_range(tile, sh, kb0, kb1);
       for (int kb = kb0; kb < kb1; ++kb, ++gk) {
         if (ep.sync_every > 0 && gk > 0 && gk % ep.sync_every == 0) {
           const int p = gk / ep.sync_every;
@@ -313,8 +376,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         mbar_wait(&tempty[acc], aph ^ 1);
         tc_fence_after();
         const uint32_t d = tmem_base + acc * BN;
-        int kb0, kb1;
-        tile_k_range(tile, sh, kb0, kb1);
+        int kb0 = 0, kb1 = sh.k_blocks;
+        if constexpr (!GROUPED) tile_k_range(tile, sh, kb0, kb1);
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&full[s], ph);
           tc_fence_after();
@@ -376,10 +439,23 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       }
     };
     for (int tile = unit; tile < total; tile += n_units) {
-      int m, n;
-      tile_coords(tile, sh, m, n);
-      const int64_t row = static_cast<int64_t>(m) * TL::TILE_M + r_in_tile;
-      const bool row_ok = row < ep.rows;
+      int m = 0, n;
+      int64_t row;
+      bool row_ok;
+      int tile_row0 = 0;        // first D row of the tile (grouped)
+      bool masked = false;      // grouped tile crossing a group end or the N tail
+      if constexpr (GROUPED) {
+        int g, row0, row_end;
+        group_tile(tile, g, row0, row_end, n);
+        row = static_cast<int64_t>(row0) + r_in_tile;
+        row_ok = row < row_end;
+        tile_row0 = row0;
+        masked = row0 + TL::TILE_M > row_end || static_cast<int64_t>(n + 1) * BN > ep.cols;
+      } else {
+        tile_coords(tile, sh, m, n);
+        row = static_cast<int64_t>(m) * TL::TILE_M + r_in_tile;
+        row_ok = row < ep.rows;
+      }
       const int n0 = n * BN;
       mbar_wait_sleep(&tfull[acc], aph);
       tc_fence_after();
@@ -434,6 +510,26 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           constexpr float LN2 = 0.69314718055994530942f;
           ep.partials[static_cast<int64_t>(n) * ep.rows + row] = make_float4(mrun * LN2, srun, trun * LN2, zt);
         }
+      } else if (GROUPED && masked) {
+        // masked per-row stores: rows past the group's end belong to the next group
+        const int64_t cleft = ep.cols - n0;
+        const int ncols = cleft < BN ? static_cast<int>(cleft) : BN;
+        uint16_t* orow = ep.grouped_out + row * ep.cols + n0;
+#pragma unroll 1
+        for (int c = 0; c < BN / 32; ++c) {
+          uint32_t r[32];
+          tmem_ld32(taddr + c * 32, r);
+          tmem_wait_ld();
+          if (c == BN / 32 - 1) release_tmem(acc);
+          if (row_ok && c * 32 < ncols) {
+            uint32_t w[16];
+#pragma unroll
+            for (int j = 0; j < 16; ++j) w[j] = pack_bf16x2(__uint_as_float(r[2 * j]), __uint_as_float(r[2 * j + 1]));
+            uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) dst[j] = make_uint4(w[4 * j], w[4 * j + 1], w[4 * j + 2], w[4 * j + 3]);
+          }
+        }
       } else {
         // store epilogues: TMEM -> regs -> (math) -> swizzled smem -> TMA store
         float g = 0.f, b2 = 0.f;
@@ -447,7 +543,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             tl = (yl < ep.cols && t64 >= 0 && t64 < BN) ? static_cast<int>(t64) : -1;
           }
         }
-        constexpr int COLS = (MODE == EPI_DZ || MODE == EPI_BF16) ? 64 : 32;  // columns per 128-byte chunk
+        constexpr int COLS = (MODE == EPI_DZ || MODE == EPI_BF16 || MODE == EPI_BF16_GROUPED) ? 64 : 32;
 #pragma unroll 1
         for (int c = 0; c < BN / COLS; ++c) {
           uint32_t w[32];
@@ -491,7 +587,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           __syncwarp();
           if (lane == 0) {
             const int c0 = n0 + c * COLS;
-            const int c1 = m * TL::TILE_M + rank * 128 + q * 32 + (tile / (sh.m_blocks * sh.n_blocks)) * sh.split_rows;
+            const int c1 = GROUPED ? tile_row0 + rank * 128 + q * 32
+                                   : m * TL::TILE_M + rank * 128 + q * 32 +
+                                         (tile / (sh.m_blocks * sh.n_blocks)) * sh.split_rows;
             if constexpr (MODE == EPI_F32_ADD)
               tma_reduce_add_2d(&tmC, sEpi + (buf - smem_u32(sEpi)), c0, c1);
             else
