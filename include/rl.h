@@ -35,6 +35,9 @@
  *    gets coef = 0.
  *  - Every 16-byte-vectorised pointer (hidden, W_vocab, d_hidden, d_w_vocab,
  *    workspace) must be 16-byte aligned; H must be a multiple of 8.
+ *  - A workspace belongs to one call at a time: calls that may execute
+ *    concurrently (different streams) need different workspaces (the GEMMs keep
+ *    their soft k-barrier counters there; rl_bwd_ex phases also keep dU there).
  */
 #ifndef RL_H_
 #define RL_H_
