@@ -289,9 +289,16 @@ size_t rl_muon_workspace_bytes(int64_t M, int64_t N);
  *   b: [n_groups, N, K] bf16 (each expert's nn.Linear weight, no transpose)
  *   offsets: [n_groups + 1] int32, DEVICE, non-decreasing, 0 .. rows (values are
  *            clamped to that range on the device; they are not otherwise validated)
+ *   row_scale: NULL or [rows] fp32: out[r, :] = row_scale[r] * (a[r, :] . b[g]^T), applied
+ *            to the fp32 accumulator. With row_scale = rl_rms_inv(a) and b = W o gamma
+ *            (the RMSNorm weight folded into the expert weights along K) this is the
+ *            expert GEMM of RMSNorm(x): diag(1/rms(x)) x (W o gamma)^T.
  *   out: [rows, N] bf16.  K % 8 == 0, N % 32 == 0, 1 <= n_groups <= 1024. */
 rl_status rl_grouped_gemm(const uint16_t* a, const uint16_t* b, const int32_t* offsets, int32_t n_groups,
-                          int64_t rows, int64_t N, int64_t K, uint16_t* out, void* stream);
+                          int64_t rows, int64_t N, int64_t K, const float* row_scale, uint16_t* out, void* stream);
+
+/* out[r] = 1 / sqrt(mean_k x[r, k]^2 + eps) for bf16 x [rows, K] (the RMSNorm scale). */
+rl_status rl_rms_inv(const uint16_t* x, int64_t rows, int64_t K, float eps, float* out, void* stream);
 
 /* ------------------------------------------------------------ utilities */
 /* Workspace needed by rl_logprob_fwd / rl_policy_loss_fwd_bwd / the split

@@ -30,3 +30,14 @@ def max_violation(expert_load: np.ndarray) -> float:
     """MaxViolation = (max_i Load_i - mean Load) / mean Load."""
     load = np.asarray(expert_load, np.float64)
     return float((load.max() - load.mean()) / load.mean())
+
+
+def rmsnorm(x: np.ndarray, gamma: np.ndarray, eps: float = 1e-6) -> np.ndarray:
+    """RMSNorm(x) = x / sqrt(mean(x^2) + eps) * gamma, per row (the pre-MoE norm)."""
+    x = np.asarray(x, np.float64)
+    return x / np.sqrt((x * x).mean(axis=1, keepdims=True) + eps) * np.asarray(gamma, np.float64)
+
+
+def grouped_mm_rmsnorm(x, gamma, b, offsets, eps=1e-6) -> np.ndarray:
+    """The expert projection of normalised tokens: grouped_mm(RMSNorm(x), b, offsets)."""
+    return grouped_mm(rmsnorm(x, gamma, eps), b, offsets)

@@ -113,7 +113,8 @@ _SIGS = {
                                     ctypes.c_float, ctypes.c_int32, ctypes.c_int32, _P, ctypes.c_size_t, _P]),
     "rl_muon_workspace_bytes": (ctypes.c_size_t, [ctypes.c_int64, ctypes.c_int64]),
     "rl_grouped_gemm": (ctypes.c_int, [_P, _P, _P, ctypes.c_int32, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
-                                       _P, _P]),
+                                       _P, _P, _P]),
+    "rl_rms_inv": (ctypes.c_int, [_P, ctypes.c_int64, ctypes.c_int64, ctypes.c_float, _P, _P]),
     "rl_workspace_bytes": (ctypes.c_size_t, [ctypes.POINTER(rl_lm_shape), ctypes.c_int32, ctypes.c_int64]),
     "rl_workspace_bytes_hostio": (ctypes.c_size_t, [ctypes.POINTER(rl_lm_shape), ctypes.c_int32]),
     "rl_default_dz_chunk_rows": (ctypes.c_int64, [ctypes.POINTER(rl_lm_shape)]),
@@ -367,8 +368,8 @@ def rl_muon_step(theta: torch.Tensor, grad: torch.Tensor, momentum: torch.Tensor
 
 
 def rl_grouped_gemm(a: torch.Tensor, b: torch.Tensor, offsets: torch.Tensor, out: torch.Tensor | None = None,
-                    stream=None) -> torch.Tensor:
-    """MoE grouped GEMM: out[r] = a[r] @ b[g(r)].T with int32 group offsets [G+1] on the device."""
+                    row_scale: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """MoE grouped GEMM: out[r] = row_scale[r] * (a[r] @ b[g(r)].T), int32 group offsets [G+1] on the device."""
     rows, K = a.shape
     G, N, K2 = b.shape
     if K2 != K or offsets.numel() != G + 1 or offsets.dtype != torch.int32:
@@ -376,7 +377,16 @@ def rl_grouped_gemm(a: torch.Tensor, b: torch.Tensor, offsets: torch.Tensor, out
     if out is None:
         out = torch.empty(rows, N, dtype=torch.bfloat16, device=a.device)
     _check(load_library().rl_grouped_gemm(_ptr(_bf16(a, "a")), _ptr(_bf16(b, "b")), _ptr(offsets), G, rows, N, K,
-                                          _ptr(out), _stream(stream)))
+                                          _ptr(row_scale), _ptr(out), _stream(stream)))
+    return out
+
+
+def rl_rms_inv(x: torch.Tensor, eps: float = 1e-6, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """1 / sqrt(mean(x^2) + eps) per row of a bf16 [rows, K] matrix."""
+    rows, K = x.shape
+    if out is None:
+        out = torch.empty(rows, dtype=torch.float32, device=x.device)
+    _check(load_library().rl_rms_inv(_ptr(_bf16(x, "x")), rows, K, float(eps), _ptr(out), _stream(stream)))
     return out
 
 

@@ -181,20 +181,43 @@ int group_m_for(int kid, int dflt) {
 // (default 2). Keeping the CTAs that share operands inside one L2 window cuts
 // K5/K6 DRAM reads by ~1/3 and lets the power-capped clock rise (~6% per step,
 // profiles/r01/). Correctness never depends on it (the wait is bounded).
-int sync_every_for(int kid) {
-  static int every = [] {
-    const char* e = getenv("RL_SYNC_EVERY");
-    return e ? atoi(e) : 32;
-  }();
-  (void)kid;
-  return every;
+// Per-GEMM overrides: RL_SYNC_EVERY_<K>, RL_SYNC_SLACK_<K> (K in FWD, DZ, DH, DW, NS).
+const char* kid_suffix(int kid) {
+  switch (kid) {
+    case RL_K_FWD_GEMM: return "FWD";
+    case RL_K_DZ_GEMM: return "DZ";
+    case RL_K_DH_GEMM: return "DH";
+    case RL_K_DW_GEMM: return "DW";
+    case RL_K_NS_GEMM: return "NS";
+    default: return "OTHER";
+  }
 }
-int sync_slack() {
-  static int slack = [] {
-    const char* e = getenv("RL_SYNC_SLACK");
-    return e ? atoi(e) : 2;
-  }();
-  return slack;
+int env_int(const char* base, int kid, int dflt) {
+  char name[64];
+  snprintf(name, sizeof(name), "%s_%s", base, kid_suffix(kid));
+  const char* e = getenv(name);
+  if (!e) e = getenv(base);
+  return e ? atoi(e) : dflt;
+}
+int sync_every_for(int kid) {
+  static int cache[32];
+  static bool init[32] = {};
+  if (kid < 0 || kid >= 32) return 0;
+  if (!init[kid]) {
+    cache[kid] = env_int("RL_SYNC_EVERY", kid, 32);
+    init[kid] = true;
+  }
+  return cache[kid];
+}
+int sync_slack_for(int kid) {
+  static int cache[32];
+  static bool init[32] = {};
+  if (kid < 0 || kid >= 32) return 2;
+  if (!init[kid]) {
+    cache[kid] = env_int("RL_SYNC_SLACK", kid, 2);
+    init[kid] = true;
+  }
+  return cache[kid];
 }
 constexpr int kMaxSyncPoints = 1 << 16;
 thread_local uint32_t* g_sync_ctr = nullptr;  // set per call from the workspace
@@ -241,7 +264,7 @@ rl_status launch_gemm_cg(int kid, const CUtensorMap& a, const CUtensorMap& b, co
       RL_CUDA(cudaMemsetAsync(g_sync_ctr, 0, static_cast<size_t>(max_sync + 1) * 4, st));
       ep2.sync_ctr = g_sync_ctr;
       ep2.sync_every = sync_every_for(kid);
-      ep2.sync_slack = sync_slack();
+      ep2.sync_slack = sync_slack_for(kid);
       ep2.max_sync = static_cast<int>(max_sync);
     }
   }
@@ -1103,6 +1126,25 @@ rl_status rl_policy_loss_fwd_bwd_hostio(const rl_lm_shape* shape, const rl_loss_
   return RL_OK;
 }
 
+rl_status rl_rms_inv(const uint16_t* x, int64_t rows, int64_t K, float eps, float* out, void* stream) {
+  g_launches = 0;
+  if (rows < 0 || K < 1) return fail(RL_ERR_SHAPE, "need rows >= 0 and K >= 1");
+  if (!(eps >= 0.f) || !isfinite(eps)) return fail(RL_ERR_INVALID_ARGUMENT, "eps must be finite and >= 0");
+  if (rows == 0) return RL_OK;
+  RL_NONNULL(x);
+  RL_NONNULL(out);
+  DevInfo d;
+  RL_TRY(device_info(d));
+  const int64_t threads = rows * 32;
+  {
+    ProfScope ps(RL_K_NS_AUX, static_cast<cudaStream_t>(stream));
+    rl::rms_inv_kernel<<<static_cast<unsigned>((threads + 255) / 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+        x, rows, K, eps, out);
+  }
+  RL_CHECK_LAUNCH();
+  return RL_OK;
+}
+
 size_t rl_newton_schulz_workspace_bytes(int64_t M, int64_t N) {
   if (check_ns_shape(M, N, 1) != RL_OK) return 0;
   return ns_layout(M, N, false).end;
@@ -1170,7 +1212,7 @@ rl_status rl_muon_step(float* theta, const float* grad, float* momentum, int64_t
 
 
 rl_status rl_grouped_gemm(const uint16_t* a, const uint16_t* b, const int32_t* offsets, int32_t n_groups, int64_t rows,
-                          int64_t N, int64_t K, uint16_t* out, void* stream) {
+                          int64_t N, int64_t K, const float* row_scale, uint16_t* out, void* stream) {
   g_launches = 0;
   if (n_groups < 1 || n_groups > rl::MAX_GROUPS) return fail(RL_ERR_SHAPE, "need 1 <= n_groups <= %d", rl::MAX_GROUPS);
   if (rows < 0 || rows > (int64_t(1) << 31) - 1 || N < 32 || N % 32 != 0 || K < 8 || K % 8 != 0 ||
@@ -1194,6 +1236,7 @@ rl_status rl_grouped_gemm(const uint16_t* a, const uint16_t* b, const int32_t* o
   ep.group_offsets = offsets;
   ep.n_groups = n_groups;
   ep.grouped_out = out;
+  ep.row_scale = row_scale;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (cta_group() == 2) return launch_grouped_cg<2>(ta, tb, tc, rows, N, K, n_groups, ep, d.sms, st);
   return launch_grouped_cg<1>(ta, tb, tc, rows, N, K, n_groups, ep, d.sms, st);

@@ -100,6 +100,7 @@ struct EpiParams {
   const int32_t* group_offsets;            // [n_groups + 1], device
   int n_groups;
   uint16_t* grouped_out;
+  const float* row_scale;                  // optional [rows]: D[r, :] *= row_scale[r] (fused RMSNorm)
   float* nvls_mc;                          // multicast VA of D ([rows][cols], fp32)
   uint32_t* nvls_flags[NVLS_MAX_RANKS];    // every rank's flag array ([rank] is local)
   int nvls_rank, nvls_world;
@@ -515,6 +516,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         const int64_t cleft = ep.cols - n0;
         const int ncols = cleft < BN ? static_cast<int>(cleft) : BN;
         uint16_t* orow = ep.grouped_out + row * ep.cols + n0;
+        const float rs = (ep.row_scale && row_ok) ? ep.row_scale[row] : 1.f;
 #pragma unroll 1
         for (int c = 0; c < BN / 32; ++c) {
           uint32_t r[32];
@@ -524,7 +526,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           if (row_ok && c * 32 < ncols) {
             uint32_t w[16];
 #pragma unroll
-            for (int j = 0; j < 16; ++j) w[j] = pack_bf16x2(__uint_as_float(r[2 * j]), __uint_as_float(r[2 * j + 1]));
+            for (int j = 0; j < 16; ++j)
+              w[j] = pack_bf16x2(__uint_as_float(r[2 * j]) * rs, __uint_as_float(r[2 * j + 1]) * rs);
             uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
 #pragma unroll
             for (int j = 0; j < 4; ++j) dst[j] = make_uint4(w[4 * j], w[4 * j + 1], w[4 * j + 2], w[4 * j + 3]);
@@ -534,6 +537,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         // store epilogues: TMEM -> regs -> (math) -> swizzled smem -> TMA store
         float g = 0.f, b2 = 0.f;
         int tl = -1;
+        const float rs = (GROUPED && ep.row_scale && row_ok) ? ep.row_scale[row] : 1.f;
         if constexpr (MODE == EPI_DZ) {
           if (row_ok) {
             g = ep.coef[row] * ep.inv_temperature;
@@ -567,6 +571,12 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                 if (tl == cb + 2 * j + 1) v1 -= g;
                 if (tl == cb + 32 + 2 * j) v2 -= g;
                 if (tl == cb + 32 + 2 * j + 1) v3 -= g;
+              }
+              if constexpr (GROUPED) {
+                v0 *= rs;
+                v1 *= rs;
+                v2 *= rs;
+                v3 *= rs;
               }
               w[j] = pack_bf16x2(v0, v1);
               w[16 + j] = pack_bf16x2(v2, v3);

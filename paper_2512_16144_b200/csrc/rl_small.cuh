@@ -392,4 +392,20 @@ __global__ void muon_apply_kernel(float* __restrict__ theta, const uint16_t* __r
     theta[i] = theta[i] * decay - step * __bfloat162float(__ushort_as_bfloat16(o[i]));
 }
 
+// 1 / sqrt(mean_k x[r, k]^2 + eps) per row (bf16 x), one warp per row, fixed-order sums.
+__global__ void rms_inv_kernel(const uint16_t* __restrict__ x, int64_t rows, int64_t K, float eps,
+                               float* __restrict__ out) {
+  const int64_t r = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (r >= rows) return;
+  const uint16_t* xr = x + r * K;
+  float acc = 0.f;
+  for (int64_t k = lane; k < K; k += 32) {
+    const float v = __bfloat162float(__ushort_as_bfloat16(xr[k]));
+    acc = fmaf(v, v, acc);
+  }
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) out[r] = rsqrtf(acc / static_cast<float>(K) + eps);
+}
+
 }  // namespace rl

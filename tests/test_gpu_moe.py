@@ -54,3 +54,26 @@ def test_grouped_gemm_vs_oracle(G, N, K, sizes):
         if r1 > r0:
             assert np.linalg.norm(got[r0:r1] - ref[r0:r1]) <= 4e-3 * np.linalg.norm(ref[r0:r1]) + 1e-6
     assert bool((buf[:guard] == 7.0).all()) and bool((buf[-guard:] == 7.0).all())
+
+
+def test_grouped_gemm_fused_rmsnorm():
+    """RMSNorm fused into the expert GEMM: row scale 1/rms(x) on the fp32 accumulator,
+    gamma folded into the weights; vs the oracle's normalise-then-multiply."""
+    rng = np.random.default_rng(3)
+    G, N, K = 8, 1408, 4096
+    n = rng.integers(100, 600, G)
+    off = np.concatenate([[0], np.cumsum(n)]).astype(np.int32)
+    rows = int(off[-1])
+    x = _bf(rng.standard_normal((rows, K)) * rng.uniform(0.5, 3.0, (rows, 1)))
+    gamma = rng.uniform(0.5, 1.5, K)
+    w = rng.standard_normal((G, N, K)) / np.sqrt(K)
+    ref = moe.grouped_mm_rmsnorm(x.float().numpy(), gamma, w, off, eps=1e-6)
+    b = _bf(w * gamma[None, None, :])
+    xs = x.cuda()
+    scale = rl.rl_rms_inv(xs, 1e-6)
+    out = rl.rl_grouped_gemm(xs, b.cuda(), torch.from_numpy(off).cuda(), row_scale=scale)
+    torch.cuda.synchronize()
+    got = out.float().cpu().numpy().astype(np.float64)
+    err = np.linalg.norm(got - ref) / np.linalg.norm(ref)
+    print("rmsnorm-fused", err)
+    assert err <= 5e-3

@@ -33,3 +33,12 @@ def test_max_violation():
     """Balanced load -> 0; one expert with twice the mean... (PAPER.md L204 definition)."""
     assert moe.max_violation(np.full(8, 5.0)) == 0.0
     assert moe.max_violation(np.array([1.0, 1.0, 1.0, 5.0])) == pytest.approx(1.5)
+
+
+def test_rmsnorm_unit_mean_square_and_scale_invariance():
+    x = np.random.default_rng(2).standard_normal((5, 64)) * 3.0
+    y = moe.rmsnorm(x, np.ones(64), eps=0.0)
+    np.testing.assert_allclose((y * y).mean(axis=1), 1.0, atol=1e-12)
+    np.testing.assert_allclose(moe.rmsnorm(7.5 * x, np.ones(64), eps=0.0), y, atol=1e-12)
+    g = np.linspace(0.5, 2.0, 64)
+    np.testing.assert_allclose(moe.rmsnorm(x, g, eps=0.0), y * g, atol=1e-12)
