@@ -391,7 +391,6 @@ def main_ours(args):
     # e2e through the host-I/O C call (pinned inputs in, report out, every step)
     e2e = None
     if not vocab_par and not args.no_e2e:
-        import ctypes  # noqa: F401
         hpin = b["hidden"].view(torch.int16).cpu().pin_memory()
         tpin = targets.cpu().pin_memory()
         ipin = infer.cpu().pin_memory()

@@ -991,15 +991,11 @@ static rl_status step_impl(const rl_lm_shape* shape, const rl_loss_params* param
   } else {
     RL_TRY(forward_impl(shape, hidden, w_vocab, targets, out->logprob, out->entropy, lse, nullptr, ws, L, sms, st));
   }
-  const int fwd = g_launches;
   RL_TRY(loss_impl(params, shape->T, shape->V_global, out->logprob, infer_logprobs, targets, rollout_adv,
                    rollout_offsets, loss_mask, coef, out->token_keep, out->rollout_guarded, out->report,
                    reinterpret_cast<rl::RolloutPartial*>(ws + L.rp), st));
-  const int mid = g_launches;
   RL_TRY(bwd_impl(shape, hidden, w_vocab, targets, lse, coef, out->d_hidden, out->d_hidden_f32, out->d_w_vocab,
                   out->accumulate_dw, ws, L, sms, st, RL_BWD_ALL, out->d_w_vocab_nvls, nullptr));
-  (void)fwd;
-  (void)mid;
   return RL_OK;
 }
 
@@ -1115,11 +1111,9 @@ rl_status rl_policy_loss_fwd_bwd_hostio(const rl_lm_shape* shape, const rl_loss_
   RL_CHECK_LAUNCH();
   rl_loss_outputs o = *out;
   if (!o.logprob) o.logprob = d_lp;
-  const int before = g_launches;
   rl_status s = step_impl(shape, params, d_hidden_in, w_vocab, d_tg, d_inf, d_adv, d_off,
                           loss_mask_host ? d_lm : nullptr, &o, ws, L, d.sms, st, T > 0 ? hs.slab.data() : nullptr,
                           slab);
-  (void)before;
   if (s != RL_OK) return s;
   RL_CUDA(cudaMemcpyAsync(report_host, out->report, sizeof(rl_loss_report), cudaMemcpyDeviceToHost, st));
   RL_CUDA(cudaStreamSynchronize(st));

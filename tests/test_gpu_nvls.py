@@ -1,5 +1,5 @@
 """The in-epilogue NVLink-multicast all-reduce (rl_nvls_reduce) against NCCL on
-2 GPUs (`-m gpu`; skipped with fewer than 2 devices). DP: dW summed over ranks;
+2-4 GPUs (`-m gpu`; skipped with fewer than 2 devices). DP: dW summed over ranks;
 vocab-parallel: dH partials summed over ranks. Both must equal the NCCL
 all-reduce of the same per-rank results up to fp32 summation order."""
 import os
@@ -16,6 +16,8 @@ if not torch.cuda.is_available() or torch.cuda.device_count() < 2:  # pragma: no
 import torch.distributed as dist  # noqa: E402
 import torch.multiprocessing as mp  # noqa: E402
 
+WORLD = min(4, torch.cuda.device_count())
+
 
 def _port():
     s = socket.socket()
@@ -31,8 +33,8 @@ def _worker(rank, port, out_dir, mode):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     torch.cuda.set_device(rank)
     dev = torch.device("cuda", rank)
-    dist.init_process_group("nccl", rank=rank, world_size=2, device_id=dev)
-    wl = synth.Workload("nv", 1, 4, 150, 512, 3000, ragged=True, delta_sigma=0.5)
+    dist.init_process_group("nccl", rank=rank, world_size=WORLD, device_id=dev)
+    wl = synth.Workload("nv", 1, 4, 150, 512, 3008, ragged=True, delta_sigma=0.5)
     T = wl.tokens
     res = {}
     infer = None
@@ -40,7 +42,7 @@ def _worker(rank, port, out_dir, mode):
         if mode == "dp":
             b = synth.make_batch_device(wl, 50 + rank, device=dev, tokens=T)
         else:
-            Vl = wl.vocab // 2
+            Vl = wl.vocab // WORLD
             b = synth.make_batch_device(wl, 50, device=dev, tokens=T, vocab=Vl, vocab_offset=rank * Vl,
                                         vocab_total=wl.vocab)
         offs = torch.from_numpy(b["offsets"]).to(dev)
@@ -72,11 +74,11 @@ def _worker(rank, port, out_dir, mode):
 
 @pytest.mark.parametrize("mode", ["dp", "vocab"])
 def test_nvls_matches_nccl(tmp_path, mode):
-    mp.start_processes(_worker, args=(_port(), str(tmp_path), mode), nprocs=2, start_method="spawn")
-    for r in range(2):
+    mp.start_processes(_worker, args=(_port(), str(tmp_path), mode), nprocs=WORLD, start_method="spawn")
+    for r in range(WORLD):
         d = np.load(tmp_path / f"{mode}{r}.npz")
         a, b = d["nvls"], d["nccl"]
         assert np.abs(b).max() > 0
         np.testing.assert_allclose(a, b, rtol=1e-5, atol=1e-6 * np.abs(b).max())
-    d0, d1 = np.load(tmp_path / f"{mode}0.npz"), np.load(tmp_path / f"{mode}1.npz")
-    assert np.array_equal(d0["nvls"], d1["nvls"])   # one reduced value, written to every replica
+    d = [np.load(tmp_path / f"{mode}{r}.npz")["nvls"] for r in range(WORLD)]
+    assert all(np.array_equal(d[0], x) for x in d[1:])   # one reduced value, written to every replica
