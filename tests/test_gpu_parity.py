@@ -310,3 +310,44 @@ def test_loss_variants_vs_oracle(variant, lo, hi):
     if hi - lo < 0.5:
         assert ref.report.masked_low + ref.report.masked_high > 0      # the clip is exercised
     print(variant, err)
+
+
+def test_cuda_graph_capture_replays_the_step():
+    """The device-side step is capturable in a CUDA graph (no host syncs, no
+    allocations): replay on new inputs equals an eager call bitwise."""
+    c = harness.make_case(RAGGED, 14, tokens=333, vocab=1000, hidden=200)
+    d = harness.to_device(c)
+    b = c.batch
+    T, H, V, R = b.T, b.H, b.V, len(c.adv)
+    shape = rl.make_shape(T, H, V)
+    params = rl.make_params(R, b.loss_denominator)
+    ws = rl.alloc_workspace(rl.rl_workspace_bytes(shape, R))
+    out = {k: torch.empty(T, device="cuda") for k in ("logprob", "coef")}
+    report = rl.new_report()
+    dh = torch.empty(T, H, dtype=torch.bfloat16, device="cuda")
+    dw = torch.empty(V, H, device="cuda")
+    adv = torch.empty(R, device="cuda")
+
+    def step():
+        rl.rl_group_advantages(d["rewards"], b.wl.group_size, adv)
+        rl.rl_policy_loss_fwd_bwd(shape, params, d["hidden"], d["w"], d["targets"], d["infer"], adv, d["offsets"],
+                                  d["loss_mask"], report=report, logprob=out["logprob"], coef=out["coef"],
+                                  d_hidden=dh, d_w_vocab=dw, workspace=ws)
+
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        step()                                   # warm-up (sets kernel attributes)
+    torch.cuda.current_stream().wait_stream(s)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        step()
+    # new inputs in the captured buffers, replay, and compare with an eager run
+    d["hidden"].copy_(torch.roll(d["hidden"], 1, 0))
+    g.replay()
+    torch.cuda.synchronize()
+    got = (out["logprob"].clone(), dh.clone(), dw.clone(), report.clone())
+    step()
+    torch.cuda.synchronize()
+    for a, e in zip(got, (out["logprob"], dh, dw, report)):
+        assert torch.equal(a, e)
