@@ -708,7 +708,7 @@ rl_status ns_impl(const float* g, int64_t M, int64_t N, int32_t steps, uint16_t*
 struct HostioStreams {
   int dev = -1;
   cudaStream_t copy = nullptr;
-  cudaEvent_t start = nullptr;
+  cudaEvent_t start = nullptr, small = nullptr;
   std::vector<cudaEvent_t> slab;
   rl_status ensure(int n) {
     int d = 0;
@@ -716,11 +716,13 @@ struct HostioStreams {
     if (d != dev) {
       copy = nullptr;
       start = nullptr;
+      small = nullptr;
       slab.clear();
       dev = d;
     }
     if (!copy) RL_CUDA(cudaStreamCreateWithFlags(&copy, cudaStreamNonBlocking));
     if (!start) RL_CUDA(cudaEventCreateWithFlags(&start, cudaEventDisableTiming));
+    if (!small) RL_CUDA(cudaEventCreateWithFlags(&small, cudaEventDisableTiming));
     while (static_cast<int>(slab.size()) < n) {
       cudaEvent_t e;
       RL_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -976,14 +978,14 @@ static rl_status step_impl(const rl_lm_shape* shape, const rl_loss_params* param
                            const uint16_t* w_vocab, const int32_t* targets, const float* infer_logprobs,
                            const float* rollout_adv, const int32_t* rollout_offsets, const uint8_t* loss_mask,
                            const rl_loss_outputs* out, uint8_t* ws, const WsLayout& L, int sms, cudaStream_t st,
-                           const cudaEvent_t* slab_events = nullptr, int64_t slab_rows = 0) {
+                           const cudaEvent_t* slab_events = nullptr, const int64_t* slab_ends = nullptr) {
   float* lse = out->lse ? out->lse : reinterpret_cast<float*>(ws + L.lse);
   float* coef = out->coef ? out->coef : reinterpret_cast<float*>(ws + L.coef);
-  if (slab_events && slab_rows > 0 && shape->T > 0) {
+  if (slab_events && slab_ends && shape->T > 0) {
     int j = 0;
-    for (int64_t r0 = 0; r0 < shape->T; r0 += slab_rows, ++j) {
+    for (int64_t r0 = 0; r0 < shape->T; r0 = slab_ends[j], ++j) {
       rl_lm_shape sub = *shape;
-      sub.T = (shape->T - r0 < slab_rows) ? shape->T - r0 : slab_rows;
+      sub.T = slab_ends[j] - r0;
       RL_CUDA(cudaStreamWaitEvent(st, slab_events[j], 0));
       RL_TRY(forward_impl(&sub, hidden + r0 * shape->H, w_vocab, targets + r0, out->logprob + r0,
                           out->entropy ? out->entropy + r0 : nullptr, lse + r0, nullptr, ws, L, sms, st));
@@ -1084,25 +1086,37 @@ rl_status rl_policy_loss_fwd_bwd_hostio(const rl_lm_shape* shape, const rl_loss_
   float* d_lp = reinterpret_cast<float*>(ws + c.take(T * 4));
   // hidden rows go up in slabs on a side stream; the forward starts on slab 0
   // while the rest is in flight (the small per-token vectors go first on `st`)
-  const int64_t slab = 4096;
-  const int n_slabs = static_cast<int>((T + slab - 1) / slab);
+  // slab ends: 1024, 4096, then every 4096 rows (a small first slab shortens the
+  // exposed part of the upload; later slabs keep the forward's tiles large)
+  std::vector<int64_t> ends;
+  for (int64_t e = 1024; ; e = (e < 4096) ? 4096 : e + 4096) {
+    ends.push_back(e < T ? e : T);
+    if (e >= T) break;
+  }
+  const int n_slabs = static_cast<int>(ends.size());
   HostioStreams& hs = hostio_streams();
   RL_TRY(hs.ensure(n_slabs));
+  // every upload goes through the copy stream, in the order the compute needs it:
+  // the small per-token/per-rollout vectors first (event `small`), then the
+  // hidden-state slabs (one event each); H2D copies share the copy engine's FIFO,
+  // so nothing the first kernels need may queue behind the big slabs
+  RL_CUDA(cudaEventRecord(hs.start, st));
+  RL_CUDA(cudaStreamWaitEvent(hs.copy, hs.start, 0));
   if (T > 0) {
-    RL_CUDA(cudaEventRecord(hs.start, st));
-    RL_CUDA(cudaStreamWaitEvent(hs.copy, hs.start, 0));
-    for (int j = 0; j < n_slabs; ++j) {
-      const int64_t r0 = j * slab, rows = (T - r0 < slab) ? T - r0 : slab;
-      RL_CUDA(cudaMemcpyAsync(d_hidden_in + r0 * shape->H, hidden_host + r0 * shape->H, rows * shape->H * 2,
-                              cudaMemcpyHostToDevice, hs.copy));
-      RL_CUDA(cudaEventRecord(hs.slab[j], hs.copy));
-    }
-    RL_CUDA(cudaMemcpyAsync(d_tg, targets_host, T * 4, cudaMemcpyHostToDevice, st));
-    RL_CUDA(cudaMemcpyAsync(d_inf, infer_host, T * 4, cudaMemcpyHostToDevice, st));
-    if (loss_mask_host) RL_CUDA(cudaMemcpyAsync(d_lm, loss_mask_host, T, cudaMemcpyHostToDevice, st));
+    RL_CUDA(cudaMemcpyAsync(d_tg, targets_host, T * 4, cudaMemcpyHostToDevice, hs.copy));
+    RL_CUDA(cudaMemcpyAsync(d_inf, infer_host, T * 4, cudaMemcpyHostToDevice, hs.copy));
+    if (loss_mask_host) RL_CUDA(cudaMemcpyAsync(d_lm, loss_mask_host, T, cudaMemcpyHostToDevice, hs.copy));
   }
-  RL_CUDA(cudaMemcpyAsync(d_rw, rewards_host, R * 4, cudaMemcpyHostToDevice, st));
-  RL_CUDA(cudaMemcpyAsync(d_off, offsets_host, (R + 1) * 4, cudaMemcpyHostToDevice, st));
+  RL_CUDA(cudaMemcpyAsync(d_rw, rewards_host, R * 4, cudaMemcpyHostToDevice, hs.copy));
+  RL_CUDA(cudaMemcpyAsync(d_off, offsets_host, (R + 1) * 4, cudaMemcpyHostToDevice, hs.copy));
+  RL_CUDA(cudaEventRecord(hs.small, hs.copy));
+  for (int j = 0; T > 0 && j < n_slabs; ++j) {
+    const int64_t r0 = j == 0 ? 0 : ends[j - 1], rows = ends[j] - r0;
+    RL_CUDA(cudaMemcpyAsync(d_hidden_in + r0 * shape->H, hidden_host + r0 * shape->H, rows * shape->H * 2,
+                            cudaMemcpyHostToDevice, hs.copy));
+    RL_CUDA(cudaEventRecord(hs.slab[j], hs.copy));
+  }
+  RL_CUDA(cudaStreamWaitEvent(st, hs.small, 0));
   const int ng = static_cast<int>(R / group_size);
   {
     ProfScope ps(RL_K_GROUP_ADV, st);
@@ -1113,7 +1127,7 @@ rl_status rl_policy_loss_fwd_bwd_hostio(const rl_lm_shape* shape, const rl_loss_
   if (!o.logprob) o.logprob = d_lp;
   rl_status s = step_impl(shape, params, d_hidden_in, w_vocab, d_tg, d_inf, d_adv, d_off,
                           loss_mask_host ? d_lm : nullptr, &o, ws, L, d.sms, st, T > 0 ? hs.slab.data() : nullptr,
-                          slab);
+                          T > 0 ? ends.data() : nullptr);
   if (s != RL_OK) return s;
   RL_CUDA(cudaMemcpyAsync(report_host, out->report, sizeof(rl_loss_report), cudaMemcpyDeviceToHost, st));
   RL_CUDA(cudaStreamSynchronize(st));
