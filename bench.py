@@ -325,7 +325,8 @@ def main_ours(args):
         else:
             phases.group_advantages(rewards, wl_rank.group_size, adv)
             phases.full_step(shape, params, hidden, w_loc, targets, infer, adv, offsets, loss_mask, report=report,
-                             logprob=logprob, lse=lse, coef=coef, d_hidden=dh, d_w_vocab=dw, workspace=ws)
+                             logprob=logprob, lse=lse, coef=coef, d_hidden=dh, d_w_vocab=dw, dz_chunk_rows=chunk,
+                             workspace=ws)
         launches[0] = phases.launches
 
     for _ in range(args.warmup):
@@ -400,7 +401,7 @@ def main_ours(args):
         del ws
         if engine is not None:
             engine.ws = None
-        wsh = rl.alloc_workspace(rl.rl_workspace_bytes_hostio(shape, R), dev)
+        wsh = rl.alloc_workspace(rl.rl_workspace_bytes_hostio(shape, R, chunk), dev)
 
         nvls_dp = engine is not None and getattr(engine, "nvls", None) is not None
 
@@ -408,11 +409,13 @@ def main_ours(args):
             if nvls_dp:
                 rl.rl_policy_loss_fwd_bwd_hostio(shape, params, wl_rank.group_size, hpin, b["w"], tpin, ipin, rpin,
                                                  opin, mpin, report=report, d_hidden=dh, d_w_vocab=engine.nvls.buf,
-                                                 d_w_vocab_nvls=engine.nvls.descriptor(), workspace=wsh)
+                                                 d_w_vocab_nvls=engine.nvls.descriptor(), dz_chunk_rows=chunk,
+                                                 workspace=wsh)
                 engine.nvls.barrier()
                 return
             rl.rl_policy_loss_fwd_bwd_hostio(shape, params, wl_rank.group_size, hpin, b["w"], tpin, ipin, rpin, opin,
-                                             mpin, report=report, d_hidden=dh, d_w_vocab=dw, workspace=wsh)
+                                             mpin, report=report, d_hidden=dh, d_w_vocab=dw, dz_chunk_rows=chunk,
+                                             workspace=wsh)
             if world > 1:
                 dist.all_reduce(dw)
 

@@ -147,6 +147,8 @@ typedef struct rl_loss_outputs {
   const rl_nvls_reduce* d_w_vocab_nvls; /* non-NULL: d_w_vocab is all-reduced in the dW
                              GEMM epilogue over NVLS (data-parallel ranks); needs
                              accumulate_dw = 0 and one dU chunk                          */
+  int64_t dz_chunk_rows;   /* rows of the bf16 dU buffer per backward pass; 0 = T (size
+                              the workspace with the same value)                         */
 } rl_loss_outputs;
 
 /* ---------------------------------------------------------------- S0 */
@@ -304,7 +306,7 @@ rl_status rl_rms_inv(const uint16_t* x, int64_t rows, int64_t K, float eps, floa
 /* Workspace needed by rl_logprob_fwd / rl_policy_loss_fwd_bwd / the split
  * phases for this shape. dz_chunk_rows = rows of the bf16 dU buffer (0 = T). */
 size_t rl_workspace_bytes(const rl_lm_shape* shape, int32_t num_rollouts, int64_t dz_chunk_rows);
-size_t rl_workspace_bytes_hostio(const rl_lm_shape* shape, int32_t num_rollouts);
+size_t rl_workspace_bytes_hostio(const rl_lm_shape* shape, int32_t num_rollouts, int64_t dz_chunk_rows);
 
 /* Default dU chunk rows used when dz_chunk_rows == 0 (currently T). */
 int64_t rl_default_dz_chunk_rows(const rl_lm_shape* shape);

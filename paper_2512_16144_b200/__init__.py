@@ -71,7 +71,7 @@ class rl_loss_outputs(ctypes.Structure):
                 ("rollout_guarded", ctypes.c_void_p), ("d_hidden", ctypes.c_void_p),
                 ("d_hidden_f32", ctypes.c_void_p), ("d_w_vocab", ctypes.c_void_p),
                 ("accumulate_dw", ctypes.c_int32), ("_pad", ctypes.c_int32),
-                ("d_w_vocab_nvls", ctypes.POINTER(rl_nvls_reduce))]
+                ("d_w_vocab_nvls", ctypes.POINTER(rl_nvls_reduce)), ("dz_chunk_rows", ctypes.c_int64)]
 
 
 class rl_kernel_time(ctypes.Structure):
@@ -116,7 +116,7 @@ _SIGS = {
                                        _P, _P, _P]),
     "rl_rms_inv": (ctypes.c_int, [_P, ctypes.c_int64, ctypes.c_int64, ctypes.c_float, _P, _P]),
     "rl_workspace_bytes": (ctypes.c_size_t, [ctypes.POINTER(rl_lm_shape), ctypes.c_int32, ctypes.c_int64]),
-    "rl_workspace_bytes_hostio": (ctypes.c_size_t, [ctypes.POINTER(rl_lm_shape), ctypes.c_int32]),
+    "rl_workspace_bytes_hostio": (ctypes.c_size_t, [ctypes.POINTER(rl_lm_shape), ctypes.c_int32, ctypes.c_int64]),
     "rl_default_dz_chunk_rows": (ctypes.c_int64, [ctypes.POINTER(rl_lm_shape)]),
     "rl_status_string": (ctypes.c_char_p, [ctypes.c_int]),
     "rl_last_error_message": (ctypes.c_char_p, []),
@@ -192,8 +192,8 @@ def rl_workspace_bytes(shape: rl_lm_shape, num_rollouts: int = 1, dz_chunk_rows:
     return int(load_library().rl_workspace_bytes(ctypes.byref(shape), int(num_rollouts), int(dz_chunk_rows)))
 
 
-def rl_workspace_bytes_hostio(shape: rl_lm_shape, num_rollouts: int) -> int:
-    return int(load_library().rl_workspace_bytes_hostio(ctypes.byref(shape), int(num_rollouts)))
+def rl_workspace_bytes_hostio(shape: rl_lm_shape, num_rollouts: int, dz_chunk_rows: int = 0) -> int:
+    return int(load_library().rl_workspace_bytes_hostio(ctypes.byref(shape), int(num_rollouts), int(dz_chunk_rows)))
 
 
 def alloc_workspace(nbytes: int, device=None) -> torch.Tensor:
@@ -224,24 +224,25 @@ def rl_logprob_fwd(shape: rl_lm_shape, hidden, w_vocab, targets, logprob, entrop
 
 def _outputs(report, logprob, entropy=None, lse=None, coef=None, token_keep=None, rollout_guarded=None,
              d_hidden=None, d_hidden_f32=None, d_w_vocab=None, accumulate_dw=False,
-             d_w_vocab_nvls=None) -> rl_loss_outputs:
+             d_w_vocab_nvls=None, dz_chunk_rows=0) -> rl_loss_outputs:
     return rl_loss_outputs(_ptr(report), _ptr(logprob), _ptr(entropy), _ptr(lse), _ptr(coef), _ptr(token_keep),
                            _ptr(rollout_guarded), _ptr(d_hidden), _ptr(d_hidden_f32), _ptr(d_w_vocab),
                            1 if accumulate_dw else 0, 0,
-                           ctypes.pointer(d_w_vocab_nvls) if d_w_vocab_nvls is not None else None)
+                           ctypes.pointer(d_w_vocab_nvls) if d_w_vocab_nvls is not None else None,
+                           int(dz_chunk_rows))
 
 
 def rl_policy_loss_fwd_bwd(shape: rl_lm_shape, params: rl_loss_params, hidden, w_vocab, targets, infer_logprobs,
                            rollout_adv, rollout_offsets, loss_mask=None, *, report, logprob, entropy=None,
                            lse=None, coef=None, token_keep=None, rollout_guarded=None, d_hidden=None,
                            d_hidden_f32=None, d_w_vocab=None, accumulate_dw=False, d_w_vocab_nvls=None,
-                           workspace=None, stream=None):
+                           dz_chunk_rows=0, workspace=None, stream=None):
     """S0..S6 on one rank (see include/rl.h). `report` is a [48] uint8 CUDA tensor.
     `d_w_vocab_nvls` (rl_nvls_reduce) all-reduces d_w_vocab over NVLS in the K6 epilogue."""
     ws = workspace if workspace is not None else alloc_workspace(
-        rl_workspace_bytes(shape, params.num_rollouts), w_vocab.device)
+        rl_workspace_bytes(shape, params.num_rollouts, dz_chunk_rows), w_vocab.device)
     out = _outputs(report, logprob, entropy, lse, coef, token_keep, rollout_guarded, d_hidden, d_hidden_f32,
-                   d_w_vocab, accumulate_dw, d_w_vocab_nvls)
+                   d_w_vocab, accumulate_dw, d_w_vocab_nvls, dz_chunk_rows)
     _check(load_library().rl_policy_loss_fwd_bwd(
         ctypes.byref(shape), ctypes.byref(params), _ptr(_bf16(hidden, "hidden")), _ptr(_bf16(w_vocab, "w_vocab")),
         _ptr(targets), _ptr(infer_logprobs), _ptr(rollout_adv), _ptr(rollout_offsets), _ptr(loss_mask),
@@ -251,11 +252,11 @@ def rl_policy_loss_fwd_bwd(shape: rl_lm_shape, params: rl_loss_params, hidden, w
 def rl_policy_loss_fwd_bwd_hostio(shape: rl_lm_shape, params: rl_loss_params, group_size: int, hidden_host,
                                   w_vocab, targets_host, infer_host, rewards_host, offsets_host,
                                   loss_mask_host=None, *, report, d_hidden=None, d_hidden_f32=None,
-                                  d_w_vocab=None, accumulate_dw=False, d_w_vocab_nvls=None, workspace=None,
-                                  stream=None) -> rl_loss_report:
+                                  d_w_vocab=None, accumulate_dw=False, d_w_vocab_nvls=None, dz_chunk_rows=0,
+                                  workspace=None, stream=None) -> rl_loss_report:
     """The same step with per-step inputs in (pinned) host tensors; returns the report."""
     ws = workspace if workspace is not None else alloc_workspace(
-        rl_workspace_bytes_hostio(shape, params.num_rollouts), w_vocab.device)
+        rl_workspace_bytes_hostio(shape, params.num_rollouts, dz_chunk_rows), w_vocab.device)
 
     def hp(t):
         if t is None:
@@ -265,7 +266,7 @@ def rl_policy_loss_fwd_bwd_hostio(shape: rl_lm_shape, params: rl_loss_params, gr
         return ctypes.c_void_p(t.data_ptr())
 
     out = _outputs(report, None, d_hidden=d_hidden, d_hidden_f32=d_hidden_f32, d_w_vocab=d_w_vocab,
-                   accumulate_dw=accumulate_dw, d_w_vocab_nvls=d_w_vocab_nvls)
+                   accumulate_dw=accumulate_dw, d_w_vocab_nvls=d_w_vocab_nvls, dz_chunk_rows=dz_chunk_rows)
     rep = rl_loss_report()
     _check(load_library().rl_policy_loss_fwd_bwd_hostio(
         ctypes.byref(shape), ctypes.byref(params), int(group_size), hp(hidden_host), _ptr(w_vocab),

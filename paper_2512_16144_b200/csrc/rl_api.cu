@@ -793,9 +793,9 @@ size_t rl_workspace_bytes(const rl_lm_shape* shape, int32_t num_rollouts, int64_
   return ws_layout(shape, num_rollouts, dz_chunk_rows).end;
 }
 
-size_t rl_workspace_bytes_hostio(const rl_lm_shape* shape, int32_t num_rollouts) {
+size_t rl_workspace_bytes_hostio(const rl_lm_shape* shape, int32_t num_rollouts, int64_t dz_chunk_rows) {
   if (check_shape(shape) != RL_OK) return 0;
-  const size_t base = ws_layout(shape, num_rollouts, 0).end;
+  const size_t base = ws_layout(shape, num_rollouts, dz_chunk_rows).end;
   Carve c;
   c.off = base;
   const size_t T = static_cast<size_t>(shape->T), R = static_cast<size_t>(num_rollouts > 0 ? num_rollouts : 1);
@@ -1017,6 +1017,9 @@ static rl_status check_step_args(const rl_lm_shape* shape, const rl_loss_params*
   RL_TRY(check_nvls(out->d_w_vocab_nvls, "d_w_vocab_nvls"));
   if (out->d_w_vocab_nvls && (out->accumulate_dw || !out->d_w_vocab))
     return fail(RL_ERR_INVALID_ARGUMENT, "d_w_vocab_nvls needs d_w_vocab and accumulate_dw = 0");
+  if (out->dz_chunk_rows < 0) return fail(RL_ERR_INVALID_ARGUMENT, "dz_chunk_rows must be >= 0");
+  if (out->d_w_vocab_nvls && out->dz_chunk_rows > 0 && out->dz_chunk_rows < shape->T)
+    return fail(RL_ERR_INVALID_ARGUMENT, "d_w_vocab_nvls needs one dU chunk (dz_chunk_rows = 0 or >= T)");
   return RL_OK;
 }
 
@@ -1034,7 +1037,7 @@ rl_status rl_policy_loss_fwd_bwd(const rl_lm_shape* shape, const rl_loss_params*
     RL_NONNULL(infer_logprobs);
     if (!aligned16(hidden)) return fail(RL_ERR_ALIGNMENT, "hidden must be 16-byte aligned");
   }
-  const WsLayout L = ws_layout(shape, params->num_rollouts, 0);
+  const WsLayout L = ws_layout(shape, params->num_rollouts, out->dz_chunk_rows);
   if (!workspace || workspace_bytes < L.end)
     return fail(RL_ERR_WORKSPACE, "workspace needs %zu bytes, got %zu", L.end, workspace_bytes);
   if (!aligned16(workspace)) return fail(RL_ERR_ALIGNMENT, "workspace must be 16-byte aligned");
@@ -1064,7 +1067,7 @@ rl_status rl_policy_loss_fwd_bwd_hostio(const rl_lm_shape* shape, const rl_loss_
     RL_NONNULL(targets_host);
     RL_NONNULL(infer_host);
   }
-  const size_t need = rl_workspace_bytes_hostio(shape, params->num_rollouts);
+  const size_t need = rl_workspace_bytes_hostio(shape, params->num_rollouts, out->dz_chunk_rows);
   if (!workspace || workspace_bytes < need)
     return fail(RL_ERR_WORKSPACE, "workspace needs %zu bytes, got %zu", need, workspace_bytes);
   if (!aligned16(workspace)) return fail(RL_ERR_ALIGNMENT, "workspace must be 16-byte aligned");
@@ -1072,7 +1075,7 @@ rl_status rl_policy_loss_fwd_bwd_hostio(const rl_lm_shape* shape, const rl_loss_
   RL_TRY(device_info(d));
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   uint8_t* ws = static_cast<uint8_t*>(workspace);
-  const WsLayout L = ws_layout(shape, params->num_rollouts, 0);
+  const WsLayout L = ws_layout(shape, params->num_rollouts, out->dz_chunk_rows);
   Carve c;
   c.off = L.end;
   const size_t R = static_cast<size_t>(params->num_rollouts);

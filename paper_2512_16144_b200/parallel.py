@@ -107,11 +107,11 @@ class LibrlPhases:
 
     def full_step(self, shape, params, hidden, w, targets, infer, adv, offsets, loss_mask, *, report, logprob,
                   entropy=None, lse=None, coef=None, keep=None, guarded=None, d_hidden=None, d_w_vocab=None,
-                  d_w_vocab_nvls=None, workspace=None):
+                  d_w_vocab_nvls=None, dz_chunk_rows=0, workspace=None):
         rl_policy_loss_fwd_bwd(shape, params, hidden, w, targets, infer, adv, offsets, loss_mask, report=report,
                                logprob=logprob, entropy=entropy, lse=lse, coef=coef, token_keep=keep,
                                rollout_guarded=guarded, d_hidden=d_hidden, d_w_vocab=d_w_vocab,
-                               d_w_vocab_nvls=d_w_vocab_nvls, workspace=workspace)
+                               d_w_vocab_nvls=d_w_vocab_nvls, dz_chunk_rows=dz_chunk_rows, workspace=workspace)
         self._count()
 
 

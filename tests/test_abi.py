@@ -36,7 +36,7 @@ def test_struct_layouts_match_header(lib):
     assert ctypes.sizeof(rl.rl_lm_shape) == 48
     assert ctypes.sizeof(rl.rl_loss_params) == 32
     assert ctypes.sizeof(rl.rl_loss_report) == 48
-    assert ctypes.sizeof(rl.rl_loss_outputs) == 96
+    assert ctypes.sizeof(rl.rl_loss_outputs) == 104
     assert ctypes.sizeof(rl.rl_nvls_reduce) == 88
     assert lib.rl_abi_version() == 1
 
