@@ -7,8 +7,11 @@ log-softmax epilogue, partial merge, Eq.1/Eq.2/guard coefficients, and the
 backward (dU recompute, dH = dU W, dW = dU^T h), plus the step's collectives.
 
   N = 1 : GLM-4.5-Air-shaped 16k-token micro-batch (H 4096, V 151552), 1 GPU.
-  N > 1 : default "stress" DP (weak scaling): 16k tokens / rank, one G=16 group
-          per rank, heavy off-policy log-probs, dW all-reduce (NCCL) every step.
+  N > 1 : default: the same GLM-16k micro-batch on every rank (data parallel, weak
+          scaling; rank r draws seed 1000 + r), dW all-reduce every step (fused in
+          the dW GEMM epilogue over NVLS when multicast is available, else NCCL).
+          --config stress: 16k tokens / rank, one G=16 group per rank, heavy
+          off-policy log-probs (about a quarter of the tokens masked by Eq.2).
           --config glm64k: vocab-parallel (strong scaling) 64k tokens, W sharded,
           partials all-gather + dH all-reduce (NCCL).
 
@@ -117,7 +120,7 @@ def workload_for(args, world):
     if args.config != "auto":
         name = args.config
     else:
-        name = "glm16k" if world == 1 else "stress"
+        name = "glm16k"
     wl = synth.CONFIGS[name]
     return name, wl
 
@@ -285,7 +288,7 @@ def main_ours(args):
     del logp_ref
 
     from paper_2512_16144_b200 import parallel
-    phases = parallel.LibrlPhases()
+    phases = parallel.LibrlPhases(dense_backward=args.dense_backward)
     adv = torch.empty(R, **f32)
     report = rl.new_report(dev)
     logprob = torch.empty(T, **f32)
@@ -367,9 +370,15 @@ def main_ours(args):
         c[1] += m
     total_k = sum(v[1] for v in per.values())
     kern = {k: {"launches": v[0], "avg_ms": v[1] / v[0], "share": v[1] / (ms * args.steps)} for k, v in per.items()}
-    gemm_rows = T if chunk == 0 else chunk
-    flops = {"K1_fwd_gemm_lse": 2.0 * T * V_local * H, "K4_bwd_dz_gemm": 2.0 * gemm_rows * V_local * H,
-             "K5_dh_gemm": 2.0 * gemm_rows * V_local * H, "K6_dw_gemm": 2.0 * gemm_rows * V_local * H}
+    # the backward GEMMs run over the rows with coef != 0 (sparse backward) unless the
+    # vocab-parallel NVLS dH reduction forces the dense path; FLOPs per launch = the
+    # step's FLOPs of that kernel / its launches per step
+    coef_t = engine.coef if engine is not None else coef
+    dense = args.dense_backward or (vocab_par and args.collective == "nvls")
+    bwd_rows = T if dense else int((coef_t != 0).sum().item())
+    step_kflops = {"K1_fwd_gemm_lse": 2.0 * T * V_local * H, "K4_bwd_dz_gemm": 2.0 * bwd_rows * V_local * H,
+                   "K5_dh_gemm": 2.0 * bwd_rows * V_local * H, "K6_dw_gemm": 2.0 * bwd_rows * V_local * H}
+    flops = {k: f / (per[k][0] / args.steps) for k, f in step_kflops.items() if k in per}
     dom = max((k for k in per if k in flops), key=lambda k: per[k][1])
     peaks, peak_src = load_peaks()
     peak = float(peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops")))
@@ -379,7 +388,9 @@ def main_ours(args):
     if os.path.exists(tpath):
         try:
             # measured for the per-rank GLM-16k shape only (profiles/traffic.json)
-            traffic = json.load(open(tpath)).get(f"{name}:{dom}") if (T, V_local) == (16384, 151552) else None
+            # (one GPU, no fused collective: the NVLS epilogue adds its own traffic)
+            same = (T, V_local) == (16384, 151552) and world == 1
+            traffic = json.load(open(tpath)).get(f"{name}:{dom}") if same else None
         except Exception:
             traffic = None
     step_flops = 8.0 * H * V_local * T   # algorithmic 8HV per token on this rank
@@ -387,7 +398,9 @@ def main_ours(args):
             "frac": achieved / peak, "traffic": traffic,
             "peak_source": f"bf16_tflops_sustained, {peak_src}",
             "step_frac_8HV": (step_flops / (ms_max / 1e3) / 1e12) / peak,
-            "step_frac_8HV_vs_burst": (step_flops / (ms_max / 1e3) / 1e12) / float(peaks.get("bf16_tflops", peak))}
+            "step_frac_8HV_vs_burst": (step_flops / (ms_max / 1e3) / 1e12) / float(peaks.get("bf16_tflops", peak)),
+            "bwd_rows": bwd_rows,
+            "step_frac_executed": (sum(step_kflops.values()) / (ms_max / 1e3) / 1e12) / peak}
 
     # e2e through the host-I/O C call (pinned inputs in, report out, every step)
     e2e = None
@@ -410,12 +423,12 @@ def main_ours(args):
                 rl.rl_policy_loss_fwd_bwd_hostio(shape, params, wl_rank.group_size, hpin, b["w"], tpin, ipin, rpin,
                                                  opin, mpin, report=report, d_hidden=dh, d_w_vocab=engine.nvls.buf,
                                                  d_w_vocab_nvls=engine.nvls.descriptor(), dz_chunk_rows=chunk,
-                                                 workspace=wsh)
+                                                 dense_backward=args.dense_backward, workspace=wsh)
                 engine.nvls.barrier()
                 return
             rl.rl_policy_loss_fwd_bwd_hostio(shape, params, wl_rank.group_size, hpin, b["w"], tpin, ipin, rpin, opin,
                                              mpin, report=report, d_hidden=dh, d_w_vocab=dw, dz_chunk_rows=chunk,
-                                             workspace=wsh)
+                                             dense_backward=args.dense_backward, workspace=wsh)
             if world > 1:
                 dist.all_reduce(dw)
 
@@ -476,6 +489,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--ref-tokens", type=int, default=256)
+    ap.add_argument("--dense-backward", action="store_true",
+                    help="run the backward GEMMs over all rows instead of the coef != 0 rows (A/B)")
     ap.add_argument("--overlap", action="store_true", help="DP + NCCL: all-reduce dW on a side stream under K5")
     ap.add_argument("--collective", default="auto", choices=["auto", "nccl", "nvls"],
                     help="nvls: the dW (DP) / dH (vocab-parallel) all-reduce is fused into the GEMM epilogue "

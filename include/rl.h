@@ -143,7 +143,8 @@ typedef struct rl_loss_outputs {
   float* d_hidden_f32;     /* [T, H] fp32 alternative (vocab-parallel partial); or NULL */
   float* d_w_vocab;        /* [V_local, H] fp32 d loss / d W_vocab; or NULL             */
   int32_t accumulate_dw;   /* 0: d_w_vocab is overwritten; 1: the gradient is added     */
-  int32_t _pad;
+  int32_t dense_backward;  /* 0 (default): the backward GEMMs run over the rows with a
+                              non-zero coef only (RL_BWD_DENSE); 1: over all T rows     */
   const rl_nvls_reduce* d_w_vocab_nvls; /* non-NULL: d_w_vocab is all-reduced in the dW
                              GEMM epilogue over NVLS (data-parallel ranks); needs
                              accumulate_dw = 0 and one dU chunk                          */
@@ -251,6 +252,13 @@ rl_status rl_bwd(const rl_lm_shape* shape, const uint16_t* hidden, const uint16_
 #define RL_BWD_DW 2
 #define RL_BWD_DH 4
 #define RL_BWD_ALL 7
+/* By default the backward runs only over the rows whose coefficient is non-zero
+ * (tokens masked by Eq.2, guarded rollouts, loss_mask = 0 rows have an all-zero dU
+ * row): K3's coef is compacted on the device (order kept), the hidden rows are
+ * gathered, and d_hidden rows of skipped tokens are written as zeros. OR
+ * RL_BWD_DENSE into `phases` to run over every row (bitwise-reproducible either
+ * way; the two differ only in fp32 summation order of dW). dh_nvls forces dense. */
+#define RL_BWD_DENSE 8
 rl_status rl_bwd_ex(const rl_lm_shape* shape, const uint16_t* hidden, const uint16_t* w_vocab,
                     const int32_t* targets, const float* lse, const float* coef, uint16_t* d_hidden,
                     float* d_hidden_f32, float* d_w_vocab, int32_t accumulate_dw, int64_t dz_chunk_rows,
@@ -338,7 +346,8 @@ typedef enum rl_kernel_id {
   RL_K_MEMSET = 8,     /* zero fill of an empty batch's dW       */
   RL_K_NS_GEMM = 9,    /* Newton-Schulz / Muon GEMMs (tcgen05)   */
   RL_K_NS_AUX = 10,    /* Newton-Schulz / Muon SIMT kernels      */
-  RL_K_GROUPED_GEMM = 11 /* MoE grouped GEMM (tcgen05)           */
+  RL_K_GROUPED_GEMM = 11, /* MoE grouped GEMM (tcgen05)          */
+  RL_K_COMPACT = 12    /* sparse-backward compaction / gather / scatter */
 } rl_kernel_id;
 
 typedef struct rl_kernel_time {

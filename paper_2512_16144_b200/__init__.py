@@ -70,7 +70,7 @@ class rl_loss_outputs(ctypes.Structure):
                 ("lse", ctypes.c_void_p), ("coef", ctypes.c_void_p), ("token_keep", ctypes.c_void_p),
                 ("rollout_guarded", ctypes.c_void_p), ("d_hidden", ctypes.c_void_p),
                 ("d_hidden_f32", ctypes.c_void_p), ("d_w_vocab", ctypes.c_void_p),
-                ("accumulate_dw", ctypes.c_int32), ("_pad", ctypes.c_int32),
+                ("accumulate_dw", ctypes.c_int32), ("dense_backward", ctypes.c_int32),
                 ("d_w_vocab_nvls", ctypes.POINTER(rl_nvls_reduce)), ("dz_chunk_rows", ctypes.c_int64)]
 
 
@@ -80,7 +80,7 @@ class rl_kernel_time(ctypes.Structure):
 
 KERNEL_NAMES = {0: "K0_group_adv", 1: "K1_fwd_gemm_lse", 2: "K2_merge", 3: "K3_loss_coef", 4: "K3b_finalize",
                 5: "K4_bwd_dz_gemm", 6: "K5_dh_gemm", 7: "K6_dw_gemm", 8: "memset", 9: "NS_gemm", 10: "NS_aux",
-                11: "grouped_gemm"}
+                11: "grouped_gemm", 12: "compact"}
 
 REPORT_BYTES = ctypes.sizeof(rl_loss_report)
 assert REPORT_BYTES == 48
@@ -224,10 +224,10 @@ def rl_logprob_fwd(shape: rl_lm_shape, hidden, w_vocab, targets, logprob, entrop
 
 def _outputs(report, logprob, entropy=None, lse=None, coef=None, token_keep=None, rollout_guarded=None,
              d_hidden=None, d_hidden_f32=None, d_w_vocab=None, accumulate_dw=False,
-             d_w_vocab_nvls=None, dz_chunk_rows=0) -> rl_loss_outputs:
+             d_w_vocab_nvls=None, dz_chunk_rows=0, dense_backward=False) -> rl_loss_outputs:
     return rl_loss_outputs(_ptr(report), _ptr(logprob), _ptr(entropy), _ptr(lse), _ptr(coef), _ptr(token_keep),
                            _ptr(rollout_guarded), _ptr(d_hidden), _ptr(d_hidden_f32), _ptr(d_w_vocab),
-                           1 if accumulate_dw else 0, 0,
+                           1 if accumulate_dw else 0, 1 if dense_backward else 0,
                            ctypes.pointer(d_w_vocab_nvls) if d_w_vocab_nvls is not None else None,
                            int(dz_chunk_rows))
 
@@ -236,13 +236,14 @@ def rl_policy_loss_fwd_bwd(shape: rl_lm_shape, params: rl_loss_params, hidden, w
                            rollout_adv, rollout_offsets, loss_mask=None, *, report, logprob, entropy=None,
                            lse=None, coef=None, token_keep=None, rollout_guarded=None, d_hidden=None,
                            d_hidden_f32=None, d_w_vocab=None, accumulate_dw=False, d_w_vocab_nvls=None,
-                           dz_chunk_rows=0, workspace=None, stream=None):
+                           dz_chunk_rows=0, dense_backward=False, workspace=None, stream=None):
     """S0..S6 on one rank (see include/rl.h). `report` is a [48] uint8 CUDA tensor.
-    `d_w_vocab_nvls` (rl_nvls_reduce) all-reduces d_w_vocab over NVLS in the K6 epilogue."""
+    `d_w_vocab_nvls` (rl_nvls_reduce) all-reduces d_w_vocab over NVLS in the K6 epilogue.
+    `dense_backward` runs the backward GEMMs over all rows instead of the coef != 0 rows."""
     ws = workspace if workspace is not None else alloc_workspace(
         rl_workspace_bytes(shape, params.num_rollouts, dz_chunk_rows), w_vocab.device)
     out = _outputs(report, logprob, entropy, lse, coef, token_keep, rollout_guarded, d_hidden, d_hidden_f32,
-                   d_w_vocab, accumulate_dw, d_w_vocab_nvls, dz_chunk_rows)
+                   d_w_vocab, accumulate_dw, d_w_vocab_nvls, dz_chunk_rows, dense_backward)
     _check(load_library().rl_policy_loss_fwd_bwd(
         ctypes.byref(shape), ctypes.byref(params), _ptr(_bf16(hidden, "hidden")), _ptr(_bf16(w_vocab, "w_vocab")),
         _ptr(targets), _ptr(infer_logprobs), _ptr(rollout_adv), _ptr(rollout_offsets), _ptr(loss_mask),
@@ -253,7 +254,7 @@ def rl_policy_loss_fwd_bwd_hostio(shape: rl_lm_shape, params: rl_loss_params, gr
                                   w_vocab, targets_host, infer_host, rewards_host, offsets_host,
                                   loss_mask_host=None, *, report, d_hidden=None, d_hidden_f32=None,
                                   d_w_vocab=None, accumulate_dw=False, d_w_vocab_nvls=None, dz_chunk_rows=0,
-                                  workspace=None, stream=None) -> rl_loss_report:
+                                  dense_backward=False, workspace=None, stream=None) -> rl_loss_report:
     """The same step with per-step inputs in (pinned) host tensors; returns the report."""
     ws = workspace if workspace is not None else alloc_workspace(
         rl_workspace_bytes_hostio(shape, params.num_rollouts, dz_chunk_rows), w_vocab.device)
@@ -266,7 +267,8 @@ def rl_policy_loss_fwd_bwd_hostio(shape: rl_lm_shape, params: rl_loss_params, gr
         return ctypes.c_void_p(t.data_ptr())
 
     out = _outputs(report, None, d_hidden=d_hidden, d_hidden_f32=d_hidden_f32, d_w_vocab=d_w_vocab,
-                   accumulate_dw=accumulate_dw, d_w_vocab_nvls=d_w_vocab_nvls, dz_chunk_rows=dz_chunk_rows)
+                   accumulate_dw=accumulate_dw, d_w_vocab_nvls=d_w_vocab_nvls, dz_chunk_rows=dz_chunk_rows,
+                   dense_backward=dense_backward)
     rep = rl_loss_report()
     _check(load_library().rl_policy_loss_fwd_bwd_hostio(
         ctypes.byref(shape), ctypes.byref(params), int(group_size), hp(hidden_host), _ptr(w_vocab),
@@ -322,7 +324,7 @@ def rl_profile_read(cap: int = 4096) -> list:
     return [(KERNEL_NAMES.get(buf[i].kernel, str(buf[i].kernel)), float(buf[i].ms)) for i in range(min(n, cap))]
 
 
-RL_BWD_DU, RL_BWD_DW, RL_BWD_DH, RL_BWD_ALL = 1, 2, 4, 7
+RL_BWD_DU, RL_BWD_DW, RL_BWD_DH, RL_BWD_ALL, RL_BWD_DENSE = 1, 2, 4, 7, 8
 
 
 def rl_bwd_ex(shape: rl_lm_shape, hidden, w_vocab, targets, lse, coef, d_hidden=None, d_hidden_f32=None,

@@ -230,7 +230,7 @@ constexpr int stages_for() {
 template <int MODE, bool A_MN, bool B_MN, int CG>
 rl_status launch_gemm_cg(int kid, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c, int64_t M,
                          int64_t N, int64_t K, int group_m, const rl::EpiParams& ep, int sms, cudaStream_t st,
-                         int k_splits = 1, int split_rows = 0) {
+                         int k_splits = 1, int split_rows = 0, const int* dyn_count = nullptr, int dyn_mode = 0) {
   constexpr int S = stages_for<CG>();
   auto kern = rl::gemm_kernel<MODE, A_MN, B_MN, CG, S>;
   constexpr int smem = rl::gemm_smem_bytes<CG, S>();
@@ -251,6 +251,8 @@ rl_status launch_gemm_cg(int kid, const CUtensorMap& a, const CUtensorMap& b, co
   sh.k_per_split = (sh.k_blocks + k_splits - 1) / k_splits;
   sh.k_splits = (sh.k_blocks + sh.k_per_split - 1) / sh.k_per_split;
   sh.split_rows = split_rows;
+  sh.dyn_count = dyn_count;
+  sh.dyn_mode = dyn_count ? dyn_mode : 0;
   if (sh.k_splits > 1 && (MODE == rl::EPI_LSE || MODE == rl::EPI_DZ || MODE == rl::EPI_F32_NVLS))
     return fail(RL_ERR_UNSUPPORTED, "split-K needs a plain store epilogue");
   const int64_t tiles = static_cast<int64_t>(sh.m_blocks) * sh.n_blocks * sh.k_splits;
@@ -291,11 +293,13 @@ rl_status launch_gemm_cg(int kid, const CUtensorMap& a, const CUtensorMap& b, co
 template <int MODE, bool A_MN, bool B_MN>
 rl_status launch_gemm(int kid, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c, int64_t M, int64_t N,
                       int64_t K, int group_m, const rl::EpiParams& ep, int sms, cudaStream_t st, int k_splits = 1,
-                      int split_rows = 0) {
+                      int split_rows = 0, const int* dyn_count = nullptr, int dyn_mode = 0) {
   if (M <= 0 || N <= 0) return RL_OK;
   if (cta_group() == 2)
-    return launch_gemm_cg<MODE, A_MN, B_MN, 2>(kid, a, b, c, M, N, K, group_m, ep, sms, st, k_splits, split_rows);
-  return launch_gemm_cg<MODE, A_MN, B_MN, 1>(kid, a, b, c, M, N, K, group_m, ep, sms, st, k_splits, split_rows);
+    return launch_gemm_cg<MODE, A_MN, B_MN, 2>(kid, a, b, c, M, N, K, group_m, ep, sms, st, k_splits, split_rows,
+                                               dyn_count, dyn_mode);
+  return launch_gemm_cg<MODE, A_MN, B_MN, 1>(kid, a, b, c, M, N, K, group_m, ep, sms, st, k_splits, split_rows,
+                                             dyn_count, dyn_mode);
 }
 
 // Grouped GEMM (MoE experts): the tile count is only known on the device (it
@@ -360,6 +364,9 @@ struct Carve {
 
 struct WsLayout {
   size_t partials, lse, coef, rp, sync, dz, end;
+  // sparse backward (rows with coef != 0): compact index, per-row vectors, counts,
+  // gathered hidden rows and one chunk of compact dH
+  size_t idx, coef_c, lse_c, tgt_c, blk_counts, chunk_counts, h_c, dh_c;
   int64_t n_tiles_v, ldz, chunk;
 };
 
@@ -378,6 +385,15 @@ WsLayout ws_layout(const rl_lm_shape* s, int32_t R, int64_t chunk_rows) {
   w.rp = c.take(static_cast<size_t>(R > 0 ? R : 1) * sizeof(rl::RolloutPartial));
   w.sync = c.take(static_cast<size_t>(kMaxSyncPoints) * 4);
   w.dz = c.take(static_cast<size_t>(w.chunk) * w.ldz * 2);
+  const int64_t Tp = (T + 255) / 256 * 256 + 256;  // compact rows + zero padding (gather_rows_kernel)
+  w.idx = c.take(static_cast<size_t>(Tp) * 4);
+  w.coef_c = c.take(static_cast<size_t>(Tp) * 4);
+  w.lse_c = c.take(static_cast<size_t>(Tp) * 4);
+  w.tgt_c = c.take(static_cast<size_t>(Tp) * 4);
+  w.blk_counts = c.take(static_cast<size_t>((T + rl::COMPACT_ROWS - 1) / rl::COMPACT_ROWS + 1) * 4);
+  w.chunk_counts = c.take(static_cast<size_t>((T + (w.chunk > 0 ? w.chunk : 1) - 1) / (w.chunk > 0 ? w.chunk : 1) + 2) * 4);
+  w.h_c = c.take(static_cast<size_t>(Tp) * s->H * 2);
+  w.dh_c = c.take(static_cast<size_t>((w.chunk + 255) / 256 * 256) * s->H * 4);
   w.end = align_up(c.off, 1024);
   return w;
 }
@@ -511,6 +527,117 @@ rl_status check_nvls(const rl_nvls_reduce* n, const char* what) {
   return RL_OK;
 }
 
+// Sparse backward: the same K4 -> K6 -> K5 over the rows whose coefficient is
+// non-zero only (their order kept). Row counts live on the device: the GEMMs read
+// them at start (dyn_mode), so nothing synchronises the host.
+rl_status bwd_sparse_impl(const rl_lm_shape* s, const uint16_t* hidden, const uint16_t* w, const int32_t* targets,
+                          const float* lse, const float* coef, uint16_t* dh, float* dh32, float* dw,
+                          int accumulate_dw, uint8_t* ws, const WsLayout& L, int sms, cudaStream_t st, int phases,
+                          const rl_nvls_reduce* dw_nvls) {
+  const int64_t T = s->T, H = s->H, V = s->V_local;
+  const int64_t chunk = L.chunk;
+  const int n_chunks = static_cast<int>((T + chunk - 1) / chunk);
+  uint16_t* dz = reinterpret_cast<uint16_t*>(ws + L.dz);
+  int32_t* idx = reinterpret_cast<int32_t*>(ws + L.idx);
+  float* coef_c = reinterpret_cast<float*>(ws + L.coef_c);
+  float* lse_c = reinterpret_cast<float*>(ws + L.lse_c);
+  int32_t* tgt_c = reinterpret_cast<int32_t*>(ws + L.tgt_c);
+  int* blk = reinterpret_cast<int*>(ws + L.blk_counts);
+  int* cc = reinterpret_cast<int*>(ws + L.chunk_counts);  // [n_chunks] per chunk, [n_chunks] total
+  uint16_t* h_c = reinterpret_cast<uint16_t*>(ws + L.h_c);
+  uint8_t* dh_c = ws + L.dh_c;
+  if (phases & RL_BWD_DU) {
+    const int nb = static_cast<int>((T + rl::COMPACT_ROWS - 1) / rl::COMPACT_ROWS);
+    {
+      ProfScope ps(RL_K_COMPACT, st);
+      rl::compact_count_kernel<<<nb, 256, 0, st>>>(coef, T, blk);
+    }
+    RL_CHECK_LAUNCH();
+    {
+      ProfScope ps(RL_K_COMPACT, st);
+      rl::compact_write_kernel<<<nb, 256, 0, st>>>(coef, lse, targets, T, blk, nb, chunk, idx, coef_c, lse_c, tgt_c,
+                                                   cc, n_chunks);
+    }
+    RL_CHECK_LAUNCH();
+    {
+      ProfScope ps(RL_K_COMPACT, st);
+      rl::gather_rows_kernel<<<2 * sms, 256, 0, st>>>(hidden, H, idx, cc + n_chunks, 256, (T + 255) / 256 * 256 + 256,
+                                                      h_c, coef_c, lse_c, tgt_c);
+    }
+    RL_CHECK_LAUNCH();
+  }
+  CUtensorMap t_w_k, t_w_mn, t_dw;
+  RL_TRY(make_map(&t_w_k, w, false, H, V, H, 64, rl::BN / cta_group()));
+  RL_TRY(make_map(&t_w_mn, w, false, H, V, H, 64, 64));
+  if (dw) RL_TRY(make_map(&t_dw, dw, true, H, V, H, 32, 32));
+  if ((phases & RL_BWD_DH) && (dh || dh32))
+    RL_CUDA(cudaMemsetAsync(dh ? static_cast<void*>(dh) : static_cast<void*>(dh32), 0,
+                            static_cast<size_t>(T) * H * (dh ? 2 : 4), st));
+  for (int ch = 0; ch < n_chunks; ++ch) {
+    const int64_t c0 = ch * chunk;
+    const int64_t rows = (T - c0 < chunk) ? (T - c0) : chunk;   // upper bound on this chunk's compact rows
+    const int* cnt = cc + ch;
+    const uint16_t* hc = h_c + c0 * H;
+    CUtensorMap t_h_k, t_dz_st, t_dz_k, t_dz_mn, t_h_mn, t_dh;
+    if (phases & RL_BWD_DU) {
+      RL_TRY(make_map(&t_h_k, hc, false, H, rows, H, 64, kARows));
+      RL_TRY(make_map(&t_dz_st, dz, false, V, rows, L.ldz, 64, 32));
+      rl::EpiParams ep = {};
+      ep.rows = rows;
+      ep.cols = V;
+      ep.inv_temperature = s->inv_temperature;
+      ep.scale_log2 = s->inv_temperature * 1.4426950408889634f;
+      ep.targets = tgt_c + c0;
+      ep.vocab_offset = s->vocab_offset;
+      ep.lse = lse_c + c0;
+      ep.coef = coef_c + c0;
+      RL_TRY((launch_gemm<rl::EPI_DZ, false, false>(RL_K_DZ_GEMM, t_h_k, t_w_k, t_dz_st, rows, V, H,
+                                                    group_m_for(RL_K_DZ_GEMM, 16), ep, sms, st, 1, 0, cnt, 1)));
+    }
+    if ((phases & RL_BWD_DW) && dw) {
+      RL_TRY(make_map(&t_dz_mn, dz, false, V, rows, L.ldz, 64, 64));
+      RL_TRY(make_map(&t_h_mn, hc, false, H, rows, H, 64, 64));
+      rl::EpiParams e6 = {};
+      e6.rows = V;
+      e6.cols = H;
+      if (dw_nvls) {
+        set_nvls(e6, dw_nvls, dw);
+        RL_TRY((launch_gemm<rl::EPI_F32_NVLS, true, true>(RL_K_DW_GEMM, t_dz_mn, t_h_mn, t_dw, V, H, rows,
+                                                            group_m_for(RL_K_DW_GEMM, 8), e6, sms, st, 1, 0, cnt, 2)));
+      } else if (ch == 0 && !accumulate_dw) {
+        RL_TRY((launch_gemm<rl::EPI_F32, true, true>(RL_K_DW_GEMM, t_dz_mn, t_h_mn, t_dw, V, H, rows,
+                                                     group_m_for(RL_K_DW_GEMM, 8), e6, sms, st, 1, 0, cnt, 2)));
+      } else {
+        RL_TRY((launch_gemm<rl::EPI_F32_ADD, true, true>(RL_K_DW_GEMM, t_dz_mn, t_h_mn, t_dw, V, H, rows,
+                                                         group_m_for(RL_K_DW_GEMM, 8), e6, sms, st, 1, 0, cnt, 2)));
+      }
+    }
+    if ((phases & RL_BWD_DH) && (dh || dh32)) {
+      RL_TRY(make_map(&t_dz_k, dz, false, V, rows, L.ldz, 64, kARows));
+      rl::EpiParams e5 = {};
+      e5.rows = rows;
+      e5.cols = H;
+      if (dh) {
+        RL_TRY(make_map(&t_dh, dh_c, false, H, rows, H, 64, 32));
+        RL_TRY((launch_gemm<rl::EPI_BF16, false, true>(RL_K_DH_GEMM, t_dz_k, t_w_mn, t_dh, rows, H, V,
+                                                       group_m_for(RL_K_DH_GEMM, 8), e5, sms, st, 1, 0, cnt, 1)));
+      } else {
+        RL_TRY(make_map(&t_dh, dh_c, true, H, rows, H, 32, 32));
+        RL_TRY((launch_gemm<rl::EPI_F32, false, true>(RL_K_DH_GEMM, t_dz_k, t_w_mn, t_dh, rows, H, V,
+                                                      group_m_for(RL_K_DH_GEMM, 8), e5, sms, st, 1, 0, cnt, 1)));
+      }
+      {
+        ProfScope ps(RL_K_COMPACT, st);
+        rl::scatter_rows_kernel<<<2 * sms, 256, 0, st>>>(dh_c, H * (dh ? 2 : 4), idx + c0, cnt,
+                                                         dh ? reinterpret_cast<uint8_t*>(dh)
+                                                            : reinterpret_cast<uint8_t*>(dh32));
+      }
+      RL_CHECK_LAUNCH();
+    }
+  }
+  return RL_OK;
+}
+
 // K4 -> K6 -> K5 per chunk of rows (dW first, so a caller can overlap its
 // reduction with dH). `phases` selects which run (RL_BWD_* bits).
 rl_status bwd_impl(const rl_lm_shape* s, const uint16_t* hidden, const uint16_t* w, const int32_t* targets,
@@ -525,6 +652,9 @@ rl_status bwd_impl(const rl_lm_shape* s, const uint16_t* hidden, const uint16_t*
   uint16_t* dz = reinterpret_cast<uint16_t*>(ws + L.dz);
   const int64_t chunk = L.chunk;
   g_sync_ctr = reinterpret_cast<uint32_t*>(ws + L.sync);
+  if (!(phases & RL_BWD_DENSE) && !dh_nvls)
+    return bwd_sparse_impl(s, hidden, w, targets, lse, coef, dh, dh32, dw, accumulate_dw, ws, L, sms, st, phases,
+                           dw_nvls);
   CUtensorMap t_h_k, t_w_k, t_dz_st, t_dz_k, t_w_mn, t_dh, t_dz_mn, t_h_mn, t_dw;
   RL_TRY(make_map(&t_w_k, w, false, H, V, H, 64, rl::BN / cta_group()));
   RL_TRY(make_map(&t_w_mn, w, false, H, V, H, 64, 64));
@@ -941,7 +1071,8 @@ rl_status rl_bwd_ex(const rl_lm_shape* shape, const uint16_t* hidden, const uint
   RL_TRY(check_nvls(dh_nvls, "dh_nvls"));
   if (dw_nvls && accumulate_dw) return fail(RL_ERR_INVALID_ARGUMENT, "dw_nvls needs accumulate_dw = 0");
   if (dh_nvls && !d_hidden_f32) return fail(RL_ERR_INVALID_ARGUMENT, "dh_nvls reduces d_hidden_f32");
-  if (phases <= 0 || phases > RL_BWD_ALL) return fail(RL_ERR_INVALID_ARGUMENT, "phases must be a non-empty RL_BWD_* mask");
+  if ((phases & RL_BWD_ALL) == 0 || (phases & ~(RL_BWD_ALL | RL_BWD_DENSE)) != 0)
+    return fail(RL_ERR_INVALID_ARGUMENT, "phases must be a non-empty RL_BWD_* mask");
   if (max_sms < 0) return fail(RL_ERR_INVALID_ARGUMENT, "max_sms must be >= 0");
   RL_TRY(check_shape(shape));
   if (d_hidden && d_hidden_f32) return fail(RL_ERR_INVALID_ARGUMENT, "pass d_hidden or d_hidden_f32, not both");
@@ -958,7 +1089,7 @@ rl_status rl_bwd_ex(const rl_lm_shape* shape, const uint16_t* hidden, const uint
   const WsLayout L = ws_layout(shape, 1, dz_chunk_rows);
   if (shape->T > 0 && (!workspace || workspace_bytes < L.end))
     return fail(RL_ERR_WORKSPACE, "workspace needs %zu bytes, got %zu", L.end, workspace_bytes);
-  if (phases != RL_BWD_ALL && L.chunk < shape->T)
+  if ((phases & RL_BWD_ALL) != RL_BWD_ALL && L.chunk < shape->T)
     return fail(RL_ERR_INVALID_ARGUMENT, "partial backward phases need one dU chunk (dz_chunk_rows = 0 or >= T)");
   if ((dw_nvls || dh_nvls) && L.chunk < shape->T)
     return fail(RL_ERR_INVALID_ARGUMENT, "NVLS reduction needs one dU chunk (dz_chunk_rows = 0 or >= T)");
@@ -997,7 +1128,8 @@ static rl_status step_impl(const rl_lm_shape* shape, const rl_loss_params* param
                    rollout_offsets, loss_mask, coef, out->token_keep, out->rollout_guarded, out->report,
                    reinterpret_cast<rl::RolloutPartial*>(ws + L.rp), st));
   RL_TRY(bwd_impl(shape, hidden, w_vocab, targets, lse, coef, out->d_hidden, out->d_hidden_f32, out->d_w_vocab,
-                  out->accumulate_dw, ws, L, sms, st, RL_BWD_ALL, out->d_w_vocab_nvls, nullptr));
+                  out->accumulate_dw, ws, L, sms, st, RL_BWD_ALL | (out->dense_backward ? RL_BWD_DENSE : 0),
+                  out->d_w_vocab_nvls, nullptr));
   return RL_OK;
 }
 

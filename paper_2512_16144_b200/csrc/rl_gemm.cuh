@@ -65,6 +65,10 @@ struct GemmShape {
   int k_splits;                      // split-K: tile t covers k-blocks of split t / (m_blocks*n_blocks)
   int k_per_split;                   // k-blocks per split
   int split_rows;                    // store epilogues: split s writes rows offset by s*split_rows
+  // device-side problem size (sparse backward): dyn_mode 1 = M rows, 2 = K rows come
+  // from *dyn_count at kernel start (the host sized the grid for the upper bound)
+  const int* dyn_count;
+  int dyn_mode;
 };
 
 __device__ __forceinline__ void tile_k_range(int tile, const GemmShape& sh, int& kb0, int& kb1) {
@@ -198,8 +202,19 @@ __device__ __noinline__ void nvls_reduce_slab_impl(const EpiParams& ep, const Ge
 template <int MODE, bool A_MN, bool B_MN, int CG, int STAGES>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                const __grid_constant__ CUtensorMap tmC, const GemmShape sh, const EpiParams ep) {
+                const __grid_constant__ CUtensorMap tmC, const GemmShape sh_in, const EpiParams ep) {
   using TL = Tiling<CG>;
+  GemmShape sh = sh_in;
+  if (sh.dyn_mode != 0) {
+    const int cnt = *sh.dyn_count;
+    if (sh.dyn_mode == 1) {
+      sh.m_blocks = (cnt + TL::TILE_M - 1) / TL::TILE_M;
+    } else {
+      sh.k_blocks = (cnt + BK - 1) / BK;
+      sh.k_per_split = sh.k_blocks;
+      sh.k_splits = 1;
+    }
+  }
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
@@ -548,6 +563,14 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           }
         }
         constexpr int COLS = (MODE == EPI_DZ || MODE == EPI_BF16 || MODE == EPI_BF16_GROUPED) ? 64 : 32;
+        // a tile with an empty K range (sparse backward, every row masked) stores zeros:
+        // the MMA issued nothing, so TMEM holds no accumulator for it
+        bool empty_k = false;
+        if constexpr (!GROUPED) {
+          int kb0, kb1;
+          tile_k_range(tile, sh, kb0, kb1);
+          empty_k = kb1 <= kb0;
+        }
 #pragma unroll 1
         for (int c = 0; c < BN / COLS; ++c) {
           uint32_t w[32];
@@ -578,8 +601,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                 v2 *= rs;
                 v3 *= rs;
               }
-              w[j] = pack_bf16x2(v0, v1);
-              w[16 + j] = pack_bf16x2(v2, v3);
+              w[j] = empty_k ? 0u : pack_bf16x2(v0, v1);
+              w[16 + j] = empty_k ? 0u : pack_bf16x2(v2, v3);
             }
           } else {
             uint32_t r0[32];
@@ -587,7 +610,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             tmem_wait_ld();
             if (c == BN / COLS - 1) release_tmem(acc);
 #pragma unroll
-            for (int j = 0; j < 32; ++j) w[j] = r0[j];
+            for (int j = 0; j < 32; ++j) w[j] = empty_k ? 0u : r0[j];
           }
           const uint32_t buf = buf0 + (chunk_ctr & 1) * EPI_BUF_BYTES;
           if (lane == 0) bulk_wait_read<1>();

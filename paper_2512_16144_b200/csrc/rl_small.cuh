@@ -294,6 +294,111 @@ __global__ void loss_finalize_kernel(const RolloutPartial* __restrict__ rp, int 
   *rep = r;
 }
 
+// ------------------------------------------------- sparse backward (rows with coef != 0)
+// Tokens whose coefficient is 0 (masked by Eq.2, guarded, loss_mask = 0, invalid)
+// have an all-zero dU row: the backward GEMMs run on the compacted rows only.
+// Compaction is order preserving and deterministic (block counts, then an in-block
+// scan); counts per dU chunk go to chunk_counts[c] = clamp(count - c*chunk, 0, chunk).
+constexpr int COMPACT_ROWS = 1024;  // rows per compaction block (256 threads x 4)
+
+__global__ void compact_count_kernel(const float* __restrict__ coef, int64_t T, int* __restrict__ block_counts) {
+  __shared__ int sh[256];
+  const int64_t r0 = static_cast<int64_t>(blockIdx.x) * COMPACT_ROWS + threadIdx.x * 4;
+  int c = 0;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) c += (r0 + j < T && coef[r0 + j] != 0.f) ? 1 : 0;
+  const int tot = block_reduce_sum(c, sh);
+  if (threadIdx.x == 0) block_counts[blockIdx.x] = tot;
+}
+
+__global__ void compact_write_kernel(const float* __restrict__ coef, const float* __restrict__ lse,
+                                     const int32_t* __restrict__ targets, int64_t T,
+                                     const int* __restrict__ block_counts, int nblocks, int64_t chunk,
+                                     int32_t* __restrict__ idx, float* __restrict__ coef_c, float* __restrict__ lse_c,
+                                     int32_t* __restrict__ tgt_c, int* __restrict__ chunk_counts, int n_chunks) {
+  __shared__ int sh[256];
+  __shared__ int base;
+  if (threadIdx.x == 0) {
+    int b = 0;
+    for (int j = 0; j < static_cast<int>(blockIdx.x); ++j) b += block_counts[j];
+    base = b;
+  }
+  const int64_t r0 = static_cast<int64_t>(blockIdx.x) * COMPACT_ROWS + threadIdx.x * 4;
+  bool f[4];
+  int c = 0;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    f[j] = r0 + j < T && coef[r0 + j] != 0.f;
+    c += f[j];
+  }
+  // exclusive scan of c over the block (Hillis-Steele in shared memory)
+  sh[threadIdx.x] = c;
+  __syncthreads();
+  for (int o = 1; o < 256; o <<= 1) {
+    const int v = threadIdx.x >= o ? sh[threadIdx.x - o] : 0;
+    __syncthreads();
+    sh[threadIdx.x] += v;
+    __syncthreads();
+  }
+  int pos = base + sh[threadIdx.x] - c;
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+    if (f[j]) {
+      const int64_t r = r0 + j;
+      idx[pos] = static_cast<int32_t>(r);
+      coef_c[pos] = coef[r];
+      lse_c[pos] = lse[r];
+      tgt_c[pos] = targets[r];
+      ++pos;
+    }
+  if (blockIdx.x == nblocks - 1 && threadIdx.x == 255) {
+    const int64_t count = pos;  // = base + inclusive scan of the last thread
+    for (int ch = 0; ch < n_chunks; ++ch) {
+      const int64_t left = count - ch * chunk;
+      chunk_counts[ch] = static_cast<int>(left < 0 ? 0 : (left > chunk ? chunk : left));
+    }
+    chunk_counts[n_chunks] = static_cast<int>(count);
+  }
+}
+
+// h_c[r] = hidden[idx[r]] for r < count; the `pad` rows after them (up to `cap`) are
+// zeroed together with their coef/lse/target, so a tail tile of any chunk (which
+// reads at most 255 rows past the chunk's last compact row) contributes exact zeros.
+__global__ void gather_rows_kernel(const uint16_t* __restrict__ hidden, int64_t H, const int32_t* __restrict__ idx,
+                                   const int* __restrict__ count_ptr, int pad, int64_t cap, uint16_t* __restrict__ h_c,
+                                   float* __restrict__ coef_c, float* __restrict__ lse_c, int32_t* __restrict__ tgt_c) {
+  const int count = *count_ptr;
+  const int64_t padded = (static_cast<int64_t>(count) + pad < cap) ? static_cast<int64_t>(count) + pad : cap;
+  const int64_t vecs = H / 8;  // 16-byte vectors per row (H % 8 == 0)
+  for (int64_t r = blockIdx.x; r < padded; r += gridDim.x) {
+    uint4* dst = reinterpret_cast<uint4*>(h_c + r * H);
+    if (r < count) {
+      const uint4* src = reinterpret_cast<const uint4*>(hidden + static_cast<int64_t>(idx[r]) * H);
+      for (int64_t v = threadIdx.x; v < vecs; v += blockDim.x) dst[v] = src[v];
+    } else {
+      for (int64_t v = threadIdx.x; v < vecs; v += blockDim.x) dst[v] = make_uint4(0, 0, 0, 0);
+      if (threadIdx.x == 0) {
+        coef_c[r] = 0.f;
+        lse_c[r] = 0.f;
+        tgt_c[r] = -1;
+      }
+    }
+  }
+}
+
+// dh[idx[r]] = dh_c[r] for r < count (dh pre-zeroed); elem bytes = 2 (bf16) or 4 (f32).
+__global__ void scatter_rows_kernel(const uint8_t* __restrict__ dh_c, int64_t row_bytes,
+                                    const int32_t* __restrict__ idx, const int* __restrict__ count_ptr,
+                                    uint8_t* __restrict__ dh) {
+  const int count = *count_ptr;
+  const int64_t vecs = row_bytes / 16;
+  for (int64_t r = blockIdx.x; r < count; r += gridDim.x) {
+    const uint4* src = reinterpret_cast<const uint4*>(dh_c + r * row_bytes);
+    uint4* dst = reinterpret_cast<uint4*>(dh + static_cast<int64_t>(idx[r]) * row_bytes);
+    for (int64_t v = threadIdx.x; v < vecs; v += blockDim.x) dst[v] = src[v];
+  }
+}
+
 // ------------------------------------------------------- Newton-Schulz aux
 // Frobenius norm: per-block fp64 partial sums of squares (fixed order), then every
 // block of the cast kernel re-sums the partials in index order (deterministic).

@@ -18,8 +18,8 @@ from __future__ import annotations
 import torch
 import torch.distributed as dist
 
-from . import (RL_BWD_DH, RL_BWD_DU, RL_BWD_DW, alloc_workspace, make_params, make_shape, rl_bwd, rl_bwd_ex,
-               rl_fwd_partials, rl_group_advantages, rl_last_launch_count, rl_logprob_fwd, rl_loss_coef,
+from . import (RL_BWD_ALL, RL_BWD_DENSE, RL_BWD_DH, RL_BWD_DU, RL_BWD_DW, alloc_workspace, make_params,
+               make_shape, rl_bwd_ex, rl_fwd_partials, rl_group_advantages, rl_last_launch_count, rl_logprob_fwd, rl_loss_coef,
                rl_merge_partials, rl_nvls_flag_count, rl_nvls_reduce, rl_policy_loss_fwd_bwd, rl_workspace_bytes)
 
 
@@ -59,10 +59,13 @@ class NvlsReduction:
 
 
 class LibrlPhases:
-    """The split phases backed by librl (device tensors, current stream)."""
+    """The split phases backed by librl (device tensors, current stream).
+    `dense_backward` runs the backward GEMMs over all rows (RL_BWD_DENSE) instead of
+    the rows with a non-zero coefficient."""
 
-    def __init__(self):
+    def __init__(self, dense_backward: bool = False):
         self.launches = 0
+        self.dense = RL_BWD_DENSE if dense_backward else 0
 
     def _count(self):
         self.launches += rl_last_launch_count()
@@ -87,12 +90,9 @@ class LibrlPhases:
 
     def bwd(self, shape, hidden, w_shard, targets, lse, coef, d_hidden_f32, d_w_vocab, dz_chunk_rows=0,
             workspace=None, dh_nvls=None):
-        if dh_nvls is None:
-            rl_bwd(shape, hidden, w_shard, targets, lse, coef, d_hidden_f32=d_hidden_f32, d_w_vocab=d_w_vocab,
-                   dz_chunk_rows=dz_chunk_rows, workspace=workspace)
-        else:
-            rl_bwd_ex(shape, hidden, w_shard, targets, lse, coef, d_hidden_f32=d_hidden_f32, d_w_vocab=d_w_vocab,
-                      dz_chunk_rows=dz_chunk_rows, dh_nvls=dh_nvls, workspace=workspace)
+        rl_bwd_ex(shape, hidden, w_shard, targets, lse, coef, d_hidden_f32=d_hidden_f32, d_w_vocab=d_w_vocab,
+                  dz_chunk_rows=dz_chunk_rows, phases=RL_BWD_ALL | self.dense, dh_nvls=dh_nvls,
+                  workspace=workspace)
         self._count()
 
     def logprob_fwd(self, shape, hidden, w, targets, logprob, entropy, lse, workspace=None):
@@ -101,8 +101,8 @@ class LibrlPhases:
 
     def bwd_phases(self, shape, hidden, w, targets, lse, coef, d_hidden, d_w_vocab, phases, max_sms=0,
                    workspace=None):
-        rl_bwd_ex(shape, hidden, w, targets, lse, coef, d_hidden=d_hidden, d_w_vocab=d_w_vocab, phases=phases,
-                  max_sms=max_sms, workspace=workspace)
+        rl_bwd_ex(shape, hidden, w, targets, lse, coef, d_hidden=d_hidden, d_w_vocab=d_w_vocab,
+                  phases=phases | self.dense, max_sms=max_sms, workspace=workspace)
         self._count()
 
     def full_step(self, shape, params, hidden, w, targets, infer, adv, offsets, loss_mask, *, report, logprob,
@@ -111,7 +111,8 @@ class LibrlPhases:
         rl_policy_loss_fwd_bwd(shape, params, hidden, w, targets, infer, adv, offsets, loss_mask, report=report,
                                logprob=logprob, entropy=entropy, lse=lse, coef=coef, token_keep=keep,
                                rollout_guarded=guarded, d_hidden=d_hidden, d_w_vocab=d_w_vocab,
-                               d_w_vocab_nvls=d_w_vocab_nvls, dz_chunk_rows=dz_chunk_rows, workspace=workspace)
+                               d_w_vocab_nvls=d_w_vocab_nvls, dz_chunk_rows=dz_chunk_rows,
+                               dense_backward=bool(self.dense), workspace=workspace)
         self._count()
 
 

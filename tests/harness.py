@@ -155,7 +155,7 @@ def to_device(c: Case, device="cuda"):
 
 
 def run_gpu_step(c: Case, *, dh_f32=False, accumulate_dw=False, dw_init=None, use_mask=True, device="cuda",
-                 loss_denominator=None):
+                 loss_denominator=None, dense_backward=False, dz_chunk_rows=0):
     import torch
     import paper_2512_16144_b200 as rl
     b = c.batch
@@ -175,7 +175,8 @@ def run_gpu_step(c: Case, *, dh_f32=False, accumulate_dw=False, dw_init=None, us
                               d["loss_mask"] if use_mask else None, report=report, logprob=out["logprob"],
                               entropy=out["entropy"], lse=out["lse"], coef=out["coef"], token_keep=out["keep"],
                               rollout_guarded=out["guarded"], d_hidden=None if dh_f32 else dh,
-                              d_hidden_f32=dh if dh_f32 else None, d_w_vocab=dw, accumulate_dw=accumulate_dw)
+                              d_hidden_f32=dh if dh_f32 else None, d_w_vocab=dw, accumulate_dw=accumulate_dw,
+                              dense_backward=dense_backward, dz_chunk_rows=dz_chunk_rows)
     torch.cuda.synchronize()
     res = {k: v.cpu().numpy() for k, v in out.items()}
     res["report"] = rl.read_report(report).as_dict()
