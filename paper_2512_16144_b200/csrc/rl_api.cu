@@ -209,6 +209,18 @@ int sync_every_for(int kid) {
   }
   return cache[kid];
 }
+// Wide 256 x 512 pair tiles (NB = 2, rl_gemm.cuh) for the long-K store GEMMs:
+// RL_WIDE[_<K>] = 0/1, default on for DH (K = V) and DW (K = T).
+bool wide_for(int kid) {
+  static int cache[32];
+  static bool init[32] = {};
+  if (kid < 0 || kid >= 32) return false;
+  if (!init[kid]) {
+    cache[kid] = env_int("RL_WIDE", kid, (kid == RL_K_DH_GEMM || kid == RL_K_DW_GEMM) ? 1 : 0);
+    init[kid] = true;
+  }
+  return cache[kid] != 0;
+}
 int sync_slack_for(int kid) {
   static int cache[32];
   static bool init[32] = {};
@@ -222,18 +234,19 @@ int sync_slack_for(int kid) {
 constexpr int kMaxSyncPoints = 1 << 16;
 thread_local uint32_t* g_sync_ctr = nullptr;  // set per call from the workspace
 
-template <int CG>
+template <int CG, int NB>
 constexpr int stages_for() {
-  return CG == 2 ? 6 : 4;
+  return CG == 2 ? (NB == 2 ? 4 : 6) : 4;
 }
 
-template <int MODE, bool A_MN, bool B_MN, int CG>
+template <int MODE, bool A_MN, bool B_MN, int CG, int NB = 1>
 rl_status launch_gemm_cg(int kid, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c, int64_t M,
                          int64_t N, int64_t K, int group_m, const rl::EpiParams& ep, int sms, cudaStream_t st,
                          int k_splits = 1, int split_rows = 0, const int* dyn_count = nullptr, int dyn_mode = 0) {
-  constexpr int S = stages_for<CG>();
-  auto kern = rl::gemm_kernel<MODE, A_MN, B_MN, CG, S>;
-  constexpr int smem = rl::gemm_smem_bytes<CG, S>();
+  constexpr int S = stages_for<CG, NB>();
+  auto kern = rl::gemm_kernel<MODE, A_MN, B_MN, CG, S, NB>;
+  constexpr int smem = rl::gemm_smem_bytes<CG, S, false, NB>();
+  static_assert(smem <= 232448, "dynamic shared memory over 227 KB");
   static bool attr_set = false;  // per instantiation
   if (!attr_set) {
     RL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
@@ -242,7 +255,7 @@ rl_status launch_gemm_cg(int kid, const CUtensorMap& a, const CUtensorMap& b, co
   using TL = rl::Tiling<CG>;
   rl::GemmShape sh;
   sh.m_blocks = static_cast<int>((M + TL::TILE_M - 1) / TL::TILE_M);
-  sh.n_blocks = static_cast<int>((N + rl::BN - 1) / rl::BN);
+  sh.n_blocks = static_cast<int>((N + rl::BN * NB - 1) / (rl::BN * NB));
   sh.k_blocks = static_cast<int>((K + rl::BK - 1) / rl::BK);
   sh.group_m = group_m;
   if (sh.k_blocks == 0) return fail(RL_ERR_SHAPE, "GEMM with K = 0");
@@ -295,6 +308,14 @@ rl_status launch_gemm(int kid, const CUtensorMap& a, const CUtensorMap& b, const
                       int64_t K, int group_m, const rl::EpiParams& ep, int sms, cudaStream_t st, int k_splits = 1,
                       int split_rows = 0, const int* dyn_count = nullptr, int dyn_mode = 0) {
   if (M <= 0 || N <= 0) return RL_OK;
+  constexpr bool kStore = MODE == rl::EPI_BF16 || MODE == rl::EPI_F32 || MODE == rl::EPI_F32_ADD ||
+                          MODE == rl::EPI_F32_NVLS;
+  if constexpr (kStore) {
+    // wide tiles only where a tile covers at least two 256-column blocks
+    if (cta_group() == 2 && wide_for(kid) && N > rl::BN)
+      return launch_gemm_cg<MODE, A_MN, B_MN, 2, 2>(kid, a, b, c, M, N, K, group_m, ep, sms, st, k_splits,
+                                                    split_rows, dyn_count, dyn_mode);
+  }
   if (cta_group() == 2)
     return launch_gemm_cg<MODE, A_MN, B_MN, 2>(kid, a, b, c, M, N, K, group_m, ep, sms, st, k_splits, split_rows,
                                                dyn_count, dyn_mode);

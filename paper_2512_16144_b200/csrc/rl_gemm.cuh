@@ -10,7 +10,13 @@
 //         the operand bytes of CG = 1 for the same FLOPs.
 // BK = 64 (one 128-byte swizzle atom of bf16), a STAGES-deep TMA ring, two TMEM
 // accumulators (2 x 256 columns) so the epilogue of tile i overlaps the MMAs of
-// tile i+1. Warp roles: warp 0 = TMA producer, warp 1 = TMEM owner + MMA issuer
+// tile i+1.
+// NB = 2 (wide tiles, CG = 2 store epilogues only): the pair computes 256 x 512
+//         with two N = 256 MMAs per k-step that share the A stage, so each SM moves
+//         48 instead of 64 bytes from L2 per 1024 MMA cycles (3/4). The one
+//         accumulator then fills all 512 TMEM columns and the epilogue is not
+//         overlapped: worth it only where a tile's main loop is long (K5, K6).
+// Warp roles: warp 0 = TMA producer, warp 1 = TMEM owner + MMA issuer
 // (leader CTA), warps 2..5 = epilogue (thread = accumulator row).
 //
 // Epilogues:
@@ -54,9 +60,10 @@ struct Tiling {
   static constexpr int STAGE = A_STAGE + B_STAGE;
 };
 
-template <int CG, int STAGES, bool GROUPED = false>
+template <int CG, int STAGES, bool GROUPED = false, int NB = 1>
 constexpr int gemm_smem_bytes() {
-  return 1024 + STAGES * Tiling<CG>::STAGE + EPI_BYTES + BAR_BYTES + (GROUPED ? (MAX_GROUPS + 1) * 4 : 0);
+  return 1024 + STAGES * (Tiling<CG>::A_STAGE + NB * Tiling<CG>::B_STAGE) + EPI_BYTES + BAR_BYTES +
+         (GROUPED ? (MAX_GROUPS + 1) * 4 : 0);
 }
 
 struct GemmShape {
@@ -158,7 +165,7 @@ __device__ __forceinline__ int grp_end(const EpiParams& ep, int g) {
 __device__ __forceinline__ int nvls_slab(int tile, uint32_t rank, int q) { return tile * 8 + rank * 4 + q; }
 
 // Owner-side reduction of one slab over the multicast group (see EpiParams::nvls_*).
-template <int TILE_M>
+template <int TILE_M, int TN>
 __device__ __noinline__ void nvls_reduce_slab_impl(const EpiParams& ep, const GemmShape& sh, int tile, uint32_t rank,
                                                    int q, int lane) {
   if (tile % ep.nvls_world != ep.nvls_rank) return;
@@ -175,35 +182,41 @@ __device__ __noinline__ void nvls_reduce_slab_impl(const EpiParams& ep, const Ge
   int m, n;
   tile_coords(tile, sh, m, n);
   const int64_t r0 = static_cast<int64_t>(m) * TILE_M + rank * 128 + q * 32;
-  const int64_t c0 = static_cast<int64_t>(n) * BN;
+  const int64_t c0 = static_cast<int64_t>(n) * TN;
   const int64_t rleft = ep.rows - r0, cleft = ep.cols - c0;
   const int rmax = rleft < 32 ? static_cast<int>(rleft) : 32;
-  const int cmax = cleft < BN ? static_cast<int>(cleft) : BN;
-  // lane l covers columns 4l..4l+3 and 128+4l..: 2 x 16 B per row, 8 rows in flight
-  for (int rb = 0; rb < rmax; rb += 8) {
-    float v[8][2][4];
+  const int cmax = cleft < TN ? static_cast<int>(cleft) : TN;
+  // lane l covers columns 4l..4l+3, 128+4l.., ...: TN/128 x 16 B per row, 16 loads in flight
+  constexpr int H = TN / 128, RB = 16 / H;
+  for (int rb = 0; rb < rmax; rb += RB) {
+    float v[RB][H][4];
 #pragma unroll
-    for (int i = 0; i < 8; ++i)
+    for (int i = 0; i < RB; ++i)
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
+      for (int h = 0; h < H; ++h) {
         const int c = h * 128 + lane * 4;
         if (rb + i < rmax && c < cmax) mc_ld_reduce_v4(ep.nvls_mc + (r0 + rb + i) * ep.cols + c0 + c, v[i][h]);
       }
 #pragma unroll
-    for (int i = 0; i < 8; ++i)
+    for (int i = 0; i < RB; ++i)
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
+      for (int h = 0; h < H; ++h) {
         const int c = h * 128 + lane * 4;
         if (rb + i < rmax && c < cmax) mc_st_v4(ep.nvls_mc + (r0 + rb + i) * ep.cols + c0 + c, v[i][h]);
       }
   }
 }
 
-template <int MODE, bool A_MN, bool B_MN, int CG, int STAGES>
+template <int MODE, bool A_MN, bool B_MN, int CG, int STAGES, int NB = 1>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const __grid_constant__ CUtensorMap tmC, const GemmShape sh_in, const EpiParams ep) {
   using TL = Tiling<CG>;
+  static_assert(NB == 1 || (NB == 2 && CG == 2 && MODE != EPI_LSE && MODE != EPI_DZ && MODE != EPI_BF16_GROUPED),
+                "wide tiles: CTA pairs, plain store epilogues");
+  constexpr int TN = BN * NB;                 // tile columns
+  constexpr int NACC = NB == 1 ? 2 : 1;       // TMEM accumulators (512 columns in total)
+  constexpr int B_STAGE_ALL = NB * TL::B_STAGE;
   GemmShape sh = sh_in;
   if (sh.dyn_mode != 0) {
     const int cnt = *sh.dyn_count;
@@ -219,7 +232,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = sA + STAGES * TL::A_STAGE;
-  uint8_t* sEpi = sB + STAGES * TL::B_STAGE;
+  uint8_t* sEpi = sB + STAGES * B_STAGE_ALL;
   uint64_t* full = reinterpret_cast<uint64_t*>(sEpi + EPI_BYTES);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
@@ -313,7 +326,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       } else {
         tile_coords(tile, sh, m, n);
         a_row = m * TL::TILE_M + rank * TL::A_ROWS;
-        b_row = n * BN + rank * TL::B_ROWS;
+        b_row = n * TN + rank * TL::B_ROWS;
       }
       int kb0 = 0, kb1 = sh.k_blocks;
       if constexpr (!GROUPED) tile_k_range(tile, sh, kb0, kb1);
@@ -335,10 +348,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         }
         mbar_wait_sleep(&empty[s], ph ^ 1);
         if (elect_one()) {
-          if (leader) mbar_expect_tx(&full[s], CG * TL::STAGE);
+          if (leader) mbar_expect_tx(&full[s], CG * (TL::A_STAGE + B_STAGE_ALL));
           const int k0 = kb * BK;
           uint8_t* a = sA + s * TL::A_STAGE;
-          uint8_t* b = sB + s * TL::B_STAGE;
+          uint8_t* b = sB + s * B_STAGE_ALL;
           if constexpr (CG == 2) {
             if (!A_MN) {
               tma_load_2d_pair(a, &tmA, &full[s], k0, a_row);
@@ -346,12 +359,18 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
               tma_load_2d_pair(a, &tmA, &full[s], a_row, k0);
               tma_load_2d_pair(a + 8192, &tmA, &full[s], a_row + 64, k0);
             }
-            if (!B_MN) {
-              tma_load_2d_pair(b, &tmB, &full[s], k0, b_row);
-            } else {
 #pragma unroll
-              for (int j = 0; j < TL::B_ROWS / 64; ++j)
-                tma_load_2d_pair(b + j * 8192, &tmB, &full[s], b_row + 64 * j, k0);
+            for (int nb = 0; nb < NB; ++nb) {
+              // block nb: columns nb*256.. of the tile; this CTA holds its half (128)
+              uint8_t* bb = b + nb * TL::B_STAGE;
+              const int br = b_row + nb * BN;
+              if (!B_MN) {
+                tma_load_2d_pair(bb, &tmB, &full[s], k0, br);
+              } else {
+#pragma unroll
+                for (int j = 0; j < TL::B_ROWS / 64; ++j)
+                  tma_load_2d_pair(bb + j * 8192, &tmB, &full[s], br + 64 * j, k0);
+              }
             }
           } else {
             if (!A_MN) {
@@ -391,7 +410,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       for (int tile = unit; tile < total; tile += n_units) {
         mbar_wait(&tempty[acc], aph ^ 1);
         tc_fence_after();
-        const uint32_t d = tmem_base + acc * BN;
+        const uint32_t d = tmem_base + acc * TN;
         int kb0 = 0, kb1 = sh.k_blocks;
         if constexpr (!GROUPED) tile_k_range(tile, sh, kb0, kb1);
         for (int kb = kb0; kb < kb1; ++kb) {
@@ -399,15 +418,20 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           tc_fence_after();
           if (elect_one()) {
             const uint32_t a0 = a_base + s * TL::A_STAGE;
-            const uint32_t b0 = b_base + s * TL::B_STAGE;
+            const uint32_t b0 = b_base + s * B_STAGE_ALL;
 #pragma unroll
             for (int k = 0; k < BK / 16; ++k) {
               const uint64_t ad = A_MN ? sw128_desc(a0 + k * 2048, 8192, 1024) : sw128_desc(a0 + k * 32, 16, 1024);
-              const uint64_t bd = B_MN ? sw128_desc(b0 + k * 2048, 8192, 1024) : sw128_desc(b0 + k * 32, 16, 1024);
-              if constexpr (CG == 2)
-                umma_bf16_pair(d, ad, bd, idesc, (kb != kb0) || (k != 0));
-              else
-                umma_bf16(d, ad, bd, idesc, (kb != kb0) || (k != 0));
+#pragma unroll
+              for (int nb = 0; nb < NB; ++nb) {
+                const uint32_t bn = b0 + nb * TL::B_STAGE;
+                const uint64_t bd =
+                    B_MN ? sw128_desc(bn + k * 2048, 8192, 1024) : sw128_desc(bn + k * 32, 16, 1024);
+                if constexpr (CG == 2)
+                  umma_bf16_pair(d + nb * BN, ad, bd, idesc, (kb != kb0) || (k != 0));
+                else
+                  umma_bf16(d + nb * BN, ad, bd, idesc, (kb != kb0) || (k != 0));
+              }
             }
             if constexpr (CG == 2)
               umma_commit_pair(&empty[s], 0x3);
@@ -427,7 +451,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             umma_commit(&tfull[acc]);
         }
         __syncwarp();
-        acc ^= 1;
+        if (NACC == 2) acc ^= 1;
         if (acc == 0) aph ^= 1;
       }
     }
@@ -442,7 +466,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     int chunk_ctr = 0;
     int it = 0;  // tile iteration of this CTA
     auto nvls_reduce_slab = [&](const EpiParams& e, const GemmShape& g, int t, uint32_t r, int qq, int l) {
-      nvls_reduce_slab_impl<TL::TILE_M>(e, g, t, r, qq, l);
+      nvls_reduce_slab_impl<TL::TILE_M, TN>(e, g, t, r, qq, l);
     };
     auto release_tmem = [&](int a) {
       tc_fence_before();
@@ -472,10 +496,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         row = static_cast<int64_t>(m) * TL::TILE_M + r_in_tile;
         row_ok = row < ep.rows;
       }
-      const int n0 = n * BN;
+      const int n0 = n * TN;
       mbar_wait_sleep(&tfull[acc], aph);
       tc_fence_after();
-      const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN;
+      const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * TN;
 
       if constexpr (MODE == EPI_LSE) {
         int64_t y = row_ok ? static_cast<int64_t>(ep.targets[row]) - ep.vocab_offset : -1;
@@ -572,14 +596,14 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           empty_k = kb1 <= kb0;
         }
 #pragma unroll 1
-        for (int c = 0; c < BN / COLS; ++c) {
+        for (int c = 0; c < TN / COLS; ++c) {
           uint32_t w[32];
           if constexpr (COLS == 64) {
             uint32_t r0[32], r1[32];
             tmem_ld32(taddr + c * 64, r0);
             tmem_ld32(taddr + c * 64 + 32, r1);
             tmem_wait_ld();
-            if (c == BN / COLS - 1) release_tmem(acc);
+            if (c == TN / COLS - 1) release_tmem(acc);
 #pragma unroll
             for (int j = 0; j < 16; ++j) {
               float v0 = __uint_as_float(r0[2 * j]), v1 = __uint_as_float(r0[2 * j + 1]);
@@ -608,7 +632,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             uint32_t r0[32];
             tmem_ld32(taddr + c * 32, r0);
             tmem_wait_ld();
-            if (c == BN / COLS - 1) release_tmem(acc);
+            if (c == TN / COLS - 1) release_tmem(acc);
 #pragma unroll
             for (int j = 0; j < 32; ++j) w[j] = empty_k ? 0u : r0[j];
           }
@@ -644,7 +668,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         }
       }
       ++it;
-      acc ^= 1;
+      if (NACC == 2) acc ^= 1;
       if (acc == 0) aph ^= 1;
     }
     if constexpr (MODE == EPI_F32_NVLS) {

@@ -60,6 +60,8 @@ def test_logprob_fwd(wl, tokens, vocab, hidden, invT):
 @pytest.mark.parametrize("wl,tokens,vocab,hidden,invT", [
     (TINY, None, None, None, 1.0),
     (RAGGED, 333, 1000, 200, 1 / 0.7),
+    (RAGGED, 333, 1000, 392, 1.0),            # one partial 256x512 (wide) tile in N for K5/K6
+    (RAGGED, 517, 1300, 776, 1.0),            # one full + one partial wide tile
     (synth.Workload("mid", 2, 8, 80, 512, 4184, ragged=True, prompt_frac=0.1, delta_sigma=1.0,
                     spike_rate=1e-3), None, None, None, 1.0),
 ])
