@@ -209,17 +209,30 @@ int sync_every_for(int kid) {
   }
   return cache[kid];
 }
-// Wide 256 x 512 pair tiles (NB = 2, rl_gemm.cuh) for the long-K store GEMMs:
-// RL_WIDE[_<K>] = 0/1, default on for DH (K = V) and DW (K = T).
+// Wide 256 x 512 pair tiles (NB = 2, rl_gemm.cuh): RL_WIDE[_<K>] = 0/1, default on
+// for K1 (FWD), K5 (DH) and K6 (DW); RL_SKEW = 0/2/3 k-blocks of block-0-first MMA
+// order at both ends of a tile (default 3), which hides the epilogue of one TMEM
+// half. K4 (DZ) stays narrow: its exp + bf16-store epilogue per half is longer
+// than that cover (measured: K4 15.6 -> 17.9 ms wide, K1 15.6 -> 15.2 ms).
 bool wide_for(int kid) {
   static int cache[32];
   static bool init[32] = {};
   if (kid < 0 || kid >= 32) return false;
   if (!init[kid]) {
-    cache[kid] = env_int("RL_WIDE", kid, (kid == RL_K_DH_GEMM || kid == RL_K_DW_GEMM) ? 1 : 0);
+    const bool dflt = kid == RL_K_FWD_GEMM || kid == RL_K_DH_GEMM || kid == RL_K_DW_GEMM;
+    cache[kid] = env_int("RL_WIDE", kid, dflt ? 1 : 0);
     init[kid] = true;
   }
   return cache[kid] != 0;
+}
+int skew() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("RL_SKEW");
+    v = e ? atoi(e) : 3;
+    if (v != 0 && v != 2) v = 3;
+  }
+  return v;
 }
 int sync_slack_for(int kid) {
   static int cache[32];
@@ -239,12 +252,12 @@ constexpr int stages_for() {
   return CG == 2 ? (NB == 2 ? 4 : 6) : 4;
 }
 
-template <int MODE, bool A_MN, bool B_MN, int CG, int NB = 1>
+template <int MODE, bool A_MN, bool B_MN, int CG, int NB = 1, int SKEW = 0>
 rl_status launch_gemm_cg(int kid, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c, int64_t M,
                          int64_t N, int64_t K, int group_m, const rl::EpiParams& ep, int sms, cudaStream_t st,
                          int k_splits = 1, int split_rows = 0, const int* dyn_count = nullptr, int dyn_mode = 0) {
   constexpr int S = stages_for<CG, NB>();
-  auto kern = rl::gemm_kernel<MODE, A_MN, B_MN, CG, S, NB>;
+  auto kern = rl::gemm_kernel<MODE, A_MN, B_MN, CG, S, NB, SKEW>;
   constexpr int smem = rl::gemm_smem_bytes<CG, S, false, NB>();
   static_assert(smem <= 232448, "dynamic shared memory over 227 KB");
   static bool attr_set = false;  // per instantiation
@@ -308,13 +321,19 @@ rl_status launch_gemm(int kid, const CUtensorMap& a, const CUtensorMap& b, const
                       int64_t K, int group_m, const rl::EpiParams& ep, int sms, cudaStream_t st, int k_splits = 1,
                       int split_rows = 0, const int* dyn_count = nullptr, int dyn_mode = 0) {
   if (M <= 0 || N <= 0) return RL_OK;
-  constexpr bool kStore = MODE == rl::EPI_BF16 || MODE == rl::EPI_F32 || MODE == rl::EPI_F32_ADD ||
-                          MODE == rl::EPI_F32_NVLS;
-  if constexpr (kStore) {
-    // wide tiles only where a tile covers at least two 256-column blocks
-    if (cta_group() == 2 && wide_for(kid) && N > rl::BN)
-      return launch_gemm_cg<MODE, A_MN, B_MN, 2, 2>(kid, a, b, c, M, N, K, group_m, ep, sms, st, k_splits,
-                                                    split_rows, dyn_count, dyn_mode);
+  // wide tiles only where a tile covers at least two 256-column blocks
+  if (cta_group() == 2 && wide_for(kid) && N > rl::BN) {
+    switch (skew()) {
+      case 0:
+        return launch_gemm_cg<MODE, A_MN, B_MN, 2, 2, 0>(kid, a, b, c, M, N, K, group_m, ep, sms, st, k_splits,
+                                                         split_rows, dyn_count, dyn_mode);
+      case 2:
+        return launch_gemm_cg<MODE, A_MN, B_MN, 2, 2, 2>(kid, a, b, c, M, N, K, group_m, ep, sms, st, k_splits,
+                                                         split_rows, dyn_count, dyn_mode);
+      default:
+        return launch_gemm_cg<MODE, A_MN, B_MN, 2, 2, 3>(kid, a, b, c, M, N, K, group_m, ep, sms, st, k_splits,
+                                                         split_rows, dyn_count, dyn_mode);
+    }
   }
   if (cta_group() == 2)
     return launch_gemm_cg<MODE, A_MN, B_MN, 2>(kid, a, b, c, M, N, K, group_m, ep, sms, st, k_splits, split_rows,

@@ -207,13 +207,13 @@ __device__ __noinline__ void nvls_reduce_slab_impl(const EpiParams& ep, const Ge
   }
 }
 
-template <int MODE, bool A_MN, bool B_MN, int CG, int STAGES, int NB = 1>
+template <int MODE, bool A_MN, bool B_MN, int CG, int STAGES, int NB = 1, int SKEW = 0>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const __grid_constant__ CUtensorMap tmC, const GemmShape sh_in, const EpiParams ep) {
   using TL = Tiling<CG>;
-  static_assert(NB == 1 || (NB == 2 && CG == 2 && MODE != EPI_LSE && MODE != EPI_DZ && MODE != EPI_BF16_GROUPED),
-                "wide tiles: CTA pairs, plain store epilogues");
+  static_assert(NB == 1 || (NB == 2 && CG == 2 && MODE != EPI_BF16_GROUPED), "wide tiles: CTA pairs, not grouped");
+  static_assert(SKEW < STAGES, "the skewed head/tail holds SKEW stages");
   constexpr int TN = BN * NB;                 // tile columns
   constexpr int NACC = NB == 1 ? 2 : 1;       // TMEM accumulators (512 columns in total)
   constexpr int B_STAGE_ALL = NB * TL::B_STAGE;
@@ -400,7 +400,96 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       for (int p = last_sync + 1; p <= ep.max_sync; ++p) red_release_add(ep.sync_ctr + p, 1u);
   } else if (warp == 1) {
     // ----------------------------------------------------------- MMA issuer
-    if (leader) {
+    if (leader && NB == 2) {
+      // Wide tiles: TMEM half h (columns h*256..) accumulates the N = 256 block h. The
+      // first and last D k-blocks of a tile run block 0 before block 1, so the
+      // epilogue drains half 0 of tile i while block 1 finishes its tail, and half 1
+      // while block 0 of tile i+1 runs its head (D*512 MMA cycles of cover each).
+      constexpr uint32_t idesc = umma_idesc_bf16(TL::TILE_M, BN, A_MN, B_MN);
+      int s = 0;
+      uint32_t ph = 0;
+      uint32_t aph = 0;
+      const uint32_t a_base = smem_u32(sA), b_base = smem_u32(sB);
+      auto issue = [&](int st, int nb, bool first) {
+        const uint32_t a0 = a_base + st * TL::A_STAGE;
+        const uint32_t bn = b_base + st * B_STAGE_ALL + nb * TL::B_STAGE;
+#pragma unroll
+        for (int k = 0; k < BK / 16; ++k) {
+          const uint64_t ad = A_MN ? sw128_desc(a0 + k * 2048, 8192, 1024) : sw128_desc(a0 + k * 32, 16, 1024);
+          const uint64_t bd = B_MN ? sw128_desc(bn + k * 2048, 8192, 1024) : sw128_desc(bn + k * 32, 16, 1024);
+          umma_bf16_pair(tmem_base + nb * BN, ad, bd, idesc, !first || (k != 0));
+        }
+      };
+      auto adv = [&](int& st, uint32_t& p) {
+        if (++st == STAGES) {
+          st = 0;
+          p ^= 1;
+        }
+      };
+      for (int tile = unit; tile < total; tile += n_units) {
+        int kb0 = 0, kb1 = sh.k_blocks;
+        tile_k_range(tile, sh, kb0, kb1);
+        const int L = kb1 > kb0 ? kb1 - kb0 : 0;
+        const int D = SKEW < L / 2 ? SKEW : L / 2;
+        // head: block 0 over k-blocks kb0..kb0+D-1, then block 1 over the same stages
+        mbar_wait(&tempty[0], aph ^ 1);
+        tc_fence_after();
+        int sh_s = s;
+        uint32_t sh_p = ph;
+        for (int j = 0; j < D; ++j) {
+          mbar_wait(&full[sh_s], sh_p);
+          tc_fence_after();
+          if (elect_one()) issue(sh_s, 0, j == 0);
+          __syncwarp();
+          adv(sh_s, sh_p);
+        }
+        mbar_wait(&tempty[1], aph ^ 1);
+        tc_fence_after();
+        for (int j = 0; j < D; ++j) {
+          if (elect_one()) {
+            issue(s, 1, j == 0);
+            umma_commit_pair(&empty[s], 0x3);
+          }
+          __syncwarp();
+          adv(s, ph);
+        }
+        // middle: both blocks per k-block
+        for (int kb = kb0 + D; kb < kb1 - D; ++kb) {
+          mbar_wait(&full[s], ph);
+          tc_fence_after();
+          if (elect_one()) {
+            issue(s, 0, kb == kb0);
+            issue(s, 1, kb == kb0);
+            umma_commit_pair(&empty[s], 0x3);
+          }
+          __syncwarp();
+          adv(s, ph);
+        }
+        // tail: block 0 finishes first -> half 0 is handed to the epilogue early
+        int st_s = s;
+        uint32_t st_p = ph;
+        for (int j = 0; j < D; ++j) {
+          mbar_wait(&full[st_s], st_p);
+          tc_fence_after();
+          if (elect_one()) issue(st_s, 0, false);
+          __syncwarp();
+          adv(st_s, st_p);
+        }
+        if (elect_one()) umma_commit_pair(&tfull[0], 0x3);
+        __syncwarp();
+        for (int j = 0; j < D; ++j) {
+          if (elect_one()) {
+            issue(s, 1, false);
+            umma_commit_pair(&empty[s], 0x3);
+          }
+          __syncwarp();
+          adv(s, ph);
+        }
+        if (elect_one()) umma_commit_pair(&tfull[1], 0x3);
+        __syncwarp();
+        aph ^= 1;
+      }
+    } else if (leader) {
       constexpr uint32_t idesc = umma_idesc_bf16(TL::TILE_M, BN, A_MN, B_MN);
       int s = 0;
       uint32_t ph = 0;
@@ -496,176 +585,180 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         row = static_cast<int64_t>(m) * TL::TILE_M + r_in_tile;
         row_ok = row < ep.rows;
       }
-      const int n0 = n * TN;
-      mbar_wait_sleep(&tfull[acc], aph);
-      tc_fence_after();
-      const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * TN;
+      for (int h = 0; h < NB; ++h) {
+        const int bi = NB == 2 ? h : acc;  // TMEM half (wide tiles) or accumulator
+        const int n0 = n * TN + h * BN;
+        mbar_wait_sleep(&tfull[bi], aph);
+        tc_fence_after();
+        const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + bi * BN;
 
-      if constexpr (MODE == EPI_LSE) {
-        int64_t y = row_ok ? static_cast<int64_t>(ep.targets[row]) - ep.vocab_offset : -1;
-        if (y >= ep.cols) y = -1;  // target lives in another vocab shard
-        const int64_t tl64 = y - n0;
-        const int tl = (tl64 >= 0 && tl64 < BN) ? static_cast<int>(tl64) : -1;
-        const int64_t nv64 = ep.cols - n0;
-        const int nvalid = nv64 < BN ? static_cast<int>(nv64) : BN;
-        float mrun = -1e30f, srun = 0.f, trun = 0.f, zt = -INFINITY;
-#pragma unroll 1
-        for (int c = 0; c < BN / 32; ++c) {
-          uint32_t r[32];
-          tmem_ld32(taddr + c * 32, r);
-          tmem_wait_ld();
-          if (c == BN / 32 - 1) release_tmem(acc);
-          float u[32];
-#pragma unroll
-          for (int j = 0; j < 32; ++j) u[j] = __uint_as_float(r[j]) * ep.scale_log2;
-          if (nvalid < BN) {
-#pragma unroll
-            for (int j = 0; j < 32; ++j)
-              if (c * 32 + j >= nvalid) u[j] = -1e30f;
-          }
-          if (tl >= c * 32 && tl < c * 32 + 32) {
-            const int jt = tl - c * 32;
-            float z = -INFINITY;
-#pragma unroll
-            for (int j = 0; j < 32; ++j) z = fmaxf(z, (j == jt) ? __uint_as_float(r[j]) : -INFINITY);
-            zt = z * ep.inv_temperature;
-          }
-          float cm = u[0];
-#pragma unroll
-          for (int j = 1; j < 32; ++j) cm = fmaxf(cm, u[j]);
-          const float mn = fmaxf(mrun, cm);
-          const float sc = ex2f(mrun - mn);
-          trun = sc * fmaf(srun, mrun - mn, trun);
-          srun *= sc;
-          mrun = mn;
-#pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            const float d = u[j] - mn;
-            const float e = ex2f(d);
-            srun += e;
-            trun = fmaf(e, d, trun);
-          }
-        }
-        if (row_ok) {
-          constexpr float LN2 = 0.69314718055994530942f;
-          ep.partials[static_cast<int64_t>(n) * ep.rows + row] = make_float4(mrun * LN2, srun, trun * LN2, zt);
-        }
-      } else if (GROUPED && masked) {
-        // masked per-row stores: rows past the group's end belong to the next group
-        const int64_t cleft = ep.cols - n0;
-        const int ncols = cleft < BN ? static_cast<int>(cleft) : BN;
-        uint16_t* orow = ep.grouped_out + row * ep.cols + n0;
-        const float rs = (ep.row_scale && row_ok) ? ep.row_scale[row] : 1.f;
-#pragma unroll 1
-        for (int c = 0; c < BN / 32; ++c) {
-          uint32_t r[32];
-          tmem_ld32(taddr + c * 32, r);
-          tmem_wait_ld();
-          if (c == BN / 32 - 1) release_tmem(acc);
-          if (row_ok && c * 32 < ncols) {
-            uint32_t w[16];
-#pragma unroll
-            for (int j = 0; j < 16; ++j)
-              w[j] = pack_bf16x2(__uint_as_float(r[2 * j]) * rs, __uint_as_float(r[2 * j + 1]) * rs);
-            uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
-#pragma unroll
-            for (int j = 0; j < 4; ++j) dst[j] = make_uint4(w[4 * j], w[4 * j + 1], w[4 * j + 2], w[4 * j + 3]);
-          }
-        }
-      } else {
-        // store epilogues: TMEM -> regs -> (math) -> swizzled smem -> TMA store
-        float g = 0.f, b2 = 0.f;
-        int tl = -1;
-        const float rs = (GROUPED && ep.row_scale && row_ok) ? ep.row_scale[row] : 1.f;
-        if constexpr (MODE == EPI_DZ) {
-          if (row_ok) {
-            g = ep.coef[row] * ep.inv_temperature;
-            b2 = ep.lse[row] * 1.4426950408889634f;
-            const int64_t yl = static_cast<int64_t>(ep.targets[row]) - ep.vocab_offset;
-            const int64_t t64 = yl - n0;
-            tl = (yl < ep.cols && t64 >= 0 && t64 < BN) ? static_cast<int>(t64) : -1;
-          }
-        }
-        constexpr int COLS = (MODE == EPI_DZ || MODE == EPI_BF16 || MODE == EPI_BF16_GROUPED) ? 64 : 32;
-        // a tile with an empty K range (sparse backward, every row masked) stores zeros:
-        // the MMA issued nothing, so TMEM holds no accumulator for it
-        bool empty_k = false;
-        if constexpr (!GROUPED) {
-          int kb0, kb1;
-          tile_k_range(tile, sh, kb0, kb1);
-          empty_k = kb1 <= kb0;
-        }
-#pragma unroll 1
-        for (int c = 0; c < TN / COLS; ++c) {
-          uint32_t w[32];
-          if constexpr (COLS == 64) {
-            uint32_t r0[32], r1[32];
-            tmem_ld32(taddr + c * 64, r0);
-            tmem_ld32(taddr + c * 64 + 32, r1);
+        if constexpr (MODE == EPI_LSE) {
+          int64_t y = row_ok ? static_cast<int64_t>(ep.targets[row]) - ep.vocab_offset : -1;
+          if (y >= ep.cols) y = -1;  // target lives in another vocab shard
+          const int64_t tl64 = y - n0;
+          const int tl = (tl64 >= 0 && tl64 < BN) ? static_cast<int>(tl64) : -1;
+          const int64_t nv64 = ep.cols - n0;
+          const int nvalid = nv64 < BN ? static_cast<int>(nv64) : BN;
+          float mrun = -1e30f, srun = 0.f, trun = 0.f, zt = -INFINITY;
+  #pragma unroll 1
+          for (int c = 0; c < BN / 32; ++c) {
+            uint32_t r[32];
+            tmem_ld32(taddr + c * 32, r);
             tmem_wait_ld();
-            if (c == TN / COLS - 1) release_tmem(acc);
-#pragma unroll
-            for (int j = 0; j < 16; ++j) {
-              float v0 = __uint_as_float(r0[2 * j]), v1 = __uint_as_float(r0[2 * j + 1]);
-              float v2 = __uint_as_float(r1[2 * j]), v3 = __uint_as_float(r1[2 * j + 1]);
-              if constexpr (MODE == EPI_DZ) {
-                v0 = g * ex2f(fmaf(v0, ep.scale_log2, -b2));
-                v1 = g * ex2f(fmaf(v1, ep.scale_log2, -b2));
-                v2 = g * ex2f(fmaf(v2, ep.scale_log2, -b2));
-                v3 = g * ex2f(fmaf(v3, ep.scale_log2, -b2));
-                const int cb = c * 64;
-                if (tl == cb + 2 * j) v0 -= g;
-                if (tl == cb + 2 * j + 1) v1 -= g;
-                if (tl == cb + 32 + 2 * j) v2 -= g;
-                if (tl == cb + 32 + 2 * j + 1) v3 -= g;
-              }
-              if constexpr (GROUPED) {
-                v0 *= rs;
-                v1 *= rs;
-                v2 *= rs;
-                v3 *= rs;
-              }
-              w[j] = empty_k ? 0u : pack_bf16x2(v0, v1);
-              w[16 + j] = empty_k ? 0u : pack_bf16x2(v2, v3);
+            if (c == BN / 32 - 1) release_tmem(bi);
+            float u[32];
+  #pragma unroll
+            for (int j = 0; j < 32; ++j) u[j] = __uint_as_float(r[j]) * ep.scale_log2;
+            if (nvalid < BN) {
+  #pragma unroll
+              for (int j = 0; j < 32; ++j)
+                if (c * 32 + j >= nvalid) u[j] = -1e30f;
             }
-          } else {
-            uint32_t r0[32];
-            tmem_ld32(taddr + c * 32, r0);
+            if (tl >= c * 32 && tl < c * 32 + 32) {
+              const int jt = tl - c * 32;
+              float z = -INFINITY;
+  #pragma unroll
+              for (int j = 0; j < 32; ++j) z = fmaxf(z, (j == jt) ? __uint_as_float(r[j]) : -INFINITY);
+              zt = z * ep.inv_temperature;
+            }
+            float cm = u[0];
+  #pragma unroll
+            for (int j = 1; j < 32; ++j) cm = fmaxf(cm, u[j]);
+            const float mn = fmaxf(mrun, cm);
+            const float sc = ex2f(mrun - mn);
+            trun = sc * fmaf(srun, mrun - mn, trun);
+            srun *= sc;
+            mrun = mn;
+  #pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              const float d = u[j] - mn;
+              const float e = ex2f(d);
+              srun += e;
+              trun = fmaf(e, d, trun);
+            }
+          }
+          if (row_ok && n0 < ep.cols) {  // one partial per 256-column block
+            constexpr float LN2 = 0.69314718055994530942f;
+            ep.partials[static_cast<int64_t>(n * NB + h) * ep.rows + row] =
+                make_float4(mrun * LN2, srun, trun * LN2, zt);
+          }
+        } else if (GROUPED && masked) {
+          // masked per-row stores: rows past the group's end belong to the next group
+          const int64_t cleft = ep.cols - n0;
+          const int ncols = cleft < BN ? static_cast<int>(cleft) : BN;
+          uint16_t* orow = ep.grouped_out + row * ep.cols + n0;
+          const float rs = (ep.row_scale && row_ok) ? ep.row_scale[row] : 1.f;
+  #pragma unroll 1
+          for (int c = 0; c < BN / 32; ++c) {
+            uint32_t r[32];
+            tmem_ld32(taddr + c * 32, r);
             tmem_wait_ld();
-            if (c == TN / COLS - 1) release_tmem(acc);
-#pragma unroll
-            for (int j = 0; j < 32; ++j) w[j] = empty_k ? 0u : r0[j];
+            if (c == BN / 32 - 1) release_tmem(bi);
+            if (row_ok && c * 32 < ncols) {
+              uint32_t w[16];
+  #pragma unroll
+              for (int j = 0; j < 16; ++j)
+                w[j] = pack_bf16x2(__uint_as_float(r[2 * j]) * rs, __uint_as_float(r[2 * j + 1]) * rs);
+              uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
+  #pragma unroll
+              for (int j = 0; j < 4; ++j) dst[j] = make_uint4(w[4 * j], w[4 * j + 1], w[4 * j + 2], w[4 * j + 3]);
+            }
           }
-          const uint32_t buf = buf0 + (chunk_ctr & 1) * EPI_BUF_BYTES;
-          if (lane == 0) bulk_wait_read<1>();
-          __syncwarp();
-          stage_row(buf, lane, w);
-          fence_async_smem();
-          __syncwarp();
-          if (lane == 0) {
-            const int c0 = n0 + c * COLS;
-            const int c1 = GROUPED ? tile_row0 + rank * 128 + q * 32
-                                   : m * TL::TILE_M + rank * 128 + q * 32 +
-                                         (tile / (sh.m_blocks * sh.n_blocks)) * sh.split_rows;
-            if constexpr (MODE == EPI_F32_ADD)
-              tma_reduce_add_2d(&tmC, sEpi + (buf - smem_u32(sEpi)), c0, c1);
-            else
-              tma_store_2d(&tmC, sEpi + (buf - smem_u32(sEpi)), c0, c1);
-            bulk_commit();
+        } else {
+          // store epilogues: TMEM -> regs -> (math) -> swizzled smem -> TMA store
+          float g = 0.f, b2 = 0.f;
+          int tl = -1;
+          const float rs = (GROUPED && ep.row_scale && row_ok) ? ep.row_scale[row] : 1.f;
+          if constexpr (MODE == EPI_DZ) {
+            if (row_ok) {
+              g = ep.coef[row] * ep.inv_temperature;
+              b2 = ep.lse[row] * 1.4426950408889634f;
+              const int64_t yl = static_cast<int64_t>(ep.targets[row]) - ep.vocab_offset;
+              const int64_t t64 = yl - n0;
+              tl = (yl < ep.cols && t64 >= 0 && t64 < BN) ? static_cast<int>(t64) : -1;
+            }
           }
-          ++chunk_ctr;
+          constexpr int COLS = (MODE == EPI_DZ || MODE == EPI_BF16 || MODE == EPI_BF16_GROUPED) ? 64 : 32;
+          // a tile with an empty K range (sparse backward, every row masked) stores zeros:
+          // the MMA issued nothing, so TMEM holds no accumulator for it
+          bool empty_k = false;
+          if constexpr (!GROUPED) {
+            int kb0, kb1;
+            tile_k_range(tile, sh, kb0, kb1);
+            empty_k = kb1 <= kb0;
+          }
+  #pragma unroll 1
+          for (int c = 0; c < BN / COLS; ++c) {
+            uint32_t w[32];
+            if constexpr (COLS == 64) {
+              uint32_t r0[32], r1[32];
+              tmem_ld32(taddr + c * 64, r0);
+              tmem_ld32(taddr + c * 64 + 32, r1);
+              tmem_wait_ld();
+              if (c == BN / COLS - 1) release_tmem(bi);
+  #pragma unroll
+              for (int j = 0; j < 16; ++j) {
+                float v0 = __uint_as_float(r0[2 * j]), v1 = __uint_as_float(r0[2 * j + 1]);
+                float v2 = __uint_as_float(r1[2 * j]), v3 = __uint_as_float(r1[2 * j + 1]);
+                if constexpr (MODE == EPI_DZ) {
+                  v0 = g * ex2f(fmaf(v0, ep.scale_log2, -b2));
+                  v1 = g * ex2f(fmaf(v1, ep.scale_log2, -b2));
+                  v2 = g * ex2f(fmaf(v2, ep.scale_log2, -b2));
+                  v3 = g * ex2f(fmaf(v3, ep.scale_log2, -b2));
+                  const int cb = c * 64;
+                  if (tl == cb + 2 * j) v0 -= g;
+                  if (tl == cb + 2 * j + 1) v1 -= g;
+                  if (tl == cb + 32 + 2 * j) v2 -= g;
+                  if (tl == cb + 32 + 2 * j + 1) v3 -= g;
+                }
+                if constexpr (GROUPED) {
+                  v0 *= rs;
+                  v1 *= rs;
+                  v2 *= rs;
+                  v3 *= rs;
+                }
+                w[j] = empty_k ? 0u : pack_bf16x2(v0, v1);
+                w[16 + j] = empty_k ? 0u : pack_bf16x2(v2, v3);
+              }
+            } else {
+              uint32_t r0[32];
+              tmem_ld32(taddr + c * 32, r0);
+              tmem_wait_ld();
+              if (c == BN / COLS - 1) release_tmem(bi);
+  #pragma unroll
+              for (int j = 0; j < 32; ++j) w[j] = empty_k ? 0u : r0[j];
+            }
+            const uint32_t buf = buf0 + (chunk_ctr & 1) * EPI_BUF_BYTES;
+            if (lane == 0) bulk_wait_read<1>();
+            __syncwarp();
+            stage_row(buf, lane, w);
+            fence_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              const int c0 = n0 + c * COLS;
+              const int c1 = GROUPED ? tile_row0 + rank * 128 + q * 32
+                                     : m * TL::TILE_M + rank * 128 + q * 32 +
+                                           (tile / (sh.m_blocks * sh.n_blocks)) * sh.split_rows;
+              if constexpr (MODE == EPI_F32_ADD)
+                tma_reduce_add_2d(&tmC, sEpi + (buf - smem_u32(sEpi)), c0, c1);
+              else
+                tma_store_2d(&tmC, sEpi + (buf - smem_u32(sEpi)), c0, c1);
+              bulk_commit();
+            }
+            ++chunk_ctr;
+          }
         }
-        if constexpr (MODE == EPI_F32_NVLS) {
-          // publish this warp's slab once its stores are globally visible
-          if (lane == 0) {
-            bulk_wait_all();
-            fence_async_global();
-            fence_sys();
-            st_release_sys(ep.nvls_flags[ep.nvls_rank] + nvls_slab(tile, rank, q), ep.nvls_epoch);
-          }
-          __syncwarp();
-          if (it >= ep.nvls_lag) nvls_reduce_slab(ep, sh, unit + (it - ep.nvls_lag) * n_units, rank, q, lane);
+      }
+      if constexpr (MODE == EPI_F32_NVLS) {
+        // publish this warp's slab once its stores are globally visible
+        if (lane == 0) {
+          bulk_wait_all();
+          fence_async_global();
+          fence_sys();
+          st_release_sys(ep.nvls_flags[ep.nvls_rank] + nvls_slab(tile, rank, q), ep.nvls_epoch);
         }
+        __syncwarp();
+        if (it >= ep.nvls_lag) nvls_reduce_slab(ep, sh, unit + (it - ep.nvls_lag) * n_units, rank, q, lane);
       }
       ++it;
       if (NACC == 2) acc ^= 1;
