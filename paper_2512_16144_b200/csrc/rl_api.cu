@@ -210,7 +210,7 @@ int sync_every_for(int kid) {
   return cache[kid];
 }
 // Wide 256 x 512 pair tiles (NB = 2, rl_gemm.cuh): RL_WIDE[_<K>] = 0/1, default on
-// for K1 (FWD), K5 (DH) and K6 (DW); RL_SKEW = 0/2/3 k-blocks of block-0-first MMA
+// for K1 (FWD), K5 (DH), K6 (DW) and the Newton-Schulz GEMMs (NS: 41.0 -> 38.6 ms); RL_SKEW = 0/2/3 k-blocks of block-0-first MMA
 // order at both ends of a tile (default 3), which hides the epilogue of one TMEM
 // half. K4 (DZ) stays narrow: its exp + bf16-store epilogue per half is longer
 // than that cover (measured: K4 15.6 -> 17.9 ms wide, K1 15.6 -> 15.2 ms).
@@ -219,7 +219,7 @@ bool wide_for(int kid) {
   static bool init[32] = {};
   if (kid < 0 || kid >= 32) return false;
   if (!init[kid]) {
-    const bool dflt = kid == RL_K_FWD_GEMM || kid == RL_K_DH_GEMM || kid == RL_K_DW_GEMM;
+    const bool dflt = kid == RL_K_FWD_GEMM || kid == RL_K_DH_GEMM || kid == RL_K_DW_GEMM || kid == RL_K_NS_GEMM;
     cache[kid] = env_int("RL_WIDE", kid, dflt ? 1 : 0);
     init[kid] = true;
   }
@@ -287,11 +287,12 @@ rl_status launch_gemm_cg(int kid, const CUtensorMap& a, const CUtensorMap& b, co
   ep2.sync_every = 0;
   if (g_sync_ctr && sync_every_for(kid) > 0) {
     const int64_t max_tiles = (tiles + units - 1) / units;
-    const int64_t max_sync = (max_tiles * sh.k_blocks - 1) / sync_every_for(kid);
+    const int se = sync_every_for(kid);
+    const int64_t max_sync = (max_tiles * sh.k_blocks - 1) / se;
     if (max_sync > 0 && max_sync < kMaxSyncPoints) {
       RL_CUDA(cudaMemsetAsync(g_sync_ctr, 0, static_cast<size_t>(max_sync + 1) * 4, st));
       ep2.sync_ctr = g_sync_ctr;
-      ep2.sync_every = sync_every_for(kid);
+      ep2.sync_every = se;
       ep2.sync_slack = sync_slack_for(kid);
       ep2.max_sync = static_cast<int>(max_sync);
     }
