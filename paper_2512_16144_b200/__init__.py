@@ -14,7 +14,7 @@ import os
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "librl.so")
+LIB_PATH = os.environ.get("RL_LIBRARY") or os.path.join(_HERE, "librl.so")  # RL_LIBRARY: another build (A/B runs)
 
 RL_OK = 0
 STATUS_NAMES = {0: "RL_OK", 1: "RL_ERR_INVALID_ARGUMENT", 2: "RL_ERR_SHAPE", 3: "RL_ERR_UNSUPPORTED",

@@ -400,94 +400,77 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       for (int p = last_sync + 1; p <= ep.max_sync; ++p) red_release_add(ep.sync_ctr + p, 1u);
   } else if (warp == 1) {
     // ----------------------------------------------------------- MMA issuer
-    if (leader && NB == 2) {
+    if constexpr (NB == 2) {
       // Wide tiles: TMEM half h (columns h*256..) accumulates the N = 256 block h. The
       // first and last D k-blocks of a tile run block 0 before block 1, so the
       // epilogue drains half 0 of tile i while block 1 finishes its tail, and half 1
       // while block 0 of tile i+1 runs its head (D*512 MMA cycles of cover each).
-      constexpr uint32_t idesc = umma_idesc_bf16(TL::TILE_M, BN, A_MN, B_MN);
-      int s = 0;
-      uint32_t ph = 0;
-      uint32_t aph = 0;
-      const uint32_t a_base = smem_u32(sA), b_base = smem_u32(sB);
-      auto issue = [&](int st, int nb, bool first) {
-        const uint32_t a0 = a_base + st * TL::A_STAGE;
-        const uint32_t bn = b_base + st * B_STAGE_ALL + nb * TL::B_STAGE;
+      // One op per (k-block, block set), one issue site (keeps the kernel small):
+      //   ops [0, D)            head, block 0      (wait full)
+      //   ops [D, 2D)           head, block 1      (release stage)
+      //   ops [2D, L)           both blocks        (wait full, release stage)
+      //   ops [L, L+D)          tail, block 0      (wait full), then tfull[0]
+      //   ops [L+D, L+2D)       tail, block 1      (release stage), then tfull[1]
+      if (leader) {
+        constexpr uint32_t idesc = umma_idesc_bf16(TL::TILE_M, BN, A_MN, B_MN);
+        uint32_t aph = 0;
+        int g0 = 0;  // k-blocks consumed before this tile (stage = g % STAGES)
+        const uint32_t a_base = smem_u32(sA), b_base = smem_u32(sB);
+        for (int tile = unit; tile < total; tile += n_units) {
+          int kb0 = 0, kb1 = sh.k_blocks;
+          tile_k_range(tile, sh, kb0, kb1);
+          const int L = kb1 > kb0 ? kb1 - kb0 : 0;
+          const int D = SKEW < L / 2 ? SKEW : L / 2;
+          mbar_wait(&tempty[0], aph ^ 1);
+          if (D == 0) mbar_wait(&tempty[1], aph ^ 1);
+          tc_fence_after();
+#pragma unroll 1
+          for (int op = 0; op < L + 2 * D; ++op) {
+            int j, nb_lo, nb_hi;
+            bool wait_full, release;
+            if (op < D) { j = op; nb_lo = 0; nb_hi = 0; wait_full = true; release = false; }
+            else if (op < 2 * D) { j = op - D; nb_lo = 1; nb_hi = 1; wait_full = false; release = true; }
+            else if (op < L) { j = op - D; nb_lo = 0; nb_hi = 1; wait_full = true; release = true; }
+            else if (op < L + D) { j = op - D; nb_lo = 0; nb_hi = 0; wait_full = true; release = false; }
+            else { j = op - 2 * D; nb_lo = 1; nb_hi = 1; wait_full = false; release = true; }
+            if (op == D && D > 0) {
+              mbar_wait(&tempty[1], aph ^ 1);
+              tc_fence_after();
+            }
+            const int g = g0 + j;
+            const int st = g % STAGES;
+            if (wait_full) {
+              mbar_wait(&full[st], (g / STAGES) & 1);
+              tc_fence_after();
+            }
+            if (elect_one()) {
+              const uint32_t a0 = a_base + st * TL::A_STAGE;
+#pragma unroll 1
+              for (int nb = nb_lo; nb <= nb_hi; ++nb) {
+                const uint32_t bn = b_base + st * B_STAGE_ALL + nb * TL::B_STAGE;
 #pragma unroll
-        for (int k = 0; k < BK / 16; ++k) {
-          const uint64_t ad = A_MN ? sw128_desc(a0 + k * 2048, 8192, 1024) : sw128_desc(a0 + k * 32, 16, 1024);
-          const uint64_t bd = B_MN ? sw128_desc(bn + k * 2048, 8192, 1024) : sw128_desc(bn + k * 32, 16, 1024);
-          umma_bf16_pair(tmem_base + nb * BN, ad, bd, idesc, !first || (k != 0));
-        }
-      };
-      auto adv = [&](int& st, uint32_t& p) {
-        if (++st == STAGES) {
-          st = 0;
-          p ^= 1;
-        }
-      };
-      for (int tile = unit; tile < total; tile += n_units) {
-        int kb0 = 0, kb1 = sh.k_blocks;
-        tile_k_range(tile, sh, kb0, kb1);
-        const int L = kb1 > kb0 ? kb1 - kb0 : 0;
-        const int D = SKEW < L / 2 ? SKEW : L / 2;
-        // head: block 0 over k-blocks kb0..kb0+D-1, then block 1 over the same stages
-        mbar_wait(&tempty[0], aph ^ 1);
-        tc_fence_after();
-        int sh_s = s;
-        uint32_t sh_p = ph;
-        for (int j = 0; j < D; ++j) {
-          mbar_wait(&full[sh_s], sh_p);
-          tc_fence_after();
-          if (elect_one()) issue(sh_s, 0, j == 0);
-          __syncwarp();
-          adv(sh_s, sh_p);
-        }
-        mbar_wait(&tempty[1], aph ^ 1);
-        tc_fence_after();
-        for (int j = 0; j < D; ++j) {
-          if (elect_one()) {
-            issue(s, 1, j == 0);
-            umma_commit_pair(&empty[s], 0x3);
+                for (int k = 0; k < BK / 16; ++k) {
+                  const uint64_t ad =
+                      A_MN ? sw128_desc(a0 + k * 2048, 8192, 1024) : sw128_desc(a0 + k * 32, 16, 1024);
+                  const uint64_t bd =
+                      B_MN ? sw128_desc(bn + k * 2048, 8192, 1024) : sw128_desc(bn + k * 32, 16, 1024);
+                  umma_bf16_pair(tmem_base + nb * BN, ad, bd, idesc, (j != 0) || (k != 0));
+                }
+              }
+              if (release) umma_commit_pair(&empty[st], 0x3);
+              if (op == L + D - 1 || (D == 0 && op == L - 1)) umma_commit_pair(&tfull[0], 0x3);
+              if (op == L + 2 * D - 1) umma_commit_pair(&tfull[1], 0x3);
+            }
+            __syncwarp();
+          }
+          if (L == 0 && elect_one()) {  // empty K range: nothing to wait for
+            umma_commit_pair(&tfull[0], 0x3);
+            umma_commit_pair(&tfull[1], 0x3);
           }
           __syncwarp();
-          adv(s, ph);
+          g0 += L;
+          aph ^= 1;
         }
-        // middle: both blocks per k-block
-        for (int kb = kb0 + D; kb < kb1 - D; ++kb) {
-          mbar_wait(&full[s], ph);
-          tc_fence_after();
-          if (elect_one()) {
-            issue(s, 0, kb == kb0);
-            issue(s, 1, kb == kb0);
-            umma_commit_pair(&empty[s], 0x3);
-          }
-          __syncwarp();
-          adv(s, ph);
-        }
-        // tail: block 0 finishes first -> half 0 is handed to the epilogue early
-        int st_s = s;
-        uint32_t st_p = ph;
-        for (int j = 0; j < D; ++j) {
-          mbar_wait(&full[st_s], st_p);
-          tc_fence_after();
-          if (elect_one()) issue(st_s, 0, false);
-          __syncwarp();
-          adv(st_s, st_p);
-        }
-        if (elect_one()) umma_commit_pair(&tfull[0], 0x3);
-        __syncwarp();
-        for (int j = 0; j < D; ++j) {
-          if (elect_one()) {
-            issue(s, 1, false);
-            umma_commit_pair(&empty[s], 0x3);
-          }
-          __syncwarp();
-          adv(s, ph);
-        }
-        if (elect_one()) umma_commit_pair(&tfull[1], 0x3);
-        __syncwarp();
-        aph ^= 1;
       }
     } else if (leader) {
       constexpr uint32_t idesc = umma_idesc_bf16(TL::TILE_M, BN, A_MN, B_MN);
@@ -585,6 +568,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         row = static_cast<int64_t>(m) * TL::TILE_M + r_in_tile;
         row_ok = row < ep.rows;
       }
+#pragma unroll 1
       for (int h = 0; h < NB; ++h) {
         const int bi = NB == 2 ? h : acc;  // TMEM half (wide tiles) or accumulator
         const int n0 = n * TN + h * BN;
