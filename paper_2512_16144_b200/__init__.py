@@ -397,10 +397,33 @@ def rl_last_launch_count() -> int:
     return int(load_library().rl_last_launch_count())
 
 
-def read_report(report: torch.Tensor) -> rl_loss_report:
-    """Copy a device report ([48] uint8) to the host (synchronises)."""
+FAULT_COUNTERS = ("nonfinite_inputs", "bad_targets", "bad_offsets")
+
+
+class RLDataFault(RuntimeError):
+    """Data-dependent input faults that librl counted and neutralised on the device
+    (include/rl.h: the token or rollout was treated as masked, coef 0)."""
+
+    def __init__(self, report: "rl_loss_report"):
+        self.report = report
+        bad = ", ".join(f"{k}={getattr(report, k)}" for k in FAULT_COUNTERS if getattr(report, k))
+        super().__init__(f"librl counted input faults: {bad}")
+
+
+def check_faults(report: "rl_loss_report") -> "rl_loss_report":
+    """Raise RLDataFault if any fault counter of a host report is non-zero."""
+    if any(getattr(report, k) for k in FAULT_COUNTERS):
+        raise RLDataFault(report)
+    return report
+
+
+def read_report(report: torch.Tensor, check: bool = False) -> rl_loss_report:
+    """Copy a device report ([48] uint8) to the host (synchronises). With check=True,
+    raise RLDataFault if the step counted non-finite log-probs, bad targets or bad
+    offsets (they were neutralised, but the batch is malformed)."""
     b = bytes(report.cpu().numpy().tobytes())
-    return rl_loss_report.from_buffer_copy(b)
+    rep = rl_loss_report.from_buffer_copy(b)
+    return check_faults(rep) if check else rep
 
 
 def new_report(device=None) -> torch.Tensor:

@@ -65,3 +65,15 @@ def test_host_validation_before_any_device_work(lib):
     p = rl.make_params(4, 10.0, alpha=0.6, beta=0.9)
     st = lib.rl_loss_coef(ctypes.byref(p), 10, 100, *([ctypes.c_void_p(16)] * 10), None, 0, None)
     assert st == 1
+
+
+def test_fault_counters_raise_on_check():
+    """Data faults are counted on the device and neutralised; the binding turns
+    non-zero counters into RLDataFault when asked (SURVEY §8(b) error split)."""
+    import paper_2512_16144_b200 as rl
+    ok = rl.rl_loss_report(loss=-0.5, kept_tokens=10)
+    assert rl.check_faults(ok) is ok
+    for key in rl.FAULT_COUNTERS:
+        bad = rl.rl_loss_report(**{key: 2})
+        with pytest.raises(rl.RLDataFault, match=key):
+            rl.check_faults(bad)
