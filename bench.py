@@ -145,6 +145,28 @@ def run_oracle_step(b, h64, w64, infer):
     return oracle.policy_loss_fwd_bwd(h64, w64, b.targets, infer, b.rewards, b.rollout_offsets, b.loss_mask)
 
 
+def host_info():
+    """CPU model and BLAS library/threads of the host that times the oracle."""
+    model = "unknown"
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    blas = "unknown"
+    try:
+        from threadpoolctl import threadpool_info
+        libs = [d for d in threadpool_info() if d.get("user_api") == "blas"]
+        if libs:
+            blas = f"{libs[0].get('internal_api')} {libs[0].get('version')} ({libs[0].get('num_threads')} threads)"
+    except Exception:  # noqa: BLE001
+        pass
+    return {"cpu_model": model, "nproc": os.cpu_count(), "blas": blas}
+
+
 def blas_threads():
     try:
         from threadpoolctl import threadpool_info
@@ -175,7 +197,7 @@ def cpu_baseline(wl, budget_s=15.0):
     return {"value": b.T / dt, "unit": "tokens/s", "cores": blas_threads(), "kind": "oracle",
             "sample": f"{b.T} tokens ({len(b.rollout_offsets) - 1} rollouts) of the {wl.name} shape "
                       f"(H={wl.hidden}, V={wl.vocab}), full fwd+bwd in fp64 numpy; bf16->fp64 decode excluded; "
-                      f"{dt:.1f} s"}
+                      f"{dt:.1f} s", **host_info()}
 
 
 def reference_arm(args):
@@ -199,7 +221,8 @@ def reference_arm(args):
     dt = float(np.mean(times))
     v = b.T / dt
     cb = {"value": v, "unit": "tokens/s", "cores": blas_threads(), "kind": "oracle",
-          "sample": f"{b.T} tokens per step of the {wl.name} shape (H={wl.hidden}, V={wl.vocab}), fp64 numpy oracle"}
+          "sample": f"{b.T} tokens per step of the {wl.name} shape (H={wl.hidden}, V={wl.vocab}), fp64 numpy oracle",
+          **host_info()}
     emit({"impl": "reference", "metric": METRIC, "value": v, "unit": "tokens/s", "n_gpus": world,
           "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
           "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
@@ -399,6 +422,7 @@ def main_ours(args):
             "peak_source": f"bf16_tflops_sustained, {peak_src}",
             "step_frac_8HV": (step_flops / (ms_max / 1e3) / 1e12) / peak,
             "step_frac_8HV_vs_burst": (step_flops / (ms_max / 1e3) / 1e12) / float(peaks.get("bf16_tflops", peak)),
+            "step_frac_6HV": (0.75 * step_flops / (ms_max / 1e3) / 1e12) / peak,
             "bwd_rows": bwd_rows,
             "step_frac_executed": (sum(step_kflops.values()) / (ms_max / 1e3) / 1e12) / peak}
 
@@ -463,6 +487,14 @@ def main_ours(args):
                                 if vocab_par else
                                 ["dW fp32 all-reduce " + ("fused in K6 epilogue (NVLS multimem)"
                                                           if args.collective == "nvls" else "(NCCL)")]))}
+        if world > 1:
+            # the step's exchange and its NVLink roofline (900 GB/s per direction): NVLS moves
+            # about 1x the buffer per GPU and direction, a ring all-reduce 2(N-1)/N x
+            nb = (T * H * 4) if vocab_par else (V_local * H * 4)
+            per_dir = nb if args.collective == "nvls" else 2 * (world - 1) / world * nb
+            cfg["collective"] = {"op": ("dH" if vocab_par else "dW") + " fp32 all-reduce",
+                                 "buffer_bytes": nb, "bytes_per_gpu_per_direction": per_dir,
+                                 "nvlink_roofline_ms": per_dir / 900e9 * 1e3}
         out = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
                "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,
                "scaling": "strong" if vocab_par else "weak", "vs_baseline": None, "dtype": "bf16",

@@ -498,7 +498,7 @@ rl_status forward_impl(const rl_lm_shape* s, const uint16_t* hidden, const uint1
   ep.partials = parts;
   g_sync_ctr = reinterpret_cast<uint32_t*>(ws + L.sync);
   RL_TRY((launch_gemm<rl::EPI_LSE, false, false>(RL_K_FWD_GEMM, ta, tb, ta, T, s->V_local, s->H, group_m_for(RL_K_FWD_GEMM, 16), ep, sms, st)));
-  const int blocks = static_cast<int>((T + 63) / 64);
+  const int blocks = static_cast<int>((T + rl::MERGE_ROWS - 1) / rl::MERGE_ROWS);
   {
     ProfScope ps(RL_K_MERGE, st);
     rl::merge_partials_kernel<<<blocks, 256, 0, st>>>(parts, static_cast<int>(L.n_tiles_v), T, logprob, entropy,
@@ -602,7 +602,7 @@ rl_status bwd_sparse_impl(const rl_lm_shape* s, const uint16_t* hidden, const ui
     RL_CHECK_LAUNCH();
     {
       ProfScope ps(RL_K_COMPACT, st);
-      rl::gather_rows_kernel<<<2 * sms, 256, 0, st>>>(hidden, H, idx, cc + n_chunks, 256, (T + 255) / 256 * 256 + 256,
+      rl::gather_rows_kernel<<<8 * sms, 256, 0, st>>>(hidden, H, idx, cc + n_chunks, 256, (T + 255) / 256 * 256 + 256,
                                                       h_c, coef_c, lse_c, tgt_c);
     }
     RL_CHECK_LAUNCH();
@@ -669,7 +669,7 @@ rl_status bwd_sparse_impl(const rl_lm_shape* s, const uint16_t* hidden, const ui
       }
       {
         ProfScope ps(RL_K_COMPACT, st);
-        rl::scatter_rows_kernel<<<2 * sms, 256, 0, st>>>(dh_c, H * (dh ? 2 : 4), idx + c0, cnt,
+        rl::scatter_rows_kernel<<<8 * sms, 256, 0, st>>>(dh_c, H * (dh ? 2 : 4), idx + c0, cnt,
                                                          dh ? reinterpret_cast<uint8_t*>(dh)
                                                             : reinterpret_cast<uint8_t*>(dh32));
       }
@@ -1058,7 +1058,7 @@ rl_status rl_merge_partials(const float* partials, int32_t n_parts, int64_t T, f
   if (!aligned16(partials)) return fail(RL_ERR_ALIGNMENT, "partials must be 16-byte aligned");
   DevInfo d;
   RL_TRY(device_info(d));
-  const int blocks = static_cast<int>((T + 63) / 64);
+  const int blocks = static_cast<int>((T + rl::MERGE_ROWS - 1) / rl::MERGE_ROWS);
   {
     ProfScope ps(RL_K_MERGE, static_cast<cudaStream_t>(stream));
     rl::merge_partials_kernel<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(

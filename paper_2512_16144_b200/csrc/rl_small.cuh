@@ -50,24 +50,37 @@ __device__ __forceinline__ Part merge2(Part a, Part b) {
   return r;
 }
 
-__global__ void merge_partials_kernel(const float4* __restrict__ parts, int n_parts, int64_t T,
-                                      float* __restrict__ logprob, float* __restrict__ entropy,
-                                      float* __restrict__ lse, float4* __restrict__ merged) {
-  __shared__ Part sh[4][64];
-  const int r = threadIdx.x & 63;
-  const int slice = threadIdx.x >> 6;
-  const int64_t row = static_cast<int64_t>(blockIdx.x) * 64 + r;
+// 32 rows x 8 vocab-tile slices per block (each warp reads 32 consecutive float4 of
+// one tile: coalesced); 4 partial loads in flight per thread; slices combined by a
+// fixed-order tree, so the merge order (and the result) does not depend on timing.
+constexpr int MERGE_ROWS = 32, MERGE_SLICES = 8;
+__global__ void __launch_bounds__(MERGE_ROWS * MERGE_SLICES)
+    merge_partials_kernel(const float4* __restrict__ parts, int n_parts, int64_t T, float* __restrict__ logprob,
+                          float* __restrict__ entropy, float* __restrict__ lse, float4* __restrict__ merged) {
+  __shared__ Part sh[MERGE_SLICES][MERGE_ROWS];
+  const int r = threadIdx.x % MERGE_ROWS;
+  const int slice = threadIdx.x / MERGE_ROWS;
+  const int64_t row = static_cast<int64_t>(blockIdx.x) * MERGE_ROWS + r;
   Part acc = {-1e30f, 0.f, 0.f, -INFINITY};
   if (row < T) {
-    for (int p = slice; p < n_parts; p += 4) {
-      const float4 v = parts[static_cast<int64_t>(p) * T + row];
+    int p = slice;
+    for (; p + 3 * MERGE_SLICES < n_parts; p += 4 * MERGE_SLICES) {
+      float4 v[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) v[k] = __ldg(parts + static_cast<int64_t>(p + k * MERGE_SLICES) * T + row);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) acc = merge2(acc, Part{v[k].x, v[k].y, v[k].z, v[k].w});
+    }
+    for (; p < n_parts; p += MERGE_SLICES) {
+      const float4 v = __ldg(parts + static_cast<int64_t>(p) * T + row);
       acc = merge2(acc, Part{v.x, v.y, v.z, v.w});
     }
   }
   sh[slice][r] = acc;
   __syncthreads();
   if (slice == 0 && row < T) {
-    Part a = merge2(merge2(sh[0][r], sh[1][r]), merge2(sh[2][r], sh[3][r]));
+    Part a = merge2(merge2(merge2(sh[0][r], sh[1][r]), merge2(sh[2][r], sh[3][r])),
+                    merge2(merge2(sh[4][r], sh[5][r]), merge2(sh[6][r], sh[7][r])));
     if (merged != nullptr) {
       merged[row] = make_float4(a.m, a.s, a.u, a.zt);
     } else {
@@ -364,38 +377,69 @@ __global__ void compact_write_kernel(const float* __restrict__ coef, const float
 // h_c[r] = hidden[idx[r]] for r < count; the `pad` rows after them (up to `cap`) are
 // zeroed together with their coef/lse/target, so a tail tile of any chunk (which
 // reads at most 255 rows past the chunk's last compact row) contributes exact zeros.
+// Flat over (row, 16-byte vector), 4 loads in flight per thread before the stores.
 __global__ void gather_rows_kernel(const uint16_t* __restrict__ hidden, int64_t H, const int32_t* __restrict__ idx,
                                    const int* __restrict__ count_ptr, int pad, int64_t cap, uint16_t* __restrict__ h_c,
                                    float* __restrict__ coef_c, float* __restrict__ lse_c, int32_t* __restrict__ tgt_c) {
   const int count = *count_ptr;
   const int64_t padded = (static_cast<int64_t>(count) + pad < cap) ? static_cast<int64_t>(count) + pad : cap;
   const int64_t vecs = H / 8;  // 16-byte vectors per row (H % 8 == 0)
-  for (int64_t r = blockIdx.x; r < padded; r += gridDim.x) {
-    uint4* dst = reinterpret_cast<uint4*>(h_c + r * H);
-    if (r < count) {
-      const uint4* src = reinterpret_cast<const uint4*>(hidden + static_cast<int64_t>(idx[r]) * H);
-      for (int64_t v = threadIdx.x; v < vecs; v += blockDim.x) dst[v] = src[v];
-    } else {
-      for (int64_t v = threadIdx.x; v < vecs; v += blockDim.x) dst[v] = make_uint4(0, 0, 0, 0);
-      if (threadIdx.x == 0) {
-        coef_c[r] = 0.f;
-        lse_c[r] = 0.f;
-        tgt_c[r] = -1;
+  const int64_t n = padded * vecs;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  const uint4* src = reinterpret_cast<const uint4*>(hidden);
+  uint4* dst = reinterpret_cast<uint4*>(h_c);
+  for (int64_t i0 = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i0 < n; i0 += 4 * stride) {
+    uint4 v[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int64_t i = i0 + k * stride;
+      v[k] = make_uint4(0, 0, 0, 0);
+      if (i < n) {
+        const int64_t r = i / vecs;
+        if (r < count) v[k] = __ldg(src + static_cast<int64_t>(idx[r]) * vecs + (i - r * vecs));
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int64_t i = i0 + k * stride;
+      if (i < n) {
+        dst[i] = v[k];
+        const int64_t r = i / vecs;
+        if (r >= count && i == r * vecs) {
+          coef_c[r] = 0.f;
+          lse_c[r] = 0.f;
+          tgt_c[r] = -1;
+        }
       }
     }
   }
 }
 
-// dh[idx[r]] = dh_c[r] for r < count (dh pre-zeroed); elem bytes = 2 (bf16) or 4 (f32).
+// dh[idx[r]] = dh_c[r] for r < count (dh pre-zeroed); row_bytes % 16 == 0.
 __global__ void scatter_rows_kernel(const uint8_t* __restrict__ dh_c, int64_t row_bytes,
                                     const int32_t* __restrict__ idx, const int* __restrict__ count_ptr,
                                     uint8_t* __restrict__ dh) {
   const int count = *count_ptr;
   const int64_t vecs = row_bytes / 16;
-  for (int64_t r = blockIdx.x; r < count; r += gridDim.x) {
-    const uint4* src = reinterpret_cast<const uint4*>(dh_c + r * row_bytes);
-    uint4* dst = reinterpret_cast<uint4*>(dh + static_cast<int64_t>(idx[r]) * row_bytes);
-    for (int64_t v = threadIdx.x; v < vecs; v += blockDim.x) dst[v] = src[v];
+  const int64_t n = static_cast<int64_t>(count) * vecs;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  const uint4* src = reinterpret_cast<const uint4*>(dh_c);
+  uint4* dst = reinterpret_cast<uint4*>(dh);
+  for (int64_t i0 = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i0 < n; i0 += 4 * stride) {
+    uint4 v[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int64_t i = i0 + k * stride;
+      if (i < n) v[k] = __ldg(src + i);
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int64_t i = i0 + k * stride;
+      if (i < n) {
+        const int64_t r = i / vecs;
+        dst[static_cast<int64_t>(idx[r]) * vecs + (i - r * vecs)] = v[k];
+      }
+    }
   }
 }
 
