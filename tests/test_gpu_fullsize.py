@@ -217,3 +217,81 @@ def test_glm64k_vocab_parallel_emulated_sampled_rows():
     assert harness.rel_fro(dh.cpu().numpy()[rows].astype(np.float64), ref.d_hidden) <= harness.GRAD_RTOL
     dw_all = torch.cat(dws).cpu().numpy().astype(np.float64)
     assert harness.rel_fro(dw_all, ref.d_w_vocab) <= harness.GRAD_RTOL
+
+
+def test_stress_full_size_sparse_backward():
+    """BASELINE 'stress' per rank (T = 16384, one G = 16 group, delta sigma 1.0,
+    spikes 1e-4): every row is a loss row and ~43% of them are masked, so the
+    sparse backward compacts thousands of rows over many tiles. The inference
+    log-probs of all rows are the engine's own log-probs plus the stress noise.
+    Checks: sampled rows' logprob/entropy vs the fp64 oracle; every coefficient
+    equals the paper's gate recomputed on the host from the returned log-probs
+    (Eq.2 closed interval, strict guard, A_i / D); dH of the sparse path is
+    bitwise the dense path's and dW agrees to fp32 summation order; the masked
+    rows' dH is exactly zero; sum_v dW[v, :] ~ 0."""
+    wl = synth.Workload("stress-rank", 1, 16, 1024, 4096, 151552, delta_sigma=1.0, spike_rate=1e-4)
+    b = synth.make_batch(wl, 7)
+    T, H, V = b.T, b.H, b.V
+    dev = "cuda"
+    bf = lambda x: torch.from_numpy(x.view(np.int16).copy()).view(torch.bfloat16).to(dev)  # noqa: E731
+    hidden, w = bf(b.hidden), bf(b.w_vocab)
+    targets = torch.from_numpy(b.targets).to(dev)
+    shape = rl.make_shape(T, H, V)
+    lp0 = torch.empty(T, device=dev)
+    rl.rl_logprob_fwd(shape, hidden, w, targets, lp0)
+    infer = synth.compose_infer_logprobs(lp0.cpu().numpy().astype(np.float64), b.delta_noise, b.spikes)
+    adv = oracle.group_advantages(b.rewards).reshape(-1).astype(np.float32)
+    D = float(T)
+    params = rl.make_params(len(adv), D)
+    off = b.rollout_offsets
+    f32 = dict(dtype=torch.float32, device=dev)
+    res = {}
+    for dense in (False, True):
+        out = dict(logprob=torch.empty(T, **f32), entropy=torch.empty(T, **f32), coef=torch.empty(T, **f32),
+                   keep=torch.empty(T, dtype=torch.uint8, device=dev),
+                   guarded=torch.empty(len(adv), dtype=torch.uint8, device=dev))
+        report = rl.new_report(dev)
+        dh = torch.empty(T, H, dtype=torch.bfloat16, device=dev)
+        dw = torch.empty(V, H, **f32)
+        rl.rl_policy_loss_fwd_bwd(shape, params, hidden, w, targets, torch.from_numpy(infer).to(dev),
+                                  torch.from_numpy(adv).to(dev), torch.from_numpy(off).to(dev), None,
+                                  report=report, logprob=out["logprob"], entropy=out["entropy"], coef=out["coef"],
+                                  token_keep=out["keep"], rollout_guarded=out["guarded"], d_hidden=dh, d_w_vocab=dw,
+                                  dense_backward=dense)
+        torch.cuda.synchronize()
+        res[dense] = ({k: v.cpu().numpy() for k, v in out.items()}, dh.view(torch.int16).cpu().numpy(),
+                      dw.cpu().numpy(), rl.read_report(report, check=True))
+    g, dh_s, dw_s, rep = res[False]
+    _, dh_d, dw_d, _ = res[True]
+
+    # sampled rows vs the fp64 oracle
+    rows = _sample_rows(b, 512, 1)
+    h64 = oracle.bf16_to_f64(b.hidden[rows])
+    lp_ref, ent_ref, _ = oracle.log_softmax_stats(oracle.lm_logits(h64, oracle.bf16_to_f64(b.w_vocab)),
+                                                   b.targets[rows])
+    assert np.max(np.abs(g["logprob"][rows] - lp_ref)) <= harness.LOGP_TOL
+    assert np.max(np.abs(g["entropy"][rows] - ent_ref)) <= harness.LOGP_TOL
+
+    # the gate, recomputed from the returned log-probs (float64 on the host)
+    k = np.exp(g["logprob"].astype(np.float64) - infer.astype(np.float64))
+    rollout_of = np.repeat(np.arange(len(adv)), np.diff(off))
+    kmin = np.full(len(adv), np.inf)
+    np.minimum.at(kmin, rollout_of, k)
+    guarded = kmin < synth.GUARD
+    keep = (k >= synth.ALPHA) & (k <= synth.BETA) & ~guarded[rollout_of]
+    near = (np.abs(k - synth.ALPHA) <= harness.BAND) | (np.abs(k - synth.BETA) <= harness.BAND)
+    assert np.all(near[g["keep"].astype(bool) != keep])
+    assert g["guarded"].astype(bool).tolist() == guarded.tolist()
+    both = keep & g["keep"].astype(bool)
+    coef_ref = k * adv[rollout_of] / D
+    assert np.allclose(g["coef"][both], coef_ref[both], rtol=1e-4, atol=0)
+    assert rep.masked_low + rep.masked_high > 0.2 * T       # heavy masking is exercised
+    kept = g["coef"] != 0
+    assert 0.3 * T < kept.sum() < 0.9 * T
+
+    # sparse == dense backward; masked rows carry zero dH
+    assert np.array_equal(dh_s, dh_d)
+    assert not dh_s[~kept].any()
+    assert harness.rel_fro(dw_s, dw_d) <= 1e-5
+    col = np.linalg.norm(dw_s.astype(np.float64).sum(0)) / np.linalg.norm(dw_s.astype(np.float64))
+    assert col < 1e-2
