@@ -473,6 +473,38 @@ def main_ours(args):
         h2d = T * H * 2 + T * 4 + T * 4 + R * 4 + (R + 1) * 4 + T
         e2e = {"value": T * world / el, "unit": "tokens/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 48,
                "ms_per_step": el * 1e3, "api": "rl_policy_loss_fwd_bwd_hostio"}
+    elif vocab_par and not args.no_e2e:
+        # vocab-parallel end to end: every rank uploads the (replicated) step inputs from
+        # pinned host memory, runs the split-phase engine and reads the report back
+        pins = {"hidden": b["hidden"].cpu().pin_memory(), "targets": targets.cpu().pin_memory(),
+                "infer": infer.cpu().pin_memory(), "rewards": rewards.cpu().pin_memory(),
+                "offsets": offsets.cpu().pin_memory(), "loss_mask": loss_mask.cpu().pin_memory()}
+        devs = {k: torch.empty_like(v, device=dev) for k, v in pins.items()}
+        rep_h = torch.empty(48, dtype=torch.uint8).pin_memory()
+
+        def hstep():
+            for k, v in pins.items():
+                devs[k].copy_(v, non_blocking=True)
+            engine.step(devs["hidden"], w_loc, devs["targets"], devs["infer"], devs["rewards"], devs["offsets"],
+                        devs["loss_mask"], dw)
+            rep_h.copy_(engine.report, non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+
+        for _ in range(max(1, args.warmup)):
+            hstep()
+        dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            hstep()
+        torch.cuda.synchronize()
+        el = (time.perf_counter() - t0) / args.steps
+        t = torch.tensor([el], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        el = float(t.item())
+        e2e = {"value": T / el, "unit": "tokens/s",
+               "h2d_bytes_per_step": int(sum(v.numel() * v.element_size() for v in pins.values())),
+               "d2h_bytes_per_step": 48, "ms_per_step": el * 1e3,
+               "api": "parallel.VocabParallelPolicyLoss.step (host inputs, per rank)"}
 
     out = None
     if rank == 0:
