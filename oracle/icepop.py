@@ -49,18 +49,21 @@ def group_advantages(S: np.ndarray) -> np.ndarray:
 
 
 # ------------------------------------------------------------ LM head + softmax
-def lm_logits(hidden: np.ndarray, w_vocab: np.ndarray, inv_temperature: float = 1.0,
+def lm_logits(hidden: np.ndarray, w_vocab: np.ndarray, inv_temperature=1.0,
               vocab_block: int = 16384) -> np.ndarray:
-    """z[t, v] = invT * sum_h hidden[t, h] * W[v, h]  (pi_train's logits in Eq.1;
-    reading R8 for the temperature). Inputs are fp64 (exact bf16 values).
-    Columns are computed a vocab block at a time only to bound memory; every
-    entry is the same single dot product either way."""
+    """z[t, v] = invT_t * sum_h hidden[t, h] * W[v, h]  (pi_train's logits in Eq.1;
+    reading R8 for the temperature, R20 for a per-token invT_t: a scalar or a [T]
+    array). Inputs are fp64 (exact bf16 values). Columns are computed a vocab
+    block at a time only to bound memory; every entry is the same single dot
+    product either way."""
     T, V = hidden.shape[0], w_vocab.shape[0]
     Z = np.empty((T, V), dtype=np.float64)
     for v0 in range(0, V, vocab_block):
         v1 = min(V, v0 + vocab_block)
         Z[:, v0:v1] = hidden @ w_vocab[v0:v1].T
-    if inv_temperature != 1.0:
+    if np.ndim(inv_temperature) == 1:
+        Z *= np.asarray(inv_temperature, dtype=np.float64)[:, None]
+    elif inv_temperature != 1.0:
         Z *= inv_temperature
     return Z
 
@@ -264,6 +267,29 @@ def variant_loss(variant, *args, **kw) -> LossReport:
     return fn(*args, **kw)
 
 
+KL_SETS = {"masked": 0, "unmasked": 1, "all": 2}
+
+
+def add_kl_term(rep: LossReport, logp, infer_logprobs, kl_tau: float, kl_set: str,
+                loss_denominator: float) -> LossReport:
+    """Reading R19 (not in Eq.1, default kl_tau = 0): the trainer's
+    KL term on the token log-ratio,
+
+      loss += (kl_tau / D) * sum_{t in S} log k_t,   log k_t = logp_t - infer_t,
+      S = valid & ~keep ("masked"), keep ("unmasked") or valid ("all"),
+
+    with S fixed by the gate (no gradient through it). d loss / d logp_t gains
+    kl_tau / D on S, so coef_t (d loss / d logp_t = -coef_t) loses kl_tau / D."""
+    if kl_tau == 0.0:
+        return rep
+    logp = np.asarray(logp, dtype=np.float64)
+    infer = np.asarray(infer_logprobs, dtype=np.float64)
+    S = {"masked": rep.valid & ~rep.keep, "unmasked": rep.keep, "all": rep.valid}[kl_set]
+    logk = np.where(S, logp - np.where(S, infer, 0.0), 0.0)
+    w = kl_tau / loss_denominator
+    return dataclasses.replace(rep, loss=float(rep.loss + w * logk.sum()), coef=rep.coef - np.where(S, w, 0.0))
+
+
 # ------------------------------------------------------------------- backward
 def icepop_backward(Z: np.ndarray, lse: np.ndarray, targets: np.ndarray, coef: np.ndarray,
                     hidden: np.ndarray, w_vocab: np.ndarray, inv_temperature: float = 1.0):
@@ -276,7 +302,7 @@ def icepop_backward(Z: np.ndarray, lse: np.ndarray, targets: np.ndarray, coef: n
     Returns (dZ, dH, dW) in fp64."""
     P = np.exp(Z - lse[:, None])
     P[np.arange(Z.shape[0]), targets] -= 1.0
-    dZ = (coef * inv_temperature)[:, None] * P
+    dZ = (coef * np.asarray(inv_temperature, dtype=np.float64))[:, None] * P
     return dZ, dZ @ w_vocab, dZ.T @ hidden
 
 
@@ -295,7 +321,7 @@ class StepResult:
 def policy_loss_fwd_bwd(hidden, w_vocab, targets, infer_logprobs, rewards, offsets,
                         loss_mask=None, *, alpha=0.5, beta=5.0, guard_threshold=1e-5,
                         loss_denominator=None, inv_temperature=1.0, backward=True,
-                        rollout_adv=None, variant="icepop") -> StepResult:
+                        rollout_adv=None, variant="icepop", kl_tau=0.0, kl_set="masked") -> StepResult:
     """The whole north-star step on one rank: S0 (advantages), S1-S2 (logits,
     log-softmax stats), S3 (Eq.1/Eq.2/guard), S4-S6 (backward). `hidden` and
     `w_vocab` are fp64 arrays (use bf16_to_f64 on bit patterns); `rewards` is
@@ -310,6 +336,7 @@ def policy_loss_fwd_bwd(hidden, w_vocab, targets, infer_logprobs, rewards, offse
     logp, ent, lse = log_softmax_stats(Z, safe_t)
     rep = variant_loss(variant, logp, infer_logprobs, A, offsets, lm, alpha, beta, guard_threshold,
                        D, targets=targets, vocab=V)
+    rep = add_kl_term(rep, logp, infer_logprobs, kl_tau, kl_set, D)
     dH = dW = None
     if backward:
         _, dH, dW = icepop_backward(Z, lse, safe_t, rep.coef, hidden, w_vocab, inv_temperature)
