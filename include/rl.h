@@ -49,7 +49,7 @@
 extern "C" {
 #endif
 
-#define RL_ABI_VERSION 1
+#define RL_ABI_VERSION 2
 
 typedef enum rl_status {
   RL_OK = 0,
@@ -70,6 +70,9 @@ typedef struct rl_lm_shape {
   int64_t V_global;        /* full vocabulary size (>= vocab_offset + V_local)       */
   float inv_temperature;   /* 1/tau applied to the logits, > 0 (R8; default 1)       */
   int32_t _pad;
+  const float* inv_temperature_rows; /* optional DEVICE [T] per-token 1/tau (> 0, finite;
+                              reading R20), overriding inv_temperature; NULL = scalar.
+                              Row t of every call's T rows (vocab shards share it).     */
 } rl_lm_shape;
 
 /* Loss variants. All share the backward: each only changes
@@ -90,8 +93,15 @@ typedef struct rl_loss_params {
   int32_t num_rollouts;    /* R = number of packed rollouts on this rank (>= 1)          */
   double loss_denominator; /* D = sum_i |y_i| over the GLOBAL step batch, > 0 (R5)        */
   int32_t variant;         /* rl_loss_variant; 0 = the paper's IcePop objective           */
+  int32_t kl_set;          /* rl_kl_set: the tokens the KL term covers                    */
+  float kl_tau;            /* KL term weight (reading R19): loss += (kl_tau/D) sum_{t in S}
+                              log k_t, coef_t -= kl_tau/D on S; 0 = off (the paper)         */
   int32_t _pad;
 } rl_loss_params;
+
+/* Token set S of the KL term (reading R19): Eq.2/guard-masked valid tokens, kept
+ * tokens, or every valid loss token. */
+typedef enum rl_kl_set { RL_KL_MASKED = 0, RL_KL_UNMASKED = 1, RL_KL_ALL = 2 } rl_kl_set;
 
 /* Device-resident loss report (SPEC LossReport + counters). Written, not
  * accumulated, by every call that takes it. Sums use a fixed-order reduction,

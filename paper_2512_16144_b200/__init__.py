@@ -33,16 +33,19 @@ class RLError(RuntimeError):
 class rl_lm_shape(ctypes.Structure):
     _fields_ = [("T", ctypes.c_int64), ("H", ctypes.c_int64), ("V_local", ctypes.c_int64),
                 ("vocab_offset", ctypes.c_int64), ("V_global", ctypes.c_int64),
-                ("inv_temperature", ctypes.c_float), ("_pad", ctypes.c_int32)]
+                ("inv_temperature", ctypes.c_float), ("_pad", ctypes.c_int32),
+                ("inv_temperature_rows", ctypes.c_void_p)]
 
 
 class rl_loss_params(ctypes.Structure):
     _fields_ = [("alpha", ctypes.c_float), ("beta", ctypes.c_float), ("guard_threshold", ctypes.c_float),
                 ("num_rollouts", ctypes.c_int32), ("loss_denominator", ctypes.c_double),
-                ("variant", ctypes.c_int32), ("_pad", ctypes.c_int32)]
+                ("variant", ctypes.c_int32), ("kl_set", ctypes.c_int32), ("kl_tau", ctypes.c_float),
+                ("_pad", ctypes.c_int32)]
 
 
 LOSS_VARIANTS = {"icepop": 0, "cispo": 1, "gspo": 2}   # rl_loss_variant
+KL_SETS = {"masked": 0, "unmasked": 1, "all": 2}        # rl_kl_set
 
 
 class rl_loss_report(ctypes.Structure):
@@ -169,16 +172,25 @@ def _stream(stream=None):
     return ctypes.c_void_p(s.cuda_stream)
 
 
-def make_shape(T, H, V_local, vocab_offset=0, V_global=None, inv_temperature=1.0) -> rl_lm_shape:
+def make_shape(T, H, V_local, vocab_offset=0, V_global=None, inv_temperature=1.0,
+               inv_temperature_rows=None) -> rl_lm_shape:
+    """`inv_temperature_rows`: optional fp32 CUDA tensor [T] of per-token 1/tau (R20);
+    the caller keeps it alive while the shape is in use."""
+    if inv_temperature_rows is not None:
+        if not inv_temperature_rows.is_cuda or inv_temperature_rows.dtype != torch.float32 \
+                or inv_temperature_rows.numel() < int(T) or not inv_temperature_rows.is_contiguous():
+            raise RLError(1, "inv_temperature_rows must be a contiguous fp32 CUDA tensor with >= T elements")
     return rl_lm_shape(int(T), int(H), int(V_local), int(vocab_offset),
-                       int(V_local + vocab_offset if V_global is None else V_global), float(inv_temperature), 0)
+                       int(V_local + vocab_offset if V_global is None else V_global), float(inv_temperature), 0,
+                       inv_temperature_rows.data_ptr() if inv_temperature_rows is not None else None)
 
 
 def make_params(num_rollouts, loss_denominator, alpha=ALPHA, beta=BETA, guard_threshold=GUARD,
-                variant="icepop") -> rl_loss_params:
+                variant="icepop", kl_tau=0.0, kl_set="masked") -> rl_loss_params:
     v = LOSS_VARIANTS[variant] if isinstance(variant, str) else int(variant)
+    ks = KL_SETS[kl_set] if isinstance(kl_set, str) else int(kl_set)
     return rl_loss_params(float(alpha), float(beta), float(guard_threshold), int(num_rollouts),
-                          float(loss_denominator), v, 0)
+                          float(loss_denominator), v, ks, float(kl_tau), 0)
 
 
 def _bf16(t: torch.Tensor | None, name: str) -> torch.Tensor | None:

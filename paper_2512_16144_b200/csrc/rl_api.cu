@@ -407,7 +407,7 @@ struct WsLayout {
   size_t partials, lse, coef, rp, sync, dz, end;
   // sparse backward (rows with coef != 0): compact index, per-row vectors, counts,
   // gathered hidden rows and one chunk of compact dH
-  size_t idx, coef_c, lse_c, tgt_c, blk_counts, chunk_counts, h_c, dh_c;
+  size_t idx, coef_c, lse_c, tgt_c, invt_c, blk_counts, chunk_counts, h_c, dh_c;
   int64_t n_tiles_v, ldz, chunk;
 };
 
@@ -431,6 +431,7 @@ WsLayout ws_layout(const rl_lm_shape* s, int32_t R, int64_t chunk_rows) {
   w.coef_c = c.take(static_cast<size_t>(Tp) * 4);
   w.lse_c = c.take(static_cast<size_t>(Tp) * 4);
   w.tgt_c = c.take(static_cast<size_t>(Tp) * 4);
+  w.invt_c = c.take(static_cast<size_t>(Tp) * 4);
   w.blk_counts = c.take(static_cast<size_t>((T + rl::COMPACT_ROWS - 1) / rl::COMPACT_ROWS + 1) * 4);
   w.chunk_counts = c.take(static_cast<size_t>((T + (w.chunk > 0 ? w.chunk : 1) - 1) / (w.chunk > 0 ? w.chunk : 1) + 2) * 4);
   w.h_c = c.take(static_cast<size_t>(Tp) * s->H * 2);
@@ -451,8 +452,14 @@ rl_status check_shape(const rl_lm_shape* s) {
                 (long long)s->V_local, (long long)s->V_global);
   if (!(s->inv_temperature > 0.f) || !isfinite(s->inv_temperature))
     return fail(RL_ERR_INVALID_ARGUMENT, "inv_temperature must be finite and > 0");
+  if (s->inv_temperature_rows && (reinterpret_cast<uintptr_t>(s->inv_temperature_rows) & 3u))
+    return fail(RL_ERR_ALIGNMENT, "inv_temperature_rows must be 4-byte aligned");
   return RL_OK;
 }
+
+static_assert(sizeof(rl_lm_shape) == 56, "rl_lm_shape layout (binding mirrors it)");
+static_assert(sizeof(rl_loss_params) == 40, "rl_loss_params layout (binding mirrors it)");
+static_assert(sizeof(rl_loss_report) == 48, "rl_loss_report layout (binding mirrors it)");
 
 rl_status check_params(const rl_loss_params* p) {
   if (!p) return fail(RL_ERR_INVALID_ARGUMENT, "params is NULL");
@@ -465,6 +472,9 @@ rl_status check_params(const rl_loss_params* p) {
   if (p->num_rollouts < 1) return fail(RL_ERR_INVALID_ARGUMENT, "num_rollouts must be >= 1");
   if (p->variant < RL_LOSS_ICEPOP || p->variant > RL_LOSS_GSPO)
     return fail(RL_ERR_INVALID_ARGUMENT, "unknown loss variant %d", p->variant);
+  if (!isfinite(p->kl_tau)) return fail(RL_ERR_INVALID_ARGUMENT, "kl_tau must be finite");
+  if (p->kl_set < RL_KL_MASKED || p->kl_set > RL_KL_ALL)
+    return fail(RL_ERR_INVALID_ARGUMENT, "unknown kl_set %d", p->kl_set);
   return RL_OK;
 }
 
@@ -492,6 +502,7 @@ rl_status forward_impl(const rl_lm_shape* s, const uint16_t* hidden, const uint1
   ep.cols = s->V_local;
   ep.inv_temperature = s->inv_temperature;
   ep.scale_log2 = s->inv_temperature * 1.4426950408889634f;
+  ep.invt_rows = s->inv_temperature_rows;
   ep.targets = targets;
   ep.vocab_offset = s->vocab_offset;
   float4* parts = reinterpret_cast<float4*>(ws + L.partials);
@@ -514,6 +525,8 @@ rl_status loss_impl(const rl_loss_params* p, int64_t T, int64_t V_global, const 
                     cudaStream_t st) {
   rl::LossArgs a;
   a.variant = p->variant;
+  a.kl_set = p->kl_set;
+  a.kl_w = static_cast<double>(p->kl_tau) / p->loss_denominator;
   a.alpha = p->alpha;
   a.beta = p->beta;
   a.guard = p->guard_threshold;
@@ -583,6 +596,7 @@ rl_status bwd_sparse_impl(const rl_lm_shape* s, const uint16_t* hidden, const ui
   float* coef_c = reinterpret_cast<float*>(ws + L.coef_c);
   float* lse_c = reinterpret_cast<float*>(ws + L.lse_c);
   int32_t* tgt_c = reinterpret_cast<int32_t*>(ws + L.tgt_c);
+  float* invt_c = reinterpret_cast<float*>(ws + L.invt_c);
   int* blk = reinterpret_cast<int*>(ws + L.blk_counts);
   int* cc = reinterpret_cast<int*>(ws + L.chunk_counts);  // [n_chunks] per chunk, [n_chunks] total
   uint16_t* h_c = reinterpret_cast<uint16_t*>(ws + L.h_c);
@@ -597,13 +611,14 @@ rl_status bwd_sparse_impl(const rl_lm_shape* s, const uint16_t* hidden, const ui
     {
       ProfScope ps(RL_K_COMPACT, st);
       rl::compact_write_kernel<<<nb, 256, 0, st>>>(coef, lse, targets, T, blk, nb, chunk, idx, coef_c, lse_c, tgt_c,
-                                                   cc, n_chunks);
+                                                   cc, n_chunks, s->inv_temperature_rows, invt_c);
     }
     RL_CHECK_LAUNCH();
     {
       ProfScope ps(RL_K_COMPACT, st);
       rl::gather_rows_kernel<<<8 * sms, 256, 0, st>>>(hidden, H, idx, cc + n_chunks, 256, (T + 255) / 256 * 256 + 256,
-                                                      h_c, coef_c, lse_c, tgt_c);
+                                                      h_c, coef_c, lse_c, tgt_c,
+                                                      s->inv_temperature_rows ? invt_c : nullptr);
     }
     RL_CHECK_LAUNCH();
   }
@@ -632,6 +647,7 @@ rl_status bwd_sparse_impl(const rl_lm_shape* s, const uint16_t* hidden, const ui
       ep.vocab_offset = s->vocab_offset;
       ep.lse = lse_c + c0;
       ep.coef = coef_c + c0;
+      ep.invt_rows = s->inv_temperature_rows ? invt_c + c0 : nullptr;
       RL_TRY((launch_gemm<rl::EPI_DZ, false, false>(RL_K_DZ_GEMM, t_h_k, t_w_k, t_dz_st, rows, V, H,
                                                     group_m_for(RL_K_DZ_GEMM, 16), ep, sms, st, 1, 0, cnt, 1)));
     }
@@ -715,6 +731,7 @@ rl_status bwd_impl(const rl_lm_shape* s, const uint16_t* hidden, const uint16_t*
     ep.vocab_offset = s->vocab_offset;
     ep.lse = lse + c0;
     ep.coef = coef + c0;
+    ep.invt_rows = s->inv_temperature_rows ? s->inv_temperature_rows + c0 : nullptr;
     if (phases & RL_BWD_DU)
       RL_TRY((launch_gemm<rl::EPI_DZ, false, false>(RL_K_DZ_GEMM, t_h_k, t_w_k, t_dz_st, rows, V, H, group_m_for(RL_K_DZ_GEMM, 16), ep, sms, st)));
     // K6: dW (+)= dU^T h
@@ -1158,6 +1175,7 @@ static rl_status step_impl(const rl_lm_shape* shape, const rl_loss_params* param
     for (int64_t r0 = 0; r0 < shape->T; r0 = slab_ends[j], ++j) {
       rl_lm_shape sub = *shape;
       sub.T = slab_ends[j] - r0;
+      if (shape->inv_temperature_rows) sub.inv_temperature_rows = shape->inv_temperature_rows + r0;
       RL_CUDA(cudaStreamWaitEvent(st, slab_events[j], 0));
       RL_TRY(forward_impl(&sub, hidden + r0 * shape->H, w_vocab, targets + r0, out->logprob + r0,
                           out->entropy ? out->entropy + r0 : nullptr, lse + r0, nullptr, ws, L, sms, st));

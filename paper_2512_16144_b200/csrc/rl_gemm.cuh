@@ -95,6 +95,7 @@ struct EpiParams {
   float4* partials;        // EPI_LSE: [n_blocks][rows]
   const float* lse;        // EPI_DZ:  [rows]
   const float* coef;       // EPI_DZ:  [rows]
+  const float* invt_rows;  // EPI_LSE / EPI_DZ: optional per-row 1/tau (R20), else inv_temperature
   // soft k-barrier (locality): producers of all CTAs arrive on sync_ctr[p] every
   // sync_every k-blocks and do not run more than sync_slack points ahead of the
   // slowest CTA, so CTAs sharing operands stay inside one L2 window. 0 = off.
@@ -584,6 +585,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           const int64_t nv64 = ep.cols - n0;
           const int nvalid = nv64 < BN ? static_cast<int>(nv64) : BN;
           float mrun = -1e30f, srun = 0.f, trun = 0.f, zt = -INFINITY;
+          const float it = (ep.invt_rows != nullptr && row_ok) ? ep.invt_rows[row] : ep.inv_temperature;
+          const float sl2 = ep.invt_rows != nullptr ? it * 1.4426950408889634f : ep.scale_log2;
   #pragma unroll 1
           for (int c = 0; c < BN / 32; ++c) {
             uint32_t r[32];
@@ -592,7 +595,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             if (c == BN / 32 - 1) release_tmem(bi);
             float u[32];
   #pragma unroll
-            for (int j = 0; j < 32; ++j) u[j] = __uint_as_float(r[j]) * ep.scale_log2;
+            for (int j = 0; j < 32; ++j) u[j] = __uint_as_float(r[j]) * sl2;
             if (nvalid < BN) {
   #pragma unroll
               for (int j = 0; j < 32; ++j)
@@ -603,7 +606,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
               float z = -INFINITY;
   #pragma unroll
               for (int j = 0; j < 32; ++j) z = fmaxf(z, (j == jt) ? __uint_as_float(r[j]) : -INFINITY);
-              zt = z * ep.inv_temperature;
+              zt = z * it;
             }
             float cm = u[0];
   #pragma unroll
@@ -650,12 +653,14 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           }
         } else {
           // store epilogues: TMEM -> regs -> (math) -> swizzled smem -> TMA store
-          float g = 0.f, b2 = 0.f;
+          float g = 0.f, b2 = 0.f, sl2 = ep.scale_log2;
           int tl = -1;
           const float rs = (GROUPED && ep.row_scale && row_ok) ? ep.row_scale[row] : 1.f;
           if constexpr (MODE == EPI_DZ) {
             if (row_ok) {
-              g = ep.coef[row] * ep.inv_temperature;
+              const float it = ep.invt_rows != nullptr ? ep.invt_rows[row] : ep.inv_temperature;
+              if (ep.invt_rows != nullptr) sl2 = it * 1.4426950408889634f;
+              g = ep.coef[row] * it;
               b2 = ep.lse[row] * 1.4426950408889634f;
               const int64_t yl = static_cast<int64_t>(ep.targets[row]) - ep.vocab_offset;
               const int64_t t64 = yl - n0;
@@ -685,10 +690,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                 float v0 = __uint_as_float(r0[2 * j]), v1 = __uint_as_float(r0[2 * j + 1]);
                 float v2 = __uint_as_float(r1[2 * j]), v3 = __uint_as_float(r1[2 * j + 1]);
                 if constexpr (MODE == EPI_DZ) {
-                  v0 = g * ex2f(fmaf(v0, ep.scale_log2, -b2));
-                  v1 = g * ex2f(fmaf(v1, ep.scale_log2, -b2));
-                  v2 = g * ex2f(fmaf(v2, ep.scale_log2, -b2));
-                  v3 = g * ex2f(fmaf(v3, ep.scale_log2, -b2));
+                  v0 = g * ex2f(fmaf(v0, sl2, -b2));
+                  v1 = g * ex2f(fmaf(v1, sl2, -b2));
+                  v2 = g * ex2f(fmaf(v2, sl2, -b2));
+                  v3 = g * ex2f(fmaf(v3, sl2, -b2));
                   const int cb = c * 64;
                   if (tl == cb + 2 * j) v0 -= g;
                   if (tl == cb + 2 * j + 1) v1 -= g;

@@ -116,6 +116,8 @@ __device__ __forceinline__ T block_reduce_sum(T v, T* sh) {
 
 struct LossArgs {
   int variant;  // rl_loss_variant
+  int kl_set;   // rl_kl_set
+  double kl_w;  // kl_tau / D (reading R19); 0 = no KL term
   float alpha, beta, guard;
   double inv_D;
   int R;
@@ -214,7 +216,7 @@ __global__ void __launch_bounds__(256) loss_coef_kernel(const LossArgs a) {
   }
 
   // pass 2: gate, coefficient, counters
-  double loss = 0.0, kl = 0.0;
+  double loss = 0.0, kl = 0.0, klterm = 0.0;
   uint32_t kept = 0, low = 0, high = 0, gtok = 0, nonfin = 0, badtgt = 0;
   for (int64_t t = t0 + threadIdx.x; t < t1; t += blockDim.x) {
     const bool lm = a.loss_mask ? (a.loss_mask[t] != 0) : true;
@@ -259,6 +261,14 @@ __global__ void __launch_bounds__(256) loss_coef_kernel(const LossArgs a) {
         c = gspo_w;
       }
       kept += kp;
+      if (a.kl_w != 0.0) {
+        // R19: loss += (kl_tau/D) log k_t on the set S; coef_t -= kl_tau/D there
+        const bool in_s = a.kl_set == RL_KL_ALL || (a.kl_set == RL_KL_UNMASKED ? kp : !kp);
+        if (in_s) {
+          klterm += a.kl_w * static_cast<double>(d);
+          c = static_cast<float>(static_cast<double>(c) - a.kl_w);
+        }
+      }
     } else if (lm) {
       nonfin += !fin;
       badtgt += (fin && !tg);
@@ -267,6 +277,7 @@ __global__ void __launch_bounds__(256) loss_coef_kernel(const LossArgs a) {
     if (a.keep) a.keep[t] = kp ? 1 : 0;
   }
   if (a.variant == RL_LOSS_GSPO) loss = (threadIdx.x == 0) ? gspo_J : 0.0;
+  loss -= klterm;  // report.loss = -sum(loss): the KL term enters with a + sign
   RolloutPartial p;
   p.loss = block_reduce_sum(loss, shd);
   p.kl = block_reduce_sum(kl, shd);
@@ -328,7 +339,8 @@ __global__ void compact_write_kernel(const float* __restrict__ coef, const float
                                      const int32_t* __restrict__ targets, int64_t T,
                                      const int* __restrict__ block_counts, int nblocks, int64_t chunk,
                                      int32_t* __restrict__ idx, float* __restrict__ coef_c, float* __restrict__ lse_c,
-                                     int32_t* __restrict__ tgt_c, int* __restrict__ chunk_counts, int n_chunks) {
+                                     int32_t* __restrict__ tgt_c, int* __restrict__ chunk_counts, int n_chunks,
+                                     const float* __restrict__ invt_rows, float* __restrict__ invt_c) {
   __shared__ int sh[256];
   __shared__ int base;
   if (threadIdx.x == 0) {
@@ -362,6 +374,7 @@ __global__ void compact_write_kernel(const float* __restrict__ coef, const float
       coef_c[pos] = coef[r];
       lse_c[pos] = lse[r];
       tgt_c[pos] = targets[r];
+      if (invt_rows != nullptr) invt_c[pos] = invt_rows[r];
       ++pos;
     }
   if (blockIdx.x == nblocks - 1 && threadIdx.x == 255) {
@@ -380,7 +393,8 @@ __global__ void compact_write_kernel(const float* __restrict__ coef, const float
 // Flat over (row, 16-byte vector), 4 loads in flight per thread before the stores.
 __global__ void gather_rows_kernel(const uint16_t* __restrict__ hidden, int64_t H, const int32_t* __restrict__ idx,
                                    const int* __restrict__ count_ptr, int pad, int64_t cap, uint16_t* __restrict__ h_c,
-                                   float* __restrict__ coef_c, float* __restrict__ lse_c, int32_t* __restrict__ tgt_c) {
+                                   float* __restrict__ coef_c, float* __restrict__ lse_c, int32_t* __restrict__ tgt_c,
+                                   float* __restrict__ invt_c) {
   const int count = *count_ptr;
   const int64_t padded = (static_cast<int64_t>(count) + pad < cap) ? static_cast<int64_t>(count) + pad : cap;
   const int64_t vecs = H / 8;  // 16-byte vectors per row (H % 8 == 0)
@@ -409,6 +423,7 @@ __global__ void gather_rows_kernel(const uint16_t* __restrict__ hidden, int64_t 
           coef_c[r] = 0.f;
           lse_c[r] = 0.f;
           tgt_c[r] = -1;
+          if (invt_c != nullptr) invt_c[r] = 1.f;
         }
       }
     }

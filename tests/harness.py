@@ -25,11 +25,13 @@ class Case:
     w64: np.ndarray
     infer: np.ndarray        # float32 stored inference log-probs
     adv: np.ndarray          # [R] float32 advantages (oracle fp64 rounded; S0 is tested separately)
-    inv_temperature: float
+    inv_temperature: object    # scalar 1/tau, or a [T] float64 array (per-token, R20)
     alpha: float = synth.ALPHA
     beta: float = synth.BETA
     guard: float = synth.GUARD
     variant: str = "icepop"
+    kl_tau: float = 0.0          # R19
+    kl_set: str = "masked"
 
 
 def make_case(wl: synth.Workload, seed=0, *, tokens=None, vocab=None, hidden=None, inv_temperature=1.0,
@@ -52,7 +54,7 @@ def run_oracle(c: Case, backward=True, loss_denominator=None):
         alpha=c.alpha, beta=c.beta, guard_threshold=c.guard,
         loss_denominator=b.loss_denominator if loss_denominator is None else loss_denominator,
         inv_temperature=c.inv_temperature, backward=backward, rollout_adv=c.adv.astype(np.float64),
-        variant=c.variant)
+        variant=c.variant, kl_tau=c.kl_tau, kl_set=c.kl_set)
 
 
 def band_tokens(c: Case, ref) -> np.ndarray:
@@ -161,9 +163,13 @@ def run_gpu_step(c: Case, *, dh_f32=False, accumulate_dw=False, dw_init=None, us
     b = c.batch
     d = to_device(c, device)
     T, H, V, R = b.T, b.H, b.V, len(c.adv)
-    shape = rl.make_shape(T, H, V, 0, V, c.inv_temperature)
+    if np.ndim(c.inv_temperature) == 1:
+        invt = torch.from_numpy(np.asarray(c.inv_temperature, dtype=np.float32)).to(device)
+        shape = rl.make_shape(T, H, V, 0, V, 1.0, inv_temperature_rows=invt)
+    else:
+        shape = rl.make_shape(T, H, V, 0, V, c.inv_temperature)
     params = rl.make_params(R, b.loss_denominator if loss_denominator is None else loss_denominator,
-                            c.alpha, c.beta, c.guard, c.variant)
+                            c.alpha, c.beta, c.guard, c.variant, kl_tau=c.kl_tau, kl_set=c.kl_set)
     f32 = dict(dtype=torch.float32, device=device)
     out = dict(logprob=torch.empty(T, **f32), entropy=torch.empty(T, **f32), lse=torch.empty(T, **f32),
                coef=torch.empty(T, **f32), keep=torch.empty(T, dtype=torch.uint8, device=device),

@@ -33,12 +33,12 @@ def test_every_declared_symbol_is_exported(lib):
 
 
 def test_struct_layouts_match_header(lib):
-    assert ctypes.sizeof(rl.rl_lm_shape) == 48
-    assert ctypes.sizeof(rl.rl_loss_params) == 32
+    assert ctypes.sizeof(rl.rl_lm_shape) == 56
+    assert ctypes.sizeof(rl.rl_loss_params) == 40
     assert ctypes.sizeof(rl.rl_loss_report) == 48
     assert ctypes.sizeof(rl.rl_loss_outputs) == 104
     assert ctypes.sizeof(rl.rl_nvls_reduce) == 88
-    assert lib.rl_abi_version() == 1
+    assert lib.rl_abi_version() == 2
 
 
 def test_status_strings(lib):
