@@ -13,7 +13,8 @@
  * head logits z_t = invT * W_vocab h_t over the full vocabulary. The library
  * minimises loss = -J and returns d loss / d hidden and d loss / d W_vocab.
  * The readings of every point the paper leaves open are listed in DESIGN.md §2
- * (R1-R15) and cited below as "R<n>".
+ * (R1-R20) and cited below as "R<n>". Options beyond Eq.1 (loss variants R16/R17,
+ * the KL term R19, per-token temperature R20) are off by default.
  *
  * Conventions for every call:
  *  - Pointers are DEVICE pointers unless the argument says HOST. The caller
@@ -184,7 +185,9 @@ rl_status rl_logprob_fwd(const rl_lm_shape* shape, const uint16_t* hidden,
 /* The whole step for one rank: logits (TMEM only) -> online log-softmax ->
  * k_t = exp(logprob_t - infer_logprobs_t) -> Eq.2 gate + rollout guard ->
  * coef_t -> loss, then the backward d loss / d u_tv = coef_t invT (p_tv - [v==y_t])
- * folded into d_hidden = dU W and d_w_vocab = dU^T hidden.
+ * folded into d_hidden = dU W and d_w_vocab = dU^T hidden. By default the
+ * backward GEMMs run over the rows with coef_t != 0 only (their dU row is the
+ * only non-zero one); d_hidden rows of the others are written as zeros.
  *   targets          [T] int32 global vocab ids (row t is scored on targets[t];
  *                    shifting labels is the caller's job)
  *   infer_logprobs   [T] fp32, log pi_infer(y_t) as stored by the inference engine
@@ -229,9 +232,10 @@ rl_status rl_fwd_partials(const rl_lm_shape* shape, const uint16_t* hidden,
 rl_status rl_merge_partials(const float* partials, int32_t n_parts, int64_t T, float* logprob,
                             float* entropy, float* lse, void* stream);
 
-/* S3: Eq.1/Eq.2/guard from logprob. Writes coef [T] (required), token_keep,
- * rollout_guarded (optional) and the report. targets/V_global only feed the
- * bad-target counter (targets may be NULL to skip it). */
+/* S3: Eq.1/Eq.2/guard (or the params' variant, plus the optional KL term R19)
+ * from logprob. Writes coef [T] (required; d loss / d logprob_t = -coef_t),
+ * token_keep, rollout_guarded (optional) and the report. targets/V_global only
+ * feed the bad-target counter (targets may be NULL to skip it). */
 rl_status rl_loss_coef(const rl_loss_params* params, int64_t T, int64_t V_global,
                        const float* logprob, const float* infer_logprobs, const int32_t* targets,
                        const float* rollout_adv, const int32_t* rollout_offsets,
