@@ -129,7 +129,8 @@ class VocabParallelPolicyLoss:
 
     def __init__(self, phases, *, T, H, V_global, num_rollouts, group_size, loss_denominator, group=None,
                  inv_temperature=1.0, alpha=0.5, beta=5.0, guard=1e-5, dz_chunk_rows=0, device=None,
-                 workspace=True, nvls=False):
+                 workspace=True, nvls=False, variant="icepop", kl_tau=0.0, kl_set="masked",
+                 inv_temperature_rows=None):
         self.ph = phases
         self.group = group
         self.world = dist.get_world_size(group)
@@ -139,8 +140,10 @@ class VocabParallelPolicyLoss:
         self.V_local = V_global // self.world
         self.vocab_offset = self.rank * self.V_local
         self.T, self.H, self.V_global, self.R, self.G = T, H, V_global, num_rollouts, group_size
-        self.shape = make_shape(T, H, self.V_local, self.vocab_offset, V_global, inv_temperature)
-        self.params = make_params(num_rollouts, loss_denominator, alpha, beta, guard)
+        self.invt_rows = inv_temperature_rows          # kept alive: the shape points at it
+        self.shape = make_shape(T, H, self.V_local, self.vocab_offset, V_global, inv_temperature,
+                                inv_temperature_rows=inv_temperature_rows)
+        self.params = make_params(num_rollouts, loss_denominator, alpha, beta, guard, variant, kl_tau, kl_set)
         self.chunk = dz_chunk_rows
         dev = device
         f32 = dict(dtype=torch.float32, device=dev)
@@ -191,7 +194,8 @@ class DataParallelPolicyLoss:
 
     def __init__(self, phases, *, T, H, V, num_rollouts, group_size, loss_denominator, group=None,
                  inv_temperature=1.0, alpha=0.5, beta=5.0, guard=1e-5, device=None, d_hidden_dtype=torch.bfloat16,
-                 workspace=True, overlap=False, comm_sms=24, nvls=False):
+                 workspace=True, overlap=False, comm_sms=24, nvls=False, variant="icepop", kl_tau=0.0,
+                 kl_set="masked", inv_temperature_rows=None):
         self.ph = phases
         # overlap: the dW all-reduce (NCCL, side stream) runs concurrently with K5,
         # which then uses all but `comm_sms` SMs (NCCL's NVLS channels need SMs).
@@ -203,8 +207,9 @@ class DataParallelPolicyLoss:
         self.group = group
         self.world = dist.get_world_size(group)
         self.T, self.H, self.V, self.R, self.G = T, H, V, num_rollouts, group_size
-        self.shape = make_shape(T, H, V, 0, V, inv_temperature)
-        self.params = make_params(num_rollouts, loss_denominator, alpha, beta, guard)
+        self.invt_rows = inv_temperature_rows          # kept alive: the shape points at it
+        self.shape = make_shape(T, H, V, 0, V, inv_temperature, inv_temperature_rows=inv_temperature_rows)
+        self.params = make_params(num_rollouts, loss_denominator, alpha, beta, guard, variant, kl_tau, kl_set)
         dev = device
         f32 = dict(dtype=torch.float32, device=dev)
         self.logprob = torch.empty(T, **f32)

@@ -48,9 +48,13 @@ class OraclePhases:
 
     def loss_coef(self, params, T, V_global, logprob, infer, targets, adv, offsets, loss_mask, coef, keep, guarded,
                   report, workspace=None):
-        rep = oracle.icepop_loss(logprob.double().numpy(), infer.double().numpy(), adv.double().numpy(),
-                                 offsets.numpy(), loss_mask.numpy(), params.alpha, params.beta,
-                                 params.guard_threshold, params.loss_denominator, targets.long().numpy(), V_global)
+        variant = {v: k for k, v in oracle.LOSS_VARIANTS.items()}[params.variant]
+        kl_set = {v: k for k, v in oracle.KL_SETS.items()}[params.kl_set]
+        lp, inf = logprob.double().numpy(), infer.double().numpy()
+        rep = oracle.variant_loss(variant, lp, inf, adv.double().numpy(), offsets.numpy(), loss_mask.numpy(),
+                                  params.alpha, params.beta, params.guard_threshold, params.loss_denominator,
+                                  targets=targets.long().numpy(), vocab=V_global)
+        rep = oracle.add_kl_term(rep, lp, inf, params.kl_tau, kl_set, params.loss_denominator)
         coef.copy_(torch.from_numpy(rep.coef))
         keep.copy_(torch.from_numpy(rep.keep.astype(np.uint8)))
         guarded.copy_(torch.from_numpy(rep.guarded.astype(np.uint8)))
@@ -77,7 +81,10 @@ class OraclePhases:
                                          alpha=params.alpha, beta=params.beta,
                                          guard_threshold=params.guard_threshold,
                                          loss_denominator=params.loss_denominator,
-                                         inv_temperature=shape.inv_temperature, rollout_adv=adv.double().numpy())
+                                         inv_temperature=shape.inv_temperature, rollout_adv=adv.double().numpy(),
+                                         variant={v: k for k, v in oracle.LOSS_VARIANTS.items()}[params.variant],
+                                         kl_tau=params.kl_tau,
+                                         kl_set={v: k for k, v in oracle.KL_SETS.items()}[params.kl_set])
         logprob.copy_(torch.from_numpy(res.logp))
         d_hidden.copy_(torch.from_numpy(res.d_hidden))
         d_w_vocab.copy_(torch.from_numpy(res.d_w_vocab))
@@ -99,13 +106,16 @@ def _bf16(bits):
     return torch.from_numpy(bits.view(np.int16).copy()).view(torch.bfloat16)
 
 
-def _vocab_worker(rank, port, out_dir):
+LOSS_KW = [{}, {"variant": "cispo", "kl_tau": 0.375, "kl_set": "all"}]   # 0.375: exact in the fp32 ABI field
+
+
+def _vocab_worker(rank, port, out_dir, kw_i=0):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=WORLD)
     b, h64, w64, infer = _batch()
     vp = parallel.VocabParallelPolicyLoss(OraclePhases(), T=b.T, H=b.H, V_global=b.V, num_rollouts=len(b.rewards.reshape(-1)),
                                           group_size=WL.group_size, loss_denominator=b.loss_denominator,
-                                          device="cpu", workspace=False)
+                                          device="cpu", workspace=False, **LOSS_KW[kw_i])
     lo, hi = vp.vocab_offset, vp.vocab_offset + vp.V_local
     dw = torch.empty(vp.V_local, b.H, dtype=torch.float64)
     for name in ("parts", "d_hidden", "logprob", "entropy", "lse", "coef", "adv"):
@@ -118,7 +128,7 @@ def _vocab_worker(rank, port, out_dir):
     dist.destroy_process_group()
 
 
-def _dp_worker(rank, port, out_dir):
+def _dp_worker(rank, port, out_dir, kw_i=0):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=WORLD)
     b, h64, w64, infer = _batch()
@@ -130,7 +140,7 @@ def _dp_worker(rank, port, out_dir):
     D = parallel.DataParallelPolicyLoss.global_denominator(lm)
     dp = parallel.DataParallelPolicyLoss(OraclePhases(), T=t1 - t0, H=b.H, V=b.V, num_rollouts=G, group_size=G,
                                          loss_denominator=D, device="cpu", d_hidden_dtype=torch.float64,
-                                         workspace=False)
+                                         workspace=False, **LOSS_KW[kw_i])
     for name in ("logprob", "entropy", "lse", "coef", "adv"):
         setattr(dp, name, getattr(dp, name).double())
     dw = torch.empty(b.V, b.H, dtype=torch.float64)
@@ -144,15 +154,16 @@ def _dp_worker(rank, port, out_dir):
     dist.destroy_process_group()
 
 
-def _reference():
+def _reference(kw_i=0):
     b, h64, w64, infer = _batch()
     return b, oracle.policy_loss_fwd_bwd(h64, w64, b.targets, infer.astype(np.float64), b.rewards,
-                                         b.rollout_offsets, b.loss_mask)
+                                         b.rollout_offsets, b.loss_mask, **LOSS_KW[kw_i])
 
 
-def test_vocab_parallel_composition(tmp_path):
-    mp.start_processes(_vocab_worker, args=(_free_port(), str(tmp_path)), nprocs=WORLD, start_method="spawn")
-    b, ref = _reference()
+@pytest.mark.parametrize("kw_i", range(len(LOSS_KW)))
+def test_vocab_parallel_composition(tmp_path, kw_i):
+    mp.start_processes(_vocab_worker, args=(_free_port(), str(tmp_path), kw_i), nprocs=WORLD, start_method="spawn")
+    b, ref = _reference(kw_i)
     outs = [np.load(tmp_path / f"vp{r}.npz") for r in range(WORLD)]
     for o in outs:   # S2/S3 are identical on every rank; dH is the reduced sum
         np.testing.assert_allclose(o["logprob"], ref.logp, atol=1e-6)
@@ -163,9 +174,10 @@ def test_vocab_parallel_composition(tmp_path):
     assert [int(o["lo"]) for o in outs] == [0, b.V // 2]
 
 
-def test_data_parallel_composition(tmp_path):
-    mp.start_processes(_dp_worker, args=(_free_port(), str(tmp_path)), nprocs=WORLD, start_method="spawn")
-    b, ref = _reference()
+@pytest.mark.parametrize("kw_i", range(len(LOSS_KW)))
+def test_data_parallel_composition(tmp_path, kw_i):
+    mp.start_processes(_dp_worker, args=(_free_port(), str(tmp_path), kw_i), nprocs=WORLD, start_method="spawn")
+    b, ref = _reference(kw_i)
     outs = [np.load(tmp_path / f"dp{r}.npz") for r in range(WORLD)]
     for o in outs:
         assert float(o["D"]) == b.loss_denominator            # global D, reading R5

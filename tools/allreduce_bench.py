@@ -1,6 +1,5 @@
 """NCCL collective timing for the dW / dH exchange sizes (run under torchrun)."""
 import os
-import time
 
 import torch
 import torch.distributed as dist
