@@ -103,7 +103,8 @@ def rollout_lengths(wl: Workload, seed: int, total_tokens: int | None = None) ->
         base[: T - int(base.sum())] += 1
         return base
     w = _rng(seed, _K_LENGTHS).lognormal(0.0, 1.0, size=R)
-    L = np.maximum(1, np.floor(w / w.sum() * T).astype(np.int64))
+    lo = 1 if T >= R else 0          # fewer tokens than rollouts: some rollouts are empty
+    L = np.maximum(lo, np.floor(w / w.sum() * T).astype(np.int64))
     # fix the rounding so the lengths sum to exactly T (largest rollouts absorb it)
     diff = T - int(L.sum())
     order = np.argsort(-L, kind="stable")
@@ -111,7 +112,7 @@ def rollout_lengths(wl: Workload, seed: int, total_tokens: int | None = None) ->
     while diff != 0:
         j = order[i % R]
         step = 1 if diff > 0 else -1
-        if L[j] + step >= 1:
+        if L[j] + step >= lo:
             L[j] += step
             diff -= step
         i += 1
