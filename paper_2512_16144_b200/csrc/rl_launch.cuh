@@ -1,0 +1,291 @@
+// librl host code: TMA tensor maps, the tuning knobs (CTA group, raster, soft k-barrier, wide tiles) and the GEMM launchers.
+// Included once, in order, by rl_api.cu (a single translation unit); everything
+// here has internal linkage.
+#pragma once
+
+namespace {
+
+// ------------------------------------------------------------ tensor maps
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+rl_status get_encode(EncodeTiledFn& fn) {
+  static EncodeTiledFn cached = nullptr;
+  static std::once_flag once;
+  static cudaError_t err = cudaSuccess;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    err = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q);
+    if (err == cudaSuccess && q == cudaDriverEntryPointSuccess) cached = reinterpret_cast<EncodeTiledFn>(p);
+  });
+  if (!cached) return fail(RL_ERR_CUDA, "cuTensorMapEncodeTiled unavailable (%s)", cudaGetErrorString(err));
+  fn = cached;
+  return RL_OK;
+}
+
+// 2-D row-major tensor [outer][inner], 128-byte swizzle, zero fill out of bounds.
+rl_status make_map(CUtensorMap* m, const void* ptr, bool f32, int64_t inner, int64_t outer, int64_t row_elems,
+                   int box_inner, int box_outer) {
+  EncodeTiledFn enc;
+  rl_status s = get_encode(enc);
+  if (s != RL_OK) return s;
+  const int esz = f32 ? 4 : 2;
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(inner), static_cast<cuuint64_t>(outer > 0 ? outer : 1)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(row_elems * esz)};
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(box_inner), static_cast<cuuint32_t>(box_outer)};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(m, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                   const_cast<void*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return fail(RL_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d) for [%lld x %lld] box %dx%d", (int)r,
+                (long long)outer, (long long)inner, box_outer, box_inner);
+  return RL_OK;
+}
+
+// ----------------------------------------------------------------- GEMMs
+// CTA-pair (cta_group::2, 256x256 tiles) by default; RL_CTA_GROUP=1 selects the
+// single-CTA 128x256 variant (kept for A/B measurements and as a fallback).
+int cta_group() {
+  static int cg = [] {
+    const char* e = getenv("RL_CTA_GROUP");
+    return (e && atoi(e) == 1) ? 1 : 2;
+  }();
+  return cg;
+}
+
+// Raster group (in m-blocks) per GEMM: tiles walk n inside groups of this many
+// m-blocks. Defaults chosen from the sweep in DESIGN.md §5; RL_GROUP_M_<K>
+// overrides (K in FWD, DZ, DH, DW) for measurements.
+int group_m_for(int kid, int dflt) {
+  static int cache[16];
+  static bool init[16] = {};
+  if (!init[kid]) {
+    const char* names[16] = {nullptr, "RL_GROUP_M_FWD", nullptr, nullptr, nullptr, "RL_GROUP_M_DZ",
+                             "RL_GROUP_M_DH", "RL_GROUP_M_DW"};
+    const char* e = names[kid] ? getenv(names[kid]) : nullptr;
+    cache[kid] = (e && atoi(e) > 0) ? atoi(e) : dflt;
+    init[kid] = true;
+  }
+  return cache[kid];
+}
+
+// Soft k-barrier between producers (see EpiParams::sync_*): every RL_SYNC_EVERY
+// k-blocks (default 32; 0 = off), at most RL_SYNC_SLACK sync points of lead
+// (default 2). Keeping the CTAs that share operands inside one L2 window cuts
+// K5/K6 DRAM reads by ~1/3 and lets the power-capped clock rise (~6% per step,
+// profiles/r01/). Correctness never depends on it (the wait is bounded).
+// Per-GEMM overrides: RL_SYNC_EVERY_<K>, RL_SYNC_SLACK_<K> (K in FWD, DZ, DH, DW, NS).
+const char* kid_suffix(int kid) {
+  switch (kid) {
+    case RL_K_FWD_GEMM: return "FWD";
+    case RL_K_DZ_GEMM: return "DZ";
+    case RL_K_DH_GEMM: return "DH";
+    case RL_K_DW_GEMM: return "DW";
+    case RL_K_NS_GEMM: return "NS";
+    default: return "OTHER";
+  }
+}
+int env_int(const char* base, int kid, int dflt) {
+  char name[64];
+  snprintf(name, sizeof(name), "%s_%s", base, kid_suffix(kid));
+  const char* e = getenv(name);
+  if (!e) e = getenv(base);
+  return e ? atoi(e) : dflt;
+}
+int sync_every_for(int kid) {
+  static int cache[32];
+  static bool init[32] = {};
+  if (kid < 0 || kid >= 32) return 0;
+  if (!init[kid]) {
+    cache[kid] = env_int("RL_SYNC_EVERY", kid, 32);
+    init[kid] = true;
+  }
+  return cache[kid];
+}
+// Wide 256 x 512 pair tiles (NB = 2, rl_gemm.cuh): RL_WIDE[_<K>] = 0/1, default on
+// for K1 (FWD), K5 (DH), K6 (DW) and the Newton-Schulz GEMMs (NS: 41.0 -> 38.6 ms); RL_SKEW = 0/2/3 k-blocks of block-0-first MMA
+// order at both ends of a tile (default 3), which hides the epilogue of one TMEM
+// half. K4 (DZ) stays narrow: its exp + bf16-store epilogue per half is longer
+// than that cover (measured: K4 15.6 -> 17.9 ms wide, K1 15.6 -> 15.2 ms).
+bool wide_for(int kid) {
+  static int cache[32];
+  static bool init[32] = {};
+  if (kid < 0 || kid >= 32) return false;
+  if (!init[kid]) {
+    const bool dflt = kid == RL_K_FWD_GEMM || kid == RL_K_DH_GEMM || kid == RL_K_DW_GEMM || kid == RL_K_NS_GEMM;
+    cache[kid] = env_int("RL_WIDE", kid, dflt ? 1 : 0);
+    init[kid] = true;
+  }
+  return cache[kid] != 0;
+}
+int skew() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("RL_SKEW");
+    v = e ? atoi(e) : 3;
+    if (v != 0 && v != 2) v = 3;
+  }
+  return v;
+}
+int sync_slack_for(int kid) {
+  static int cache[32];
+  static bool init[32] = {};
+  if (kid < 0 || kid >= 32) return 2;
+  if (!init[kid]) {
+    cache[kid] = env_int("RL_SYNC_SLACK", kid, 2);
+    init[kid] = true;
+  }
+  return cache[kid];
+}
+constexpr int kMaxSyncPoints = 1 << 16;
+thread_local uint32_t* g_sync_ctr = nullptr;  // set per call from the workspace
+
+template <int CG, int NB>
+constexpr int stages_for() {
+  return CG == 2 ? (NB == 2 ? 4 : 6) : 4;
+}
+
+template <int MODE, bool A_MN, bool B_MN, int CG, int NB = 1, int SKEW = 0>
+rl_status launch_gemm_cg(int kid, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c, int64_t M,
+                         int64_t N, int64_t K, int group_m, const rl::EpiParams& ep, int sms, cudaStream_t st,
+                         int k_splits = 1, int split_rows = 0, const int* dyn_count = nullptr, int dyn_mode = 0) {
+  constexpr int S = stages_for<CG, NB>();
+  auto kern = rl::gemm_kernel<MODE, A_MN, B_MN, CG, S, NB, SKEW>;
+  constexpr int smem = rl::gemm_smem_bytes<CG, S, false, NB>();
+  static_assert(smem <= 232448, "dynamic shared memory over 227 KB");
+  static bool attr_set = false;  // per instantiation
+  if (!attr_set) {
+    RL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    attr_set = true;
+  }
+  using TL = rl::Tiling<CG>;
+  rl::GemmShape sh;
+  sh.m_blocks = static_cast<int>((M + TL::TILE_M - 1) / TL::TILE_M);
+  sh.n_blocks = static_cast<int>((N + rl::BN * NB - 1) / (rl::BN * NB));
+  sh.k_blocks = static_cast<int>((K + rl::BK - 1) / rl::BK);
+  sh.group_m = group_m;
+  if (sh.k_blocks == 0) return fail(RL_ERR_SHAPE, "GEMM with K = 0");
+  if (k_splits < 1) k_splits = 1;
+  if (k_splits > sh.k_blocks) k_splits = sh.k_blocks;
+  sh.k_per_split = (sh.k_blocks + k_splits - 1) / k_splits;
+  sh.k_splits = (sh.k_blocks + sh.k_per_split - 1) / sh.k_per_split;
+  sh.split_rows = split_rows;
+  sh.dyn_count = dyn_count;
+  sh.dyn_mode = dyn_count ? dyn_mode : 0;
+  if (sh.k_splits > 1 && (MODE == rl::EPI_LSE || MODE == rl::EPI_DZ || MODE == rl::EPI_F32_NVLS))
+    return fail(RL_ERR_UNSUPPORTED, "split-K needs a plain store epilogue");
+  const int64_t tiles = static_cast<int64_t>(sh.m_blocks) * sh.n_blocks * sh.k_splits;
+  const int units = static_cast<int>(tiles < sms / CG ? tiles : sms / CG);
+  rl::EpiParams ep2 = ep;
+  ep2.sync_every = 0;
+  if (g_sync_ctr && sync_every_for(kid) > 0) {
+    const int64_t max_tiles = (tiles + units - 1) / units;
+    const int se = sync_every_for(kid);
+    const int64_t max_sync = (max_tiles * sh.k_blocks - 1) / se;
+    if (max_sync > 0 && max_sync < kMaxSyncPoints) {
+      RL_CUDA(cudaMemsetAsync(g_sync_ctr, 0, static_cast<size_t>(max_sync + 1) * 4, st));
+      ep2.sync_ctr = g_sync_ctr;
+      ep2.sync_every = se;
+      ep2.sync_slack = sync_slack_for(kid);
+      ep2.max_sync = static_cast<int>(max_sync);
+    }
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(units * CG);
+  cfg.blockDim = dim3(rl::GEMM_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CG;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  {
+    ProfScope ps(kid, st);
+    RL_CUDA(cudaLaunchKernelEx(&cfg, kern, a, b, c, sh, ep2));
+  }
+  RL_CHECK_LAUNCH();
+  return RL_OK;
+}
+
+template <int MODE, bool A_MN, bool B_MN>
+rl_status launch_gemm(int kid, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c, int64_t M, int64_t N,
+                      int64_t K, int group_m, const rl::EpiParams& ep, int sms, cudaStream_t st, int k_splits = 1,
+                      int split_rows = 0, const int* dyn_count = nullptr, int dyn_mode = 0) {
+  if (M <= 0 || N <= 0) return RL_OK;
+  // wide tiles only where a tile covers at least two 256-column blocks
+  if (cta_group() == 2 && wide_for(kid) && N > rl::BN) {
+    switch (skew()) {
+      case 0:
+        return launch_gemm_cg<MODE, A_MN, B_MN, 2, 2, 0>(kid, a, b, c, M, N, K, group_m, ep, sms, st, k_splits,
+                                                         split_rows, dyn_count, dyn_mode);
+      case 2:
+        return launch_gemm_cg<MODE, A_MN, B_MN, 2, 2, 2>(kid, a, b, c, M, N, K, group_m, ep, sms, st, k_splits,
+                                                         split_rows, dyn_count, dyn_mode);
+      default:
+        return launch_gemm_cg<MODE, A_MN, B_MN, 2, 2, 3>(kid, a, b, c, M, N, K, group_m, ep, sms, st, k_splits,
+                                                         split_rows, dyn_count, dyn_mode);
+    }
+  }
+  if (cta_group() == 2)
+    return launch_gemm_cg<MODE, A_MN, B_MN, 2>(kid, a, b, c, M, N, K, group_m, ep, sms, st, k_splits, split_rows,
+                                               dyn_count, dyn_mode);
+  return launch_gemm_cg<MODE, A_MN, B_MN, 1>(kid, a, b, c, M, N, K, group_m, ep, sms, st, k_splits, split_rows,
+                                             dyn_count, dyn_mode);
+}
+
+// Grouped GEMM (MoE experts): the tile count is only known on the device (it
+// depends on the group offsets), so the grid is sized from an upper bound.
+template <int CG>
+rl_status launch_grouped_cg(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c, int64_t rows,
+                            int64_t N, int64_t K, int n_groups, const rl::EpiParams& ep, int sms, cudaStream_t st) {
+  constexpr int S = CG == 2 ? 5 : 3;
+  auto kern = rl::gemm_kernel<rl::EPI_BF16_GROUPED, false, false, CG, S>;
+  constexpr int smem = rl::gemm_smem_bytes<CG, S, true>();
+  static bool attr_set = false;
+  if (!attr_set) {
+    RL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    attr_set = true;
+  }
+  using TL = rl::Tiling<CG>;
+  rl::GemmShape sh = {};
+  sh.n_blocks = static_cast<int>((N + rl::BN - 1) / rl::BN);
+  sh.m_blocks = static_cast<int>((rows + TL::TILE_M - 1) / TL::TILE_M) + n_groups;  // bound on group m-blocks
+  sh.k_blocks = static_cast<int>((K + rl::BK - 1) / rl::BK);
+  sh.group_m = 1;
+  sh.k_splits = 1;
+  sh.k_per_split = sh.k_blocks;
+  const int64_t tiles = static_cast<int64_t>(sh.m_blocks) * sh.n_blocks;
+  const int units = static_cast<int>(tiles < sms / CG ? tiles : sms / CG);
+  rl::EpiParams e = ep;
+  e.sync_every = 0;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(units * CG);
+  cfg.blockDim = dim3(rl::GEMM_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CG;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  {
+    ProfScope ps(RL_K_GROUPED_GEMM, st);
+    RL_CUDA(cudaLaunchKernelEx(&cfg, kern, a, b, c, sh, e));
+  }
+  RL_CHECK_LAUNCH();
+  return RL_OK;
+}
+
+// Rows of A staged per CTA per tile (the TMA box height for A loads).
+constexpr int kARows = 128;
+
+}  // namespace
