@@ -15,6 +15,8 @@ package; tests substitute a CPU double to check this host logic on gloo.
 """
 from __future__ import annotations
 
+import os
+
 import torch
 import torch.distributed as dist
 
@@ -45,7 +47,11 @@ class NvlsReduction:
         torch.cuda.synchronize(device)
         self.handle.barrier(channel=0)
 
-    def descriptor(self, lag=2) -> rl_nvls_reduce:
+    def descriptor(self, lag=None) -> rl_nvls_reduce:
+        """lag: the owner reduces a slab this many tiles after its own store of it
+        (more lag = more slack for slower ranks; RL_NVLS_LAG, default 2)."""
+        if lag is None:
+            lag = int(os.environ.get("RL_NVLS_LAG", "2"))
         self.epoch += 1
         d = rl_nvls_reduce()
         d.multicast = self.handle.multicast_ptr
