@@ -332,7 +332,8 @@ def main_ours(args):
         engine = parallel.DataParallelPolicyLoss(phases, T=T, H=H, V=Vt, num_rollouts=R,
                                                  group_size=wl_rank.group_size, loss_denominator=D, device=dev,
                                                  overlap=args.overlap, comm_sms=args.comm_sms,
-                                                 nvls=args.collective == "nvls")
+                                                 nvls=args.collective == "nvls",
+                                                 reduce_scatter=args.dw_reduce_scatter and args.collective == "nvls")
         ws = engine.ws
         dh = engine.d_hidden
     else:
@@ -446,7 +447,9 @@ def main_ours(args):
             if nvls_dp:
                 rl.rl_policy_loss_fwd_bwd_hostio(shape, params, wl_rank.group_size, hpin, b["w"], tpin, ipin, rpin,
                                                  opin, mpin, report=report, d_hidden=dh, d_w_vocab=engine.nvls.buf,
-                                                 d_w_vocab_nvls=engine.nvls.descriptor(), dz_chunk_rows=chunk,
+                                                 d_w_vocab_nvls=engine.nvls.descriptor(
+                                                     mode=1 if engine.reduce_scatter else 0),
+                                                 dz_chunk_rows=chunk,
                                                  dense_backward=args.dense_backward, workspace=wsh)
                 engine.nvls.barrier()
                 return
@@ -523,8 +526,11 @@ def main_ours(args):
             # the step's exchange and its NVLink roofline (900 GB/s per direction): NVLS moves
             # about 1x the buffer per GPU and direction, a ring all-reduce 2(N-1)/N x
             nb = (T * H * 4) if vocab_par else (V_local * H * 4)
-            per_dir = nb if args.collective == "nvls" else 2 * (world - 1) / world * nb
-            cfg["collective"] = {"op": ("dH" if vocab_par else "dW") + " fp32 all-reduce",
+            rs = (not vocab_par) and args.dw_reduce_scatter and args.collective == "nvls"
+            per_dir = (nb * (world - 1) / world if rs else nb) if args.collective == "nvls" \
+                else 2 * (world - 1) / world * nb
+            cfg["collective"] = {"op": ("dH" if vocab_par else "dW") + " fp32 " +
+                                 ("reduce-scatter (vocab rows)" if rs else "all-reduce"),
                                  "buffer_bytes": nb, "bytes_per_gpu_per_direction": per_dir,
                                  "nvlink_roofline_ms": per_dir / 900e9 * 1e3}
         out = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
@@ -555,6 +561,8 @@ def main():
     ap.add_argument("--ref-tokens", type=int, default=256)
     ap.add_argument("--dense-backward", action="store_true",
                     help="run the backward GEMMs over all rows instead of the coef != 0 rows (A/B)")
+    ap.add_argument("--dw-reduce-scatter", action="store_true",
+                    help="DP + NVLS: reduce-scatter dW by vocab rows (FSDP-consistent) instead of all-reduce")
     ap.add_argument("--overlap", action="store_true", help="DP + NCCL: all-reduce dW on a side stream under K5")
     ap.add_argument("--collective", default="auto", choices=["auto", "nccl", "nvls"],
                     help="nvls: the dW (DP) / dH (vocab-parallel) all-reduce is fused into the GEMM epilogue "

@@ -123,10 +123,15 @@ typedef struct rl_loss_report {
 /* Fused cross-rank reduction of an fp32 output over an NVLink multicast group
  * (NVLS), done inside the producing GEMM's epilogue: every rank stores its own
  * contribution into its replica of a symmetric buffer (the usual output pointer),
- * publishes a per-slab flag, and the rank owning each tile sums that slab over
- * all replicas with multimem.ld_reduce and writes the sum to all of them with
- * multimem.st. After the call, and after a cross-rank barrier the caller runs on
- * the same stream, every replica holds the sum over ranks (an all-reduce).
+ * publishes a per-slab flag (32 output rows), and the slab's owner sums it over
+ * all replicas with multimem.ld_reduce.
+ *   mode RL_NVLS_ALL_REDUCE (0): the owner is tile % world and writes the sum to
+ *     every replica with multimem.st; after the call, and after a cross-rank
+ *     barrier the caller runs on the same stream, every replica holds the sum.
+ *   mode RL_NVLS_REDUCE_SCATTER (1, FSDP-consistent): rank r owns the
+ *     output rows [r S, min((r+1) S, rows)), S = rl_nvls_shard_rows(rows, world),
+ *     and writes their sum to its own replica only (half the NVLink traffic);
+ *     its other rows keep its own contribution.
  * Requirements: the output pointer is this rank's view of the symmetric buffer
  * whose multicast VA is `multicast`; each flag array holds rl_nvls_flag_count()
  * uint32 entries, zeroed once at allocation; `epoch` increases on every call;
@@ -139,7 +144,13 @@ typedef struct rl_nvls_reduce {
   int32_t world;                      /* ranks in the group, 2..RL_NVLS_MAX_RANKS          */
   uint32_t epoch;                     /* > every epoch used before with these flags        */
   int32_t lag;                        /* tiles between a slab's store and its reduction; 0 = 2 */
+  int32_t mode;                       /* rl_nvls_mode                                      */
+  int32_t _pad;
 } rl_nvls_reduce;
+typedef enum rl_nvls_mode { RL_NVLS_ALL_REDUCE = 0, RL_NVLS_REDUCE_SCATTER = 1 } rl_nvls_mode;
+
+/* Rows per rank of the reduce-scatter mode: ceil(rows / (32 world)) * 32 (whole slabs). */
+int64_t rl_nvls_shard_rows(int64_t rows, int32_t world);
 
 /* Outputs of rl_policy_loss_fwd_bwd. Optional pointers may be NULL. */
 typedef struct rl_loss_outputs {

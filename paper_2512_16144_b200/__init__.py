@@ -65,7 +65,10 @@ NVLS_MAX_RANKS = 8
 class rl_nvls_reduce(ctypes.Structure):
     _fields_ = [("multicast", ctypes.c_void_p), ("flags", ctypes.c_void_p * NVLS_MAX_RANKS),
                 ("rank", ctypes.c_int32), ("world", ctypes.c_int32), ("epoch", ctypes.c_uint32),
-                ("lag", ctypes.c_int32)]
+                ("lag", ctypes.c_int32), ("mode", ctypes.c_int32), ("_pad", ctypes.c_int32)]
+
+
+RL_NVLS_ALL_REDUCE, RL_NVLS_REDUCE_SCATTER = 0, 1
 
 
 class rl_loss_outputs(ctypes.Structure):
@@ -109,6 +112,7 @@ _SIGS = {
                                  ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(rl_nvls_reduce),
                                  ctypes.POINTER(rl_nvls_reduce), _P, ctypes.c_size_t, _P]),
     "rl_nvls_flag_count": (ctypes.c_int64, [ctypes.POINTER(rl_lm_shape), ctypes.c_int32]),
+    "rl_nvls_shard_rows": (ctypes.c_int64, [ctypes.c_int64, ctypes.c_int32]),
     "rl_newton_schulz": (ctypes.c_int, [_P, ctypes.c_int64, ctypes.c_int64, ctypes.c_int32, _P, _P,
                                         ctypes.c_size_t, _P]),
     "rl_newton_schulz_workspace_bytes": (ctypes.c_size_t, [ctypes.c_int64, ctypes.c_int64]),
@@ -351,6 +355,11 @@ def rl_bwd_ex(shape: rl_lm_shape, hidden, w_vocab, targets, lse, coef, d_hidden=
                                     ctypes.pointer(dw_nvls) if dw_nvls is not None else None,
                                     ctypes.pointer(dh_nvls) if dh_nvls is not None else None,
                                     _ptr(ws), ws.numel(), _stream(stream)))
+
+
+def rl_nvls_shard_rows(rows: int, world: int) -> int:
+    """Rows each rank owns in the reduce-scatter mode (whole 32-row slabs)."""
+    return int(load_library().rl_nvls_shard_rows(int(rows), int(world)))
 
 
 def rl_nvls_flag_count(shape: rl_lm_shape, which: int) -> int:

@@ -62,6 +62,8 @@ int32_t rl_profile_read(rl_kernel_time* out, int32_t cap) {
 
 int64_t rl_default_dz_chunk_rows(const rl_lm_shape* shape) { return shape ? shape->T : 0; }
 
+int64_t rl_nvls_shard_rows(int64_t rows, int32_t world) { return nvls_shard_rows(rows, world); }
+
 int64_t rl_nvls_flag_count(const rl_lm_shape* shape, int32_t which) {
   if (!shape) return 0;
   // slabs = tiles x 8 (2 CTAs x 4 epilogue warps), counted with the smaller

@@ -118,6 +118,9 @@ struct EpiParams {
   int nvls_rank, nvls_world;
   uint32_t nvls_epoch;
   int nvls_lag;                            // reduce the slab finished this many tiles ago
+  int nvls_mode;                           // 0 all-reduce (owner tile % world), 1 reduce-scatter by rows
+  int64_t nvls_shard;                      // mode 1: rows per rank (a multiple of 32)
+  float* nvls_local;                       // mode 1: this rank's replica (plain stores)
 };
 
 __device__ __forceinline__ void red_release_add(uint32_t* p, uint32_t v) {
@@ -169,7 +172,15 @@ __device__ __forceinline__ int nvls_slab(int tile, uint32_t rank, int q) { retur
 template <int TILE_M, int TN>
 __device__ __noinline__ void nvls_reduce_slab_impl(const EpiParams& ep, const GemmShape& sh, int tile, uint32_t rank,
                                                    int q, int lane) {
-  if (tile % ep.nvls_world != ep.nvls_rank) return;
+  int m, n;
+  tile_coords(tile, sh, m, n);
+  const int64_t r0 = static_cast<int64_t>(m) * TILE_M + rank * 128 + q * 32;
+  if (ep.nvls_mode == 0) {
+    if (tile % ep.nvls_world != ep.nvls_rank) return;
+  } else {
+    const int64_t own = r0 / ep.nvls_shard;
+    if ((own < ep.nvls_world ? own : ep.nvls_world - 1) != ep.nvls_rank || r0 >= ep.rows) return;
+  }
   const int slab = nvls_slab(tile, rank, q);
   if (lane < ep.nvls_world) {
     const uint32_t* f = ep.nvls_flags[lane] + slab;
@@ -180,9 +191,6 @@ __device__ __noinline__ void nvls_reduce_slab_impl(const EpiParams& ep, const Ge
     }
   }
   __syncwarp();
-  int m, n;
-  tile_coords(tile, sh, m, n);
-  const int64_t r0 = static_cast<int64_t>(m) * TILE_M + rank * 128 + q * 32;
   const int64_t c0 = static_cast<int64_t>(n) * TN;
   const int64_t rleft = ep.rows - r0, cleft = ep.cols - c0;
   const int rmax = rleft < 32 ? static_cast<int>(rleft) : 32;
@@ -203,7 +211,13 @@ __device__ __noinline__ void nvls_reduce_slab_impl(const EpiParams& ep, const Ge
 #pragma unroll
       for (int h = 0; h < H; ++h) {
         const int c = h * 128 + lane * 4;
-        if (rb + i < rmax && c < cmax) mc_st_v4(ep.nvls_mc + (r0 + rb + i) * ep.cols + c0 + c, v[i][h]);
+        if (rb + i < rmax && c < cmax) {
+          const int64_t off = (r0 + rb + i) * ep.cols + c0 + c;
+          if (ep.nvls_mode == 0)
+            mc_st_v4(ep.nvls_mc + off, v[i][h]);
+          else
+            *reinterpret_cast<float4*>(ep.nvls_local + off) = make_float4(v[i][h][0], v[i][h][1], v[i][h][2], v[i][h][3]);
+        }
       }
   }
 }

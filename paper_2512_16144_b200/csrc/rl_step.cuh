@@ -78,8 +78,15 @@ rl_status loss_impl(const rl_loss_params* p, int64_t T, int64_t V_global, const 
 // K4 -> K5 -> K6 per chunk of rows.
 // Fill the NVLS fields of an epilogue from the caller's descriptor; the
 // multicast VA is offset like the local output pointer `local`.
+int64_t nvls_shard_rows(int64_t rows, int32_t world) {
+  return world > 0 ? (rows + 32 * int64_t(world) - 1) / (32 * int64_t(world)) * 32 : rows;
+}
+
+// e.rows must be set first (the reduce-scatter shard is a row range of D)
 void set_nvls(rl::EpiParams& e, const rl_nvls_reduce* n, const float* local) {
-  (void)local;
+  e.nvls_local = const_cast<float*>(local);
+  e.nvls_mode = n->mode;
+  e.nvls_shard = nvls_shard_rows(e.rows, n->world);
   e.nvls_mc = static_cast<float*>(n->multicast);
   for (int r = 0; r < rl::NVLS_MAX_RANKS; ++r) e.nvls_flags[r] = n->flags[r];
   e.nvls_rank = n->rank;
@@ -96,6 +103,8 @@ rl_status check_nvls(const rl_nvls_reduce* n, const char* what) {
   for (int r = 0; r < n->world; ++r)
     if (!n->flags[r]) return fail(RL_ERR_INVALID_ARGUMENT, "%s: flags[%d] is NULL", what, r);
   if (n->epoch == 0) return fail(RL_ERR_INVALID_ARGUMENT, "%s: epoch must be > 0 (flags start at 0)", what);
+  if (n->mode != RL_NVLS_ALL_REDUCE && n->mode != RL_NVLS_REDUCE_SCATTER)
+    return fail(RL_ERR_INVALID_ARGUMENT, "%s: unknown mode %d", what, n->mode);
   return RL_OK;
 }
 

@@ -74,6 +74,7 @@ rl_status check_shape(const rl_lm_shape* s) {
 static_assert(sizeof(rl_lm_shape) == 56, "rl_lm_shape layout (binding mirrors it)");
 static_assert(sizeof(rl_loss_params) == 40, "rl_loss_params layout (binding mirrors it)");
 static_assert(sizeof(rl_loss_report) == 48, "rl_loss_report layout (binding mirrors it)");
+static_assert(sizeof(rl_nvls_reduce) == 96, "rl_nvls_reduce layout (binding mirrors it)");
 
 rl_status check_params(const rl_loss_params* p) {
   if (!p) return fail(RL_ERR_INVALID_ARGUMENT, "params is NULL");

@@ -22,7 +22,7 @@ import torch.distributed as dist
 
 from . import (RL_BWD_ALL, RL_BWD_DENSE, RL_BWD_DH, RL_BWD_DU, RL_BWD_DW, alloc_workspace, make_params,
                make_shape, rl_bwd_ex, rl_fwd_partials, rl_group_advantages, rl_last_launch_count, rl_logprob_fwd, rl_loss_coef,
-               rl_merge_partials, rl_nvls_flag_count, rl_nvls_reduce, rl_policy_loss_fwd_bwd, rl_workspace_bytes)
+               rl_merge_partials, rl_nvls_flag_count, rl_nvls_reduce, rl_nvls_shard_rows, rl_policy_loss_fwd_bwd, rl_workspace_bytes)
 
 
 class NvlsReduction:
@@ -47,7 +47,7 @@ class NvlsReduction:
         torch.cuda.synchronize(device)
         self.handle.barrier(channel=0)
 
-    def descriptor(self, lag=None) -> rl_nvls_reduce:
+    def descriptor(self, lag=None, mode=0) -> rl_nvls_reduce:
         """lag: the owner reduces a slab this many tiles after its own store of it
         (more lag = more slack for slower ranks; RL_NVLS_LAG, default 2)."""
         if lag is None:
@@ -57,7 +57,7 @@ class NvlsReduction:
         d.multicast = self.handle.multicast_ptr
         for r in range(self.world):
             d.flags[r] = self.flag_handle.buffer_ptrs[r]
-        d.rank, d.world, d.epoch, d.lag = self.rank, self.world, self.epoch, lag
+        d.rank, d.world, d.epoch, d.lag, d.mode = self.rank, self.world, self.epoch, lag, mode
         return d
 
     def barrier(self):
@@ -201,7 +201,7 @@ class DataParallelPolicyLoss:
     def __init__(self, phases, *, T, H, V, num_rollouts, group_size, loss_denominator, group=None,
                  inv_temperature=1.0, alpha=0.5, beta=5.0, guard=1e-5, device=None, d_hidden_dtype=torch.bfloat16,
                  workspace=True, overlap=False, comm_sms=24, nvls=False, variant="icepop", kl_tau=0.0,
-                 kl_set="masked", inv_temperature_rows=None):
+                 kl_set="masked", inv_temperature_rows=None, reduce_scatter=False):
         self.ph = phases
         # overlap: the dW all-reduce (NCCL, side stream) runs concurrently with K5,
         # which then uses all but `comm_sms` SMs (NCCL's NVLS channels need SMs).
@@ -232,6 +232,12 @@ class DataParallelPolicyLoss:
         # nvls: dW is all-reduced inside the K6 epilogue (NVLink multicast); the
         # step then returns the symmetric buffer that holds the sum.
         self.nvls = NvlsReduction(V, H, rl_nvls_flag_count(self.shape, 0), group, dev) if nvls else None
+        # reduce_scatter (NVLS only, FSDP-consistent): rank r ends with the summed dW rows
+        # [r S, (r+1) S) (S = rl_nvls_shard_rows); step() returns that shard
+        self.reduce_scatter = bool(reduce_scatter)
+        if self.reduce_scatter and not nvls:
+            raise ValueError("reduce_scatter needs nvls=True")
+        self.shard_rows = rl_nvls_shard_rows(V, self.world) if self.reduce_scatter else None
 
     @staticmethod
     def global_denominator(loss_mask: torch.Tensor, group=None) -> float:
@@ -247,8 +253,13 @@ class DataParallelPolicyLoss:
             ph.full_step(self.shape, self.params, hidden, w, targets, infer, self.adv, offsets, loss_mask,
                          report=self.report, logprob=self.logprob, entropy=self.entropy, lse=self.lse,
                          coef=self.coef, keep=self.keep, guarded=self.guarded, d_hidden=self.d_hidden,
-                         d_w_vocab=self.nvls.buf, d_w_vocab_nvls=self.nvls.descriptor(), workspace=self.ws)
+                         d_w_vocab=self.nvls.buf,
+                         d_w_vocab_nvls=self.nvls.descriptor(mode=1 if self.reduce_scatter else 0),
+                         workspace=self.ws)
             self.nvls.barrier()                                   # the exchange, fused into K6's epilogue
+            if self.reduce_scatter:
+                r = dist.get_rank(self.group)
+                return self.nvls.buf[r * self.shard_rows:(r + 1) * self.shard_rows]
             return self.nvls.buf
         if not self.overlap:
             ph.full_step(self.shape, self.params, hidden, w, targets, infer, self.adv, offsets, loss_mask,

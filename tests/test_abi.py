@@ -37,7 +37,7 @@ def test_struct_layouts_match_header(lib):
     assert ctypes.sizeof(rl.rl_loss_params) == 40
     assert ctypes.sizeof(rl.rl_loss_report) == 48
     assert ctypes.sizeof(rl.rl_loss_outputs) == 104
-    assert ctypes.sizeof(rl.rl_nvls_reduce) == 88
+    assert ctypes.sizeof(rl.rl_nvls_reduce) == 96
     assert lib.rl_abi_version() == 2
 
 

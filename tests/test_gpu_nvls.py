@@ -39,7 +39,7 @@ def _worker(rank, port, out_dir, mode):
     res = {}
     infer = None
     for nv in (False, False, True):
-        if mode == "dp":
+        if mode in ("dp", "dp_rs"):
             b = synth.make_batch_device(wl, 50 + rank, device=dev, tokens=T)
         else:
             Vl = wl.vocab // WORLD
@@ -49,11 +49,12 @@ def _worker(rank, port, out_dir, mode):
         lm = torch.from_numpy(b["loss_mask"]).to(dev)
         rw = torch.from_numpy(b["rewards"]).to(dev)
         inf = infer if infer is not None else torch.full((T,), -1.0, device=dev)
-        if mode == "dp":
+        if mode in ("dp", "dp_rs"):
             D = parallel.DataParallelPolicyLoss.global_denominator(lm)
             eng = parallel.DataParallelPolicyLoss(parallel.LibrlPhases(), T=T, H=wl.hidden, V=wl.vocab,
                                                   num_rollouts=wl.num_rollouts, group_size=wl.group_size,
-                                                  loss_denominator=D, device=dev, nvls=nv)
+                                                  loss_denominator=D, device=dev, nvls=nv,
+                                                  reduce_scatter=nv and mode == "dp_rs")
             dw = torch.empty(wl.vocab, wl.hidden, device=dev)
             out = eng.step(b["hidden"], b["w"], b["targets"], inf, rw, offs, lm, None if nv else dw)
         else:
@@ -82,3 +83,17 @@ def test_nvls_matches_nccl(tmp_path, mode):
         np.testing.assert_allclose(a, b, rtol=1e-5, atol=1e-6 * np.abs(b).max())
     d = [np.load(tmp_path / f"{mode}{r}.npz")["nvls"] for r in range(WORLD)]
     assert all(np.array_equal(d[0], x) for x in d[1:])   # one reduced value, written to every replica
+
+
+def test_nvls_reduce_scatter_matches_nccl_rows(tmp_path):
+    """FSDP-consistent mode: rank r's returned shard equals rows [r S, (r+1) S) of the
+    NCCL all-reduced dW (S = rl_nvls_shard_rows)."""
+    import paper_2512_16144_b200 as rl
+    mp.start_processes(_worker, args=(_port(), str(tmp_path), "dp_rs"), nprocs=WORLD, start_method="spawn")
+    for r in range(WORLD):
+        d = np.load(tmp_path / f"dp_rs{r}.npz")
+        full, shard = d["nccl"], d["nvls"]
+        S = rl.rl_nvls_shard_rows(full.shape[0], WORLD)
+        ref = full[r * S:(r + 1) * S]
+        assert shard.shape == ref.shape and np.abs(ref).max() > 0
+        np.testing.assert_allclose(shard, ref, rtol=1e-5, atol=1e-6 * np.abs(full).max())
