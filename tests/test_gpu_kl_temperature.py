@@ -112,3 +112,33 @@ def test_bad_kl_params_rejected():
     c.kl_tau, c.kl_set = 0.1, 7
     with pytest.raises(rl.RLError):
         harness.run_gpu_step(c)
+
+
+def test_hostio_slabs_with_per_token_temperature():
+    """The host-I/O call runs the forward slab by slab as the hidden rows arrive
+    (slab ends 1024, 4096, ...); the per-row temperature pointer is offset per slab.
+    Its outputs equal the device-resident call's bit for bit."""
+    wl = synth.Workload("slab", 4, 4, 320, 64, 512, ragged=True, delta_sigma=0.8, spike_rate=0.001)
+    T = 5000
+    invT = np.random.default_rng(9).uniform(0.6, 1.6, T).astype(np.float32).astype(np.float64)
+    c = harness.make_case(wl, 45, tokens=T, vocab=512, hidden=64, inv_temperature=invT)
+    c.kl_tau = 0.125
+    gdev = harness.run_gpu_step(c)
+    b = c.batch
+    H, V, R = b.H, b.V, len(c.adv)
+    d = harness.to_device(c)
+    invt = torch.from_numpy(invT.astype(np.float32)).cuda()
+    shape = rl.make_shape(T, H, V, inv_temperature_rows=invt)
+    params = rl.make_params(R, b.loss_denominator, kl_tau=0.125)
+    report = rl.new_report()
+    dh = torch.empty(T, H, dtype=torch.bfloat16, device="cuda")
+    dw = torch.empty(V, H, device="cuda")
+    pin = lambda x: torch.from_numpy(np.ascontiguousarray(x)).pin_memory()  # noqa: E731
+    rep = rl.rl_policy_loss_fwd_bwd_hostio(
+        shape, params, b.wl.group_size, pin(b.hidden.view(np.int16)), d["w"], pin(b.targets), pin(c.infer),
+        pin(b.rewards.reshape(-1)), pin(b.rollout_offsets), pin(b.loss_mask), report=report, d_hidden=dh,
+        d_w_vocab=dw)
+    assert rep.as_dict() == gdev["report"]
+    assert np.array_equal(dh.float().cpu().numpy(), gdev["d_hidden"])
+    assert np.array_equal(dw.cpu().numpy(), gdev["d_w_vocab"])
+    harness.compare(c, harness.run_oracle(c), gdev)
