@@ -407,6 +407,21 @@ def main_ours(args):
     peaks, peak_src = load_peaks()
     peak = float(peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops")))
     achieved = flops[dom] / (kern[dom]["avg_ms"] / 1e3) / 1e12
+    # every kernel against its own roofline: the GEMMs in TF/s, the HBM-side kernels in
+    # GB/s of algorithmic bytes (K2: the [tiles x T] float4 partials + 3 outputs; the
+    # compaction group: gather + scatter of the kept rows, 2 x read+write of n x H bf16)
+    hbm_peak = float(peaks.get("hbm_gbs", 6459.3))
+    n_tiles = -(-V_local // 256)
+    hbm_bytes = {"K2_merge": 16.0 * n_tiles * T + 12.0 * T,
+                 "compact": (8.0 * bwd_rows * H + 4.0 * T) if not dense else 0.0}
+    for k, v in kern.items():
+        if k in flops:
+            v["tflops"] = flops[k] / (v["avg_ms"] / 1e3) / 1e12
+            v["frac_of_sustained_bf16"] = v["tflops"] / peak
+        elif k in hbm_bytes and hbm_bytes[k] > 0:
+            per_launch = hbm_bytes[k] / (v["launches"] / args.steps)
+            v["gbs"] = per_launch / (v["avg_ms"] / 1e3) / 1e9
+            v["frac_of_hbm"] = v["gbs"] / hbm_peak
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):
