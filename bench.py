@@ -566,7 +566,8 @@ def main_ours(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=40,
+                    help="timed steps (40 x ~60 ms: >= 2 s back to back, so the clock reaches its sustained power-capped state)")
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="auto", choices=["auto", "small", "glm16k", "glm64k", "stress"])
