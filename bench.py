@@ -210,7 +210,10 @@ def reference_arm(args):
         threadpool_limits(os.cpu_count())
     except Exception:  # noqa: BLE001
         pass
-    b, h64, w64, infer = oracle_sample(wl, args.ref_tokens)
+    # tokens per reference step: 256, or 64 when many steps are asked for (each step also
+    # pays a fixed ~1-2 s for the fp64 [V, H] dW), so K + W steps end within minutes
+    ref_tokens = args.ref_tokens or (256 if args.steps + args.warmup <= 43 else 64)
+    b, h64, w64, infer = oracle_sample(wl, ref_tokens)
     for _ in range(args.warmup):
         run_oracle_step(b, h64, w64, infer)
     times = []
@@ -574,7 +577,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
-    ap.add_argument("--ref-tokens", type=int, default=256)
+    ap.add_argument("--ref-tokens", type=int, default=0, help="reference arm: tokens per step (0 = 256, or 64 for > 40 steps)")
     ap.add_argument("--dense-backward", action="store_true",
                     help="run the backward GEMMs over all rows instead of the coef != 0 rows (A/B)")
     ap.add_argument("--dw-reduce-scatter", action="store_true",
