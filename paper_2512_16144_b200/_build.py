@@ -8,13 +8,16 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "librl.so")
 SOURCES = ["rl_api.cu"]
-DEPS = ["rl_api.cu", "rl_gemm.cuh", "rl_ptx.cuh", "rl_small.cuh"]
+# every source and header of the library (the host side is split over several .cuh)
+DEPS = sorted(f for f in os.listdir(CSRC) if f.endswith((".cu", ".cuh")))
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC",
     "-cudart", "static", "-Xptxas", "-v",
 ]
+# extra -D flags for A/B builds (RL_NVCC_DEFINES="-DFOO=1 ..."); empty for the product build
+EXTRA = os.environ.get("RL_NVCC_DEFINES", "").split()
 
 
 def _stale():
@@ -29,7 +32,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
         return LIB
     nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-    cmd = [nvcc, *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"),
+    cmd = [nvcc, *NVCC_FLAGS, *EXTRA, "-I", os.path.join(ROOT, "include"),
            *[os.path.join(CSRC, s) for s in SOURCES], "-o", LIB + ".tmp"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
