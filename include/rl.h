@@ -307,6 +307,24 @@ rl_status rl_newton_schulz(const float* g, int64_t M, int64_t N, int32_t steps, 
                            size_t workspace_bytes, void* stream);
 size_t rl_newton_schulz_workspace_bytes(int64_t M, int64_t N);
 
+/* The same Newton-Schulz with G row-sharded across ranks (tall: the rows of
+ * d_w_vocab, e.g. after the NVLS reduce-scatter; P:L179-181 distributed Muon).
+ * X^T X = sum over ranks of X_r^T X_r, so the ranks only exchange an N x N Gram
+ * per iteration and one scalar; each rank updates its own rows (X_r <- X_r C).
+ * The caller runs, with G_r [M_local, N] fp32 and the same workspace throughout:
+ *   rl_ns_shard_sumsq(G_r -> sumsq[1] fp64)          then all-reduce(sumsq, SUM)
+ *   for j in 0..steps-1:
+ *     rl_ns_shard_gram(j, G_r, sumsq -> gram [N, N] fp32)  then all-reduce(gram, SUM)
+ *     rl_ns_shard_apply(j, steps, gram -> out_r [M_local, N] bf16 on the last j)
+ * (j = 0 also forms X_0 = bf16(G_r / (sqrt(sumsq) + 1e-7))). Requires M_local >= N;
+ * workspace: rl_newton_schulz_workspace_bytes(M_local, N). */
+rl_status rl_ns_shard_sumsq(const float* g, int64_t M_local, int64_t N, double* sumsq, void* workspace,
+                            size_t workspace_bytes, void* stream);
+rl_status rl_ns_shard_gram(int32_t j, const float* g, const double* sumsq, int64_t M_local, int64_t N,
+                           float* gram, void* workspace, size_t workspace_bytes, void* stream);
+rl_status rl_ns_shard_apply(int32_t j, int32_t steps, const float* gram, int64_t M_local, int64_t N,
+                            uint16_t* out, void* workspace, size_t workspace_bytes, void* stream);
+
 /* One Muon update of an fp32 parameter matrix theta [M, N] (reading R18):
  *   m <- mu m + g;  u = nesterov ? g + mu m : m;
  *   theta <- theta (1 - lr wd) - lr sqrt(max(1, M/N)) NS_steps(u).

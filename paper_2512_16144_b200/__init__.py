@@ -116,6 +116,11 @@ _SIGS = {
     "rl_newton_schulz": (ctypes.c_int, [_P, ctypes.c_int64, ctypes.c_int64, ctypes.c_int32, _P, _P,
                                         ctypes.c_size_t, _P]),
     "rl_newton_schulz_workspace_bytes": (ctypes.c_size_t, [ctypes.c_int64, ctypes.c_int64]),
+    "rl_ns_shard_sumsq": (ctypes.c_int, [_P, ctypes.c_int64, ctypes.c_int64, _P, _P, ctypes.c_size_t, _P]),
+    "rl_ns_shard_gram": (ctypes.c_int, [ctypes.c_int32, _P, _P, ctypes.c_int64, ctypes.c_int64, _P, _P,
+                                        ctypes.c_size_t, _P]),
+    "rl_ns_shard_apply": (ctypes.c_int, [ctypes.c_int32, ctypes.c_int32, _P, ctypes.c_int64, ctypes.c_int64, _P,
+                                         _P, ctypes.c_size_t, _P]),
     "rl_muon_step": (ctypes.c_int, [_P, _P, _P, ctypes.c_int64, ctypes.c_int64, ctypes.c_float, ctypes.c_float,
                                     ctypes.c_float, ctypes.c_int32, ctypes.c_int32, _P, ctypes.c_size_t, _P]),
     "rl_muon_workspace_bytes": (ctypes.c_size_t, [ctypes.c_int64, ctypes.c_int64]),
@@ -378,6 +383,27 @@ def rl_newton_schulz(g: torch.Tensor, steps: int = 5, out: torch.Tensor | None =
     _check(load_library().rl_newton_schulz(_ptr(g), M, N, int(steps), _ptr(out), _ptr(ws), ws.numel(),
                                            _stream(stream)))
     return out
+
+
+def rl_ns_shard_sumsq(g: torch.Tensor, sumsq: torch.Tensor, workspace, stream=None):
+    """Row-sharded Newton-Schulz, phase 0: sumsq[0] = sum of g^2 over this shard (fp64)."""
+    M, N = g.shape
+    _check(load_library().rl_ns_shard_sumsq(_ptr(g), M, N, _ptr(sumsq), _ptr(workspace), workspace.numel(),
+                                            _stream(stream)))
+
+
+def rl_ns_shard_gram(j: int, g: torch.Tensor, sumsq: torch.Tensor, gram: torch.Tensor, workspace, stream=None):
+    """Iteration j: (j = 0: X_0 from g and the global sumsq) gram = X_r^T X_r (fp32 [N, N])."""
+    M, N = g.shape
+    _check(load_library().rl_ns_shard_gram(int(j), _ptr(g), _ptr(sumsq), M, N, _ptr(gram), _ptr(workspace),
+                                           workspace.numel(), _stream(stream)))
+
+
+def rl_ns_shard_apply(j: int, steps: int, gram: torch.Tensor, M_local: int, N: int, out: torch.Tensor | None,
+                      workspace, stream=None):
+    """Iteration j with the all-reduced gram: X_r <- X_r (aI + bA + cA^2); out on the last j."""
+    _check(load_library().rl_ns_shard_apply(int(j), int(steps), _ptr(gram), int(M_local), int(N), _ptr(out),
+                                            _ptr(workspace), workspace.numel(), _stream(stream)))
 
 
 def rl_muon_step(theta: torch.Tensor, grad: torch.Tensor, momentum: torch.Tensor, lr: float, mu: float = 0.95,

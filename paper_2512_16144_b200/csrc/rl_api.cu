@@ -469,6 +469,64 @@ rl_status rl_newton_schulz(const float* g, int64_t M, int64_t N, int32_t steps, 
   return ns_impl(g, M, N, steps, out, static_cast<uint8_t*>(workspace), l, d.sms, static_cast<cudaStream_t>(stream));
 }
 
+static rl_status ns_shard_check(int64_t M, int64_t N, int32_t steps, void* workspace, size_t workspace_bytes,
+                                NsLayout& l, DevInfo& d) {
+  RL_TRY(check_ns_shape(M, N, steps));
+  if (M < N) return fail(RL_ERR_SHAPE, "row-sharded Newton-Schulz needs M_local >= N (tall shards)");
+  if (!aligned16(workspace)) return fail(RL_ERR_ALIGNMENT, "workspace must be 16-byte aligned");
+  l = ns_layout(M, N, false);
+  if (!workspace || workspace_bytes < l.end)
+    return fail(RL_ERR_WORKSPACE, "workspace needs %zu bytes, got %zu", l.end, workspace_bytes);
+  return device_info(d);
+}
+
+rl_status rl_ns_shard_sumsq(const float* g, int64_t M_local, int64_t N, double* sumsq, void* workspace,
+                            size_t workspace_bytes, void* stream) {
+  g_launches = 0;
+  RL_NONNULL(g);
+  RL_NONNULL(sumsq);
+  if (!aligned16(g)) return fail(RL_ERR_ALIGNMENT, "g must be 16-byte aligned");
+  NsLayout l;
+  DevInfo d;
+  RL_TRY(ns_shard_check(M_local, N, 1, workspace, workspace_bytes, l, d));
+  return ns_shard_sumsq_impl(g, M_local, N, sumsq, static_cast<uint8_t*>(workspace), l,
+                             static_cast<cudaStream_t>(stream));
+}
+
+rl_status rl_ns_shard_gram(int32_t j, const float* g, const double* sumsq, int64_t M_local, int64_t N, float* gram,
+                           void* workspace, size_t workspace_bytes, void* stream) {
+  g_launches = 0;
+  RL_NONNULL(gram);
+  if (j < 0) return fail(RL_ERR_INVALID_ARGUMENT, "iteration j must be >= 0");
+  if (j == 0) {
+    RL_NONNULL(g);
+    RL_NONNULL(sumsq);
+    if (!aligned16(g)) return fail(RL_ERR_ALIGNMENT, "g must be 16-byte aligned");
+  }
+  if (!aligned16(gram)) return fail(RL_ERR_ALIGNMENT, "gram must be 16-byte aligned");
+  NsLayout l;
+  DevInfo d;
+  RL_TRY(ns_shard_check(M_local, N, 1, workspace, workspace_bytes, l, d));
+  return ns_shard_gram_impl(j, g, sumsq, M_local, N, gram, static_cast<uint8_t*>(workspace), l, d.sms,
+                            static_cast<cudaStream_t>(stream));
+}
+
+rl_status rl_ns_shard_apply(int32_t j, int32_t steps, const float* gram, int64_t M_local, int64_t N, uint16_t* out,
+                            void* workspace, size_t workspace_bytes, void* stream) {
+  g_launches = 0;
+  RL_NONNULL(gram);
+  if (j < 0 || j >= steps) return fail(RL_ERR_INVALID_ARGUMENT, "need 0 <= j < steps");
+  if (j == steps - 1) {
+    RL_NONNULL(out);
+    if (!aligned16(out)) return fail(RL_ERR_ALIGNMENT, "out must be 16-byte aligned");
+  }
+  NsLayout l;
+  DevInfo d;
+  RL_TRY(ns_shard_check(M_local, N, steps, workspace, workspace_bytes, l, d));
+  return ns_shard_apply_impl(j, steps, gram, M_local, N, out, static_cast<uint8_t*>(workspace), l, d.sms,
+                             static_cast<cudaStream_t>(stream));
+}
+
 rl_status rl_muon_step(float* theta, const float* grad, float* momentum, int64_t M, int64_t N, float lr, float mu,
                        float weight_decay, int32_t nesterov, int32_t steps, void* workspace, size_t workspace_bytes,
                        void* stream) {

@@ -123,6 +123,94 @@ rl_status ns_impl(const float* g, int64_t M, int64_t N, int32_t steps, uint16_t*
   return RL_OK;
 }
 
+// Row-sharded Newton-Schulz (tall): the phases of ns_impl between which the caller
+// all-reduces the sum of squares and the Gram. X_j lives in xa (j even) / xb (j odd).
+rl_status ns_shard_sumsq_impl(const float* g, int64_t M, int64_t N, double* sumsq, uint8_t* ws, const NsLayout& l,
+                              cudaStream_t st) {
+  double* partials = reinterpret_cast<double*>(ws + l.partials);
+  {
+    ProfScope ps(RL_K_NS_AUX, st);
+    rl::sumsq_partial_kernel<<<kNsPartials, 256, 0, st>>>(g, M * N, partials);
+  }
+  RL_CHECK_LAUNCH();
+  {
+    ProfScope ps(RL_K_NS_AUX, st);
+    rl::sum_partials_kernel<<<1, 256, 0, st>>>(partials, kNsPartials, sumsq);
+  }
+  RL_CHECK_LAUNCH();
+  return RL_OK;
+}
+
+rl_status ns_shard_gram_impl(int j, const float* g, const double* sumsq, int64_t M, int64_t N, float* gram, uint8_t* ws,
+                             const NsLayout& l, int sms, cudaStream_t st) {
+  const int64_t K = l.K;  // = N (tall shard)
+  uint16_t* xa = reinterpret_cast<uint16_t*>(ws + l.xa);
+  uint16_t* xb = reinterpret_cast<uint16_t*>(ws + l.xb);
+  uint16_t* g16 = reinterpret_cast<uint16_t*>(ws + l.g16);
+  g_sync_ctr = reinterpret_cast<uint32_t*>(ws + l.sync);
+  if (j == 0) {
+    ProfScope ps(RL_K_NS_AUX, st);
+    // the global sum of squares as a single "partial": every block reads the same value
+    rl::ns_prep_kernel<<<8 * sms, 256, 0, st>>>(g, M * N, sumsq, 1, xa);
+  }
+  RL_CHECK_LAUNCH();
+  uint16_t* src = (j % 2 == 0) ? xa : xb;
+  float* parts = reinterpret_cast<float*>(ws + l.parts);
+  CUtensorMap t_xm, t_g32;
+  RL_TRY(make_map(&t_xm, src, false, N, M, N, 64, 64));
+  RL_TRY(make_map(&t_g32, parts, true, K, K * l.splits, K, 32, 32));
+  rl::EpiParams e = {};
+  e.rows = K;
+  e.cols = K;
+  RL_TRY((launch_gemm<rl::EPI_F32, true, true>(RL_K_NS_GEMM, t_xm, t_xm, t_g32, N, N, M, 8, e, sms, st, l.splits,
+                                               static_cast<int>(K))));
+  {
+    ProfScope ps(RL_K_NS_AUX, st);
+    rl::split_reduce_cast_kernel<<<8 * sms, 256, 0, st>>>(parts, l.splits, K * K, gram, g16);
+  }
+  RL_CHECK_LAUNCH();
+  return RL_OK;
+}
+
+rl_status ns_shard_apply_impl(int j, int steps, const float* gram, int64_t M, int64_t N, uint16_t* out, uint8_t* ws,
+                              const NsLayout& l, int sms, cudaStream_t st) {
+  constexpr float ca = 3.4445f, cb = -4.7750f, cc = 2.0315f;
+  const int64_t K = l.K;
+  uint16_t* xa = reinterpret_cast<uint16_t*>(ws + l.xa);
+  uint16_t* xb = reinterpret_cast<uint16_t*>(ws + l.xb);
+  uint16_t* g16 = reinterpret_cast<uint16_t*>(ws + l.g16);
+  float* g2 = reinterpret_cast<float*>(ws + l.g2);
+  uint16_t* c16 = reinterpret_cast<uint16_t*>(ws + l.c16);
+  g_sync_ctr = reinterpret_cast<uint32_t*>(ws + l.sync);
+  uint16_t* src = (j % 2 == 0) ? xa : xb;
+  uint16_t* dst = (j == steps - 1) ? out : ((j % 2 == 0) ? xb : xa);
+  {
+    ProfScope ps(RL_K_NS_AUX, st);
+    rl::cast_bf16_kernel<<<8 * sms, 256, 0, st>>>(gram, K * K, g16);   // the all-reduced Gram
+  }
+  RL_CHECK_LAUNCH();
+  CUtensorMap t_g16k, t_g16m, t_g2, t_c16m, t_xk, t_out;
+  RL_TRY(make_map(&t_g16k, g16, false, K, K, K, 64, kARows));
+  RL_TRY(make_map(&t_g16m, g16, false, K, K, K, 64, 64));
+  RL_TRY(make_map(&t_g2, g2, true, K, K, K, 32, 32));
+  RL_TRY(make_map(&t_c16m, c16, false, K, K, K, 64, 64));
+  RL_TRY(make_map(&t_xk, src, false, N, M, N, 64, kARows));
+  RL_TRY(make_map(&t_out, dst, false, N, M, N, 64, 32));
+  rl::EpiParams e = {};
+  e.rows = K;
+  e.cols = K;
+  RL_TRY((launch_gemm<rl::EPI_F32, false, true>(RL_K_NS_GEMM, t_g16k, t_g16m, t_g2, K, K, K, 8, e, sms, st)));
+  {
+    ProfScope ps(RL_K_NS_AUX, st);
+    rl::ns_poly_kernel<<<8 * sms, 256, 0, st>>>(gram, g2, K, ca, cb, cc, c16);
+  }
+  RL_CHECK_LAUNCH();
+  e.rows = M;
+  e.cols = N;
+  RL_TRY((launch_gemm<rl::EPI_BF16, false, true>(RL_K_NS_GEMM, t_xk, t_c16m, t_out, M, N, N, 8, e, sms, st)));
+  return RL_OK;
+}
+
 // Side stream + events of the host-I/O call (per host thread and device).
 struct HostioStreams {
   int dev = -1;

@@ -508,6 +508,15 @@ __global__ void ns_prep_kernel(const float* __restrict__ g, int64_t n, const dou
     x0[i] = f32_to_bf16_bits(g[i] * s);
 }
 
+// out[0] = fixed-order sum of n fp64 partials (one block)
+__global__ void sum_partials_kernel(const double* __restrict__ partials, int n, double* __restrict__ out) {
+  __shared__ double sh[256];
+  double p = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) p += partials[i];
+  const double t = block_reduce_sum(p, sh);
+  if (threadIdx.x == 0) out[0] = t;
+}
+
 __global__ void cast_bf16_kernel(const float* __restrict__ a, int64_t n, uint16_t* __restrict__ out) {
   for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x)

@@ -22,7 +22,8 @@ import torch.distributed as dist
 
 from . import (RL_BWD_ALL, RL_BWD_DENSE, RL_BWD_DH, RL_BWD_DU, RL_BWD_DW, alloc_workspace, make_params,
                make_shape, rl_bwd_ex, rl_fwd_partials, rl_group_advantages, rl_last_launch_count, rl_logprob_fwd, rl_loss_coef,
-               rl_merge_partials, rl_nvls_flag_count, rl_nvls_reduce, rl_nvls_shard_rows, rl_policy_loss_fwd_bwd, rl_workspace_bytes)
+               rl_merge_partials, rl_ns_shard_apply, rl_ns_shard_gram, rl_ns_shard_sumsq,
+               rl_nvls_flag_count, rl_nvls_reduce, rl_nvls_shard_rows, rl_policy_loss_fwd_bwd, rl_workspace_bytes)
 
 
 class NvlsReduction:
@@ -78,6 +79,19 @@ class LibrlPhases:
 
     def group_advantages(self, rewards, group_size, adv):
         rl_group_advantages(rewards, group_size, adv)
+        self._count()
+
+    # row-sharded Newton-Schulz (newton_schulz_row_sharded)
+    def ns_sumsq(self, g, sumsq, workspace):
+        rl_ns_shard_sumsq(g, sumsq, workspace)
+        self._count()
+
+    def ns_gram(self, j, g, sumsq, gram, workspace):
+        rl_ns_shard_gram(j, g, sumsq, gram, workspace)
+        self._count()
+
+    def ns_apply(self, j, steps, gram, M_local, N, out, workspace):
+        rl_ns_shard_apply(j, steps, gram, M_local, N, out, workspace)
         self._count()
 
     def fwd_partials(self, shape, hidden, w_shard, targets, partials, workspace=None):
@@ -283,3 +297,27 @@ class DataParallelPolicyLoss:
                       max_sms=self.dh_sms, workspace=self.ws)
         main.wait_stream(self.comm)
         return d_w_vocab
+
+
+def newton_schulz_row_sharded(phases, g_shard, steps=5, group=None, workspace=None, out=None):
+    """Muon's Newton-Schulz on a tall matrix whose rows are sharded across `group`
+    (e.g. d_w_vocab after the NVLS reduce-scatter): X^T X is the sum of
+    the ranks' X_r^T X_r, so per iteration the ranks all-reduce one N x N fp32 Gram
+    (and once the sum of squares for ||G||_F) and each updates its own rows. Returns
+    this rank's rows of NS(G) in bf16; with one rank it equals rl_newton_schulz."""
+    M, N = g_shard.shape
+    dev = g_shard.device
+    if workspace is None and dev.type == "cuda":
+        from . import load_library
+        workspace = alloc_workspace(load_library().rl_newton_schulz_workspace_bytes(M, N), dev)
+    sumsq = torch.zeros(1, dtype=torch.float64, device=dev)
+    gram = torch.empty(N, N, dtype=torch.float32 if dev.type == "cuda" else torch.float64, device=dev)
+    if out is None:
+        out = torch.empty(M, N, dtype=torch.bfloat16 if dev.type == "cuda" else torch.float64, device=dev)
+    phases.ns_sumsq(g_shard, sumsq, workspace)
+    dist.all_reduce(sumsq, group=group)                                   # ||G||_F^2
+    for j in range(steps):
+        phases.ns_gram(j, g_shard, sumsq, gram, workspace)
+        dist.all_reduce(gram, group=group)                                # the N x N Gram
+        phases.ns_apply(j, steps, gram, M, N, out, workspace)
+    return out

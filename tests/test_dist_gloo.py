@@ -14,6 +14,7 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 import oracle
+import oracle.muon
 import synth
 from paper_2512_16144_b200 import parallel
 
@@ -89,6 +90,23 @@ class OraclePhases:
         d_hidden.copy_(torch.from_numpy(res.d_hidden))
         d_w_vocab.copy_(torch.from_numpy(res.d_w_vocab))
         self.loss = res.report.loss
+
+
+    # row-sharded Newton-Schulz (fp64, the oracle's quintic)
+    def ns_sumsq(self, g, sumsq, workspace):
+        sumsq.fill_(float((g.double() ** 2).sum()))
+
+    def ns_gram(self, j, g, sumsq, gram, workspace):
+        if j == 0:
+            self.X = g.double().numpy() / (np.sqrt(float(sumsq[0])) + oracle.muon.NS_EPS)
+        gram.copy_(torch.from_numpy(self.X.T @ self.X))
+
+    def ns_apply(self, j, steps, gram, M_local, N, out, workspace):
+        a, b, c = oracle.muon.NS_COEFFS
+        A = gram.double().numpy()
+        self.X = self.X @ (a * np.eye(N) + b * A + c * (A @ A))
+        if j == steps - 1:
+            out.copy_(torch.from_numpy(self.X))
 
 
 WL = synth.Workload("dist", 2, 4, 12, 32, 96, ragged=True, prompt_frac=0.2, delta_sigma=0.8, spike_rate=0.02)
@@ -184,3 +202,22 @@ def test_data_parallel_composition(tmp_path, kw_i):
         np.testing.assert_allclose(o["dw"], ref.d_w_vocab, atol=1e-12)   # all-reduced dW
         np.testing.assert_allclose(o["dh"], ref.d_hidden[int(o["t0"]):int(o["t1"])], atol=1e-12)
         assert float(o["loss"][0]) == pytest.approx(ref.report.loss, abs=1e-12)
+
+
+def _ns_worker(rank, port, out_dir):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=WORLD)
+    G = np.random.default_rng(3).standard_normal((96, 16))
+    rows = np.array_split(np.arange(96), WORLD)[rank]
+    out = parallel.newton_schulz_row_sharded(OraclePhases(), torch.from_numpy(G[rows].copy()), steps=5)
+    np.save(os.path.join(out_dir, f"ns{rank}.npy"), out.numpy())
+    dist.destroy_process_group()
+
+
+def test_row_sharded_newton_schulz_composition(tmp_path):
+    """Sharding rows and all-reducing the Gram (and ||G||^2) is Newton-Schulz of the
+    full matrix: X^T X = sum_r X_r^T X_r (oracle.newton_schulz, fp64)."""
+    mp.start_processes(_ns_worker, args=(_free_port(), str(tmp_path)), nprocs=WORLD, start_method="spawn")
+    got = np.concatenate([np.load(tmp_path / f"ns{r}.npy") for r in range(WORLD)])
+    G = np.random.default_rng(3).standard_normal((96, 16))
+    np.testing.assert_allclose(got, oracle.muon.newton_schulz(G, 5), rtol=0, atol=1e-12)
