@@ -74,7 +74,7 @@ int group_m_for(int kid, int dflt) {
 }
 
 // Soft k-barrier between producers (see EpiParams::sync_*): every RL_SYNC_EVERY
-// k-blocks (default 32; 0 = off), at most RL_SYNC_SLACK sync points of lead
+// k-blocks (default 32, 16 for the wide dH/dW GEMMs; 0 = off), at most RL_SYNC_SLACK sync points of lead
 // (default 2). Keeping the CTAs that share operands inside one L2 window cuts
 // K5/K6 DRAM reads by ~1/3 and lets the power-capped clock rise (~6% per step,
 // profiles/r01/). Correctness never depends on it (the wait is bounded).
@@ -101,7 +101,10 @@ int sync_every_for(int kid) {
   static bool init[32] = {};
   if (kid < 0 || kid >= 32) return 0;
   if (!init[kid]) {
-    cache[kid] = env_int("RL_SYNC_EVERY", kid, 32);
+    // 16 for the wide dH / dW GEMMs (their 48 KB k-blocks move twice the bytes per
+    // window): DRAM reads 23.4 -> 17.3 GB each, step 60.7 -> 59.6 ms
+    // (profiles/r01/sync_window_ab/); 32 elsewhere
+    cache[kid] = env_int("RL_SYNC_EVERY", kid, (kid == RL_K_DH_GEMM || kid == RL_K_DW_GEMM) ? 16 : 32);
     init[kid] = true;
   }
   return cache[kid];
