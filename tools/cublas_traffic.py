@@ -1,3 +1,6 @@
+"""The three step-GEMM shapes on cuBLAS (torch.matmul, bf16) at the GLM-16k shape, for an ncu
+comparison of L2->SM / DRAM traffic with librl (profiles/r01/ncu_full_cublas_gemms.md).
+usage: ncu --set full -k regex:"^(?!.*(elementwise|distribution)).*" -c 3 python tools/cublas_traffic.py"""
 import torch
 T,H,V=16384,4096,151552
 g=torch.Generator(device="cuda").manual_seed(0)
