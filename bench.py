@@ -236,24 +236,28 @@ def reference_arm(args):
 
 
 # ------------------------------------------------------------------ our arm
-def main_ours(args):
+def _setup(args):
+    """Process group, collective, per-rank workload and its synthetic batch."""
+    import types
+
     import torch
     import torch.distributed as dist
 
     import paper_2512_16144_b200 as rl
     import synth
 
-    rank, world, local = env_rank()
-    if world != args.gpus:
-        args.gpus = world
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    if world > 1:
+    r = types.SimpleNamespace()
+    r.rank, r.world, r.local = env_rank()
+    if r.world != args.gpus:
+        args.gpus = r.world
+    torch.cuda.set_device(r.local)
+    r.dev = dev = torch.device("cuda", r.local)
+    if r.world > 1:
         dist.init_process_group("nccl", device_id=dev)
-    name, wl = workload_for(args, world)
+    r.name, r.wl = workload_for(args, r.world)
     if args.collective == "auto":
         args.collective = "nccl"
-        if world > 1:
+        if r.world > 1:
             import torch.distributed._symmetric_memory as symm_mem
             try:
                 probe = symm_mem.empty(1024, dtype=torch.float32, device=dev)
@@ -263,145 +267,167 @@ def main_ours(args):
                 args.collective = "nvls" if ok.item() else "nccl"
             except Exception:  # noqa: BLE001 - no symmetric memory / multicast here: NCCL
                 args.collective = "nccl"
-    vocab_par = name == "glm64k" and world > 1
-    mode = "vocab" if vocab_par else "dp"
-    H, Vt = wl.hidden, wl.vocab
-    if name == "stress":
+    r.vocab_par = r.name == "glm64k" and r.world > 1
+    r.mode = "vocab" if r.vocab_par else "dp"
+    r.H, r.Vt = r.wl.hidden, r.wl.vocab
+    if r.name == "stress":
         # 16k tokens and one G=16 prompt group per rank (the guard and advantages stay local)
-        T = wl.tokens // wl.n_ranks
-        wl_rank = synth.Workload("stress-rank", 1, wl.group_size, wl.rollout_len, H, Vt,
-                                 delta_sigma=wl.delta_sigma, spike_rate=wl.spike_rate)
+        r.T = r.wl.tokens // r.wl.n_ranks
+        r.wl_rank = synth.Workload("stress-rank", 1, r.wl.group_size, r.wl.rollout_len, r.H, r.Vt,
+                                   delta_sigma=r.wl.delta_sigma, spike_rate=r.wl.spike_rate)
     else:
-        T = wl.tokens
-        wl_rank = wl
-    if vocab_par:
-        assert Vt % world == 0
-        V_local, v_off = Vt // world, rank * (Vt // world)
+        r.T = r.wl.tokens
+        r.wl_rank = r.wl
+    if r.vocab_par:
+        assert r.Vt % r.world == 0
+        r.V_local, r.v_off = r.Vt // r.world, r.rank * (r.Vt // r.world)
     else:
-        V_local, v_off = Vt, 0
-    seed = 1000 + (0 if vocab_par else rank)
-    b = synth.make_batch_device(wl_rank, seed, device=dev, tokens=T, vocab=V_local, vocab_offset=v_off,
-                                vocab_total=Vt)
-    R = len(b["offsets"]) - 1
-    shape = rl.make_shape(T, H, V_local, v_off, Vt)
-    f32 = dict(dtype=torch.float32, device=dev)
-    targets = b["targets"]
-    offsets = torch.from_numpy(b["offsets"]).to(dev)
-    loss_mask = torch.from_numpy(b["loss_mask"]).to(dev)
-    rewards = torch.from_numpy(b["rewards"]).to(dev)
-    D_local = float(b["loss_mask"].sum())
-    if world > 1 and not vocab_par:
-        t = torch.tensor([D_local], dtype=torch.float64, device=dev)
+        r.V_local, r.v_off = r.Vt, 0
+    seed = 1000 + (0 if r.vocab_par else r.rank)
+    r.b = b = synth.make_batch_device(r.wl_rank, seed, device=dev, tokens=r.T, vocab=r.V_local,
+                                      vocab_offset=r.v_off, vocab_total=r.Vt)
+    r.R = len(b["offsets"]) - 1
+    r.shape = rl.make_shape(r.T, r.H, r.V_local, r.v_off, r.Vt)
+    r.targets = b["targets"]
+    r.offsets = torch.from_numpy(b["offsets"]).to(dev)
+    r.loss_mask = torch.from_numpy(b["loss_mask"]).to(dev)
+    r.rewards = torch.from_numpy(b["rewards"]).to(dev)
+    D = float(b["loss_mask"].sum())
+    if r.world > 1 and not r.vocab_par:
+        t = torch.tensor([D], dtype=torch.float64, device=dev)
         dist.all_reduce(t)
         D = float(t.item())
-    else:
-        D = D_local
-    params = rl.make_params(R, D)
-
-    # stored inference log-probs: the trainer's own log-prob minus the drawn mismatch
-    logp_ref = torch.empty(T, **f32)
-    if vocab_par:
-        parts = torch.empty(world, T, 4, **f32)
-        ws0 = rl.alloc_workspace(rl.rl_workspace_bytes(shape, R, 16384), dev)
-        rl.rl_fwd_partials(shape, b["hidden"], b["w"], targets, parts[rank], workspace=ws0)
-        dist.all_gather_into_tensor(parts, parts[rank].contiguous())
-        rl.rl_merge_partials(parts, world, T, logp_ref)
-        del ws0
-    else:
-        rl.rl_logprob_fwd(shape, b["hidden"], b["w"], targets, logp_ref)
-    infer = torch.clamp(logp_ref - b["delta"], max=0.0)
-    infer = torch.where(b["spikes"], torch.zeros_like(infer), infer).contiguous()
-    del logp_ref
-
-    from paper_2512_16144_b200 import parallel
-    phases = parallel.LibrlPhases(dense_backward=args.dense_backward)
-    adv = torch.empty(R, **f32)
-    report = rl.new_report(dev)
-    logprob = torch.empty(T, **f32)
-    lse = torch.empty(T, **f32)
-    coef = torch.empty(T, **f32)
-    dw = torch.empty(V_local, H, **f32)
+    r.D = D
+    r.params = rl.make_params(r.R, D)
     # dU in 16k-row chunks: keeps K5/K6's per-wave working set inside L2 (the K = T
     # reduction of K6 at 64k rows loses ~20% to HBM re-reads otherwise)
-    chunk = 0 if T <= 16384 else 16384
-    if vocab_par:
-        nv = args.collective == "nvls"
-        engine = parallel.VocabParallelPolicyLoss(phases, T=T, H=H, V_global=Vt, num_rollouts=R,
-                                                  group_size=wl_rank.group_size, loss_denominator=D,
-                                                  dz_chunk_rows=0 if nv else chunk, device=dev, nvls=nv)
-        ws = engine.ws
-        dh = engine.d_hidden
-    elif world > 1:
-        engine = parallel.DataParallelPolicyLoss(phases, T=T, H=H, V=Vt, num_rollouts=R,
-                                                 group_size=wl_rank.group_size, loss_denominator=D, device=dev,
-                                                 overlap=args.overlap, comm_sms=args.comm_sms,
-                                                 nvls=args.collective == "nvls",
-                                                 reduce_scatter=args.dw_reduce_scatter and args.collective == "nvls")
-        ws = engine.ws
-        dh = engine.d_hidden
-    else:
-        engine = None
-        ws = rl.alloc_workspace(rl.rl_workspace_bytes(shape, R, chunk), dev)
-        dh = torch.empty(T, H, dtype=torch.bfloat16, device=dev)
-    torch.cuda.synchronize()
+    r.chunk = 0 if r.T <= 16384 else 16384
+    return r
 
-    launches = [0]
-    hidden, w_loc = b["hidden"], b["w"]
+
+def _stored_infer_logprobs(r):
+    """The stored inference log-probs: the trainer's own log-prob minus the drawn mismatch."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2512_16144_b200 as rl
+
+    logp_ref = torch.empty(r.T, dtype=torch.float32, device=r.dev)
+    if r.vocab_par:
+        parts = torch.empty(r.world, r.T, 4, dtype=torch.float32, device=r.dev)
+        ws0 = rl.alloc_workspace(rl.rl_workspace_bytes(r.shape, r.R, 16384), r.dev)
+        rl.rl_fwd_partials(r.shape, r.b["hidden"], r.b["w"], r.targets, parts[r.rank], workspace=ws0)
+        dist.all_gather_into_tensor(parts, parts[r.rank].contiguous())
+        rl.rl_merge_partials(parts, r.world, r.T, logp_ref)
+        del ws0
+    else:
+        rl.rl_logprob_fwd(r.shape, r.b["hidden"], r.b["w"], r.targets, logp_ref)
+    infer = torch.clamp(logp_ref - r.b["delta"], max=0.0)
+    return torch.where(r.b["spikes"], torch.zeros_like(infer), infer).contiguous()
+
+
+def _make_engine(r, args):
+    """Output buffers, workspace and (N > 1) the multi-GPU engine; returns step()."""
+    import torch
+
+    import paper_2512_16144_b200 as rl
+    from paper_2512_16144_b200 import parallel
+
+    f32 = dict(dtype=torch.float32, device=r.dev)
+    r.phases = parallel.LibrlPhases(dense_backward=args.dense_backward)
+    r.adv = torch.empty(r.R, **f32)
+    r.report = rl.new_report(r.dev)
+    r.logprob = torch.empty(r.T, **f32)
+    r.lse = torch.empty(r.T, **f32)
+    r.coef = torch.empty(r.T, **f32)
+    r.dw = torch.empty(r.V_local, r.H, **f32)
+    nv = args.collective == "nvls"
+    if r.vocab_par:
+        r.engine = parallel.VocabParallelPolicyLoss(r.phases, T=r.T, H=r.H, V_global=r.Vt, num_rollouts=r.R,
+                                                    group_size=r.wl_rank.group_size, loss_denominator=r.D,
+                                                    dz_chunk_rows=0 if nv else r.chunk, device=r.dev, nvls=nv)
+        r.ws, r.dh = r.engine.ws, r.engine.d_hidden
+    elif r.world > 1:
+        r.engine = parallel.DataParallelPolicyLoss(r.phases, T=r.T, H=r.H, V=r.Vt, num_rollouts=r.R,
+                                                   group_size=r.wl_rank.group_size, loss_denominator=r.D,
+                                                   device=r.dev, overlap=args.overlap, comm_sms=args.comm_sms,
+                                                   nvls=nv, reduce_scatter=args.dw_reduce_scatter and nv)
+        r.ws, r.dh = r.engine.ws, r.engine.d_hidden
+    else:
+        r.engine = None
+        r.ws = rl.alloc_workspace(rl.rl_workspace_bytes(r.shape, r.R, r.chunk), r.dev)
+        r.dh = torch.empty(r.T, r.H, dtype=torch.bfloat16, device=r.dev)
+    torch.cuda.synchronize()
+    r.launches = 0
+    hidden, w_loc = r.b["hidden"], r.b["w"]
 
     def step():
-        phases.launches = 0
-        if engine is not None:
-            engine.step(hidden, w_loc, targets, infer, rewards, offsets, loss_mask, dw)
+        r.phases.launches = 0
+        if r.engine is not None:
+            r.engine.step(hidden, w_loc, r.targets, r.infer, r.rewards, r.offsets, r.loss_mask, r.dw)
         else:
-            phases.group_advantages(rewards, wl_rank.group_size, adv)
-            phases.full_step(shape, params, hidden, w_loc, targets, infer, adv, offsets, loss_mask, report=report,
-                             logprob=logprob, lse=lse, coef=coef, d_hidden=dh, d_w_vocab=dw, dz_chunk_rows=chunk,
-                             workspace=ws)
-        launches[0] = phases.launches
+            r.phases.group_advantages(r.rewards, r.wl_rank.group_size, r.adv)
+            r.phases.full_step(r.shape, r.params, hidden, w_loc, r.targets, r.infer, r.adv, r.offsets, r.loss_mask,
+                               report=r.report, logprob=r.logprob, lse=r.lse, coef=r.coef, d_hidden=r.dh,
+                               d_w_vocab=r.dw, dz_chunk_rows=r.chunk, workspace=r.ws)
+        r.launches = r.phases.launches
+
+    return step
+
+
+def _time_steps(r, args, step):
+    """W warm-up steps, then exactly K timed steps between barriers + syncs, CUDA events
+    on the launching stream, max over ranks; per-launch kernel times and clocks."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2512_16144_b200 as rl
 
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
-    if world > 1:
+    if r.world > 1:
         dist.barrier()
     stream = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     rl.rl_profile_enable(True)
     rl.rl_profile_read()
-    with ClockSampler([local] if world == 1 else list(range(world))) as clk:
+    with ClockSampler([r.local] if r.world == 1 else list(range(r.world))) as clk:
         torch.cuda.synchronize()
-        if world > 1:
+        if r.world > 1:
             dist.barrier()
         e0.record(stream)
         for _ in range(args.steps):
             step()
         e1.record(stream)
         torch.cuda.synchronize()
-        if world > 1:
+        if r.world > 1:
             dist.barrier()
     rl.rl_profile_enable(False)
-    prof = rl.rl_profile_read(1 << 16)
-    ms = e0.elapsed_time(e1) / args.steps
-    t = torch.tensor([ms], dtype=torch.float64, device=dev)
-    if world > 1:
+    r.prof = rl.rl_profile_read(1 << 16)
+    r.ms = e0.elapsed_time(e1) / args.steps
+    t = torch.tensor([r.ms], dtype=torch.float64, device=r.dev)
+    if r.world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max = float(t.item())
-    tokens_per_step = T if vocab_par else T * world
-    value = tokens_per_step / (ms_max / 1e3)
+    r.ms_max = float(t.item())
+    r.clk = clk
+    r.value = (r.T if r.vocab_par else r.T * r.world) / (r.ms_max / 1e3)
 
-    # per-kernel share of the timed region and the dominant kernel's roofline
+
+def _kernel_report(r, args):
+    """Per-kernel shares and rooflines; the roofline object of the dominant kernel."""
     per = {}
-    for k, m in prof:
+    for k, m in r.prof:
         c = per.setdefault(k, [0, 0.0])
         c[0] += 1
         c[1] += m
-    total_k = sum(v[1] for v in per.values())
-    kern = {k: {"launches": v[0], "avg_ms": v[1] / v[0], "share": v[1] / (ms * args.steps)} for k, v in per.items()}
+    kern = {k: {"launches": v[0], "avg_ms": v[1] / v[0], "share": v[1] / (r.ms * args.steps)} for k, v in per.items()}
     # the backward GEMMs run over the rows with coef != 0 (sparse backward) unless the
     # vocab-parallel NVLS dH reduction forces the dense path; FLOPs per launch = the
     # step's FLOPs of that kernel / its launches per step
-    coef_t = engine.coef if engine is not None else coef
-    dense = args.dense_backward or (vocab_par and args.collective == "nvls")
+    T, H, V_local = r.T, r.H, r.V_local
+    coef_t = r.engine.coef if r.engine is not None else r.coef
+    dense = args.dense_backward or (r.vocab_par and args.collective == "nvls")
     bwd_rows = T if dense else int((coef_t != 0).sum().item())
     step_kflops = {"K1_fwd_gemm_lse": 2.0 * T * V_local * H, "K4_bwd_dz_gemm": 2.0 * bwd_rows * V_local * H,
                    "K5_dh_gemm": 2.0 * bwd_rows * V_local * H, "K6_dw_gemm": 2.0 * bwd_rows * V_local * H}
@@ -431,136 +457,161 @@ def main_ours(args):
         try:
             # measured for the per-rank GLM-16k shape only (profiles/traffic.json)
             # (one GPU, no fused collective: the NVLS epilogue adds its own traffic)
-            same = (T, V_local) == (16384, 151552) and world == 1
-            traffic = json.load(open(tpath)).get(f"{name}:{dom}") if same else None
-        except Exception:
+            same = (T, V_local) == (16384, 151552) and r.world == 1
+            traffic = json.load(open(tpath)).get(f"{r.name}:{dom}") if same else None
+        except Exception:  # noqa: BLE001
             traffic = None
     step_flops = 8.0 * H * V_local * T   # algorithmic 8HV per token on this rank
+    rate = lambda f: f / (r.ms_max / 1e3) / 1e12  # noqa: E731
     roof = {"bound": "tensor", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
             "frac": achieved / peak, "traffic": traffic,
             "peak_source": f"bf16_tflops_sustained, {peak_src}",
-            "step_frac_8HV": (step_flops / (ms_max / 1e3) / 1e12) / peak,
-            "step_frac_8HV_vs_burst": (step_flops / (ms_max / 1e3) / 1e12) / float(peaks.get("bf16_tflops", peak)),
-            "step_frac_6HV": (0.75 * step_flops / (ms_max / 1e3) / 1e12) / peak,
+            "step_frac_8HV": rate(step_flops) / peak,
+            "step_frac_8HV_vs_burst": rate(step_flops) / float(peaks.get("bf16_tflops", peak)),
+            "step_frac_6HV": rate(0.75 * step_flops) / peak,
             "bwd_rows": bwd_rows,
-            "step_frac_executed": (sum(step_kflops.values()) / (ms_max / 1e3) / 1e12) / peak}
+            "step_frac_executed": rate(sum(step_kflops.values())) / peak}
+    return kern, roof
 
-    # e2e through the host-I/O C call (pinned inputs in, report out, every step)
-    e2e = None
-    if not vocab_par and not args.no_e2e:
-        hpin = b["hidden"].view(torch.int16).cpu().pin_memory()
-        tpin = targets.cpu().pin_memory()
-        ipin = infer.cpu().pin_memory()
-        rpin = torch.from_numpy(b["rewards"]).pin_memory()
-        opin = torch.from_numpy(b["offsets"]).pin_memory()
-        mpin = torch.from_numpy(b["loss_mask"]).pin_memory()
-        del ws
-        if engine is not None:
-            engine.ws = None
-        wsh = rl.alloc_workspace(rl.rl_workspace_bytes_hostio(shape, R, chunk), dev)
 
-        nvls_dp = engine is not None and getattr(engine, "nvls", None) is not None
+def _timed_host_steps(r, args, hstep):
+    """Warm-up, then K host-driven steps on the wall clock (each ends in a D2H read), max over ranks."""
+    import torch
+    import torch.distributed as dist
 
-        def hstep():
-            if nvls_dp:
-                rl.rl_policy_loss_fwd_bwd_hostio(shape, params, wl_rank.group_size, hpin, b["w"], tpin, ipin, rpin,
-                                                 opin, mpin, report=report, d_hidden=dh, d_w_vocab=engine.nvls.buf,
-                                                 d_w_vocab_nvls=engine.nvls.descriptor(
-                                                     mode=1 if engine.reduce_scatter else 0),
-                                                 dz_chunk_rows=chunk,
-                                                 dense_backward=args.dense_backward, workspace=wsh)
-                engine.nvls.barrier()
-                return
-            rl.rl_policy_loss_fwd_bwd_hostio(shape, params, wl_rank.group_size, hpin, b["w"], tpin, ipin, rpin, opin,
-                                             mpin, report=report, d_hidden=dh, d_w_vocab=dw, dz_chunk_rows=chunk,
-                                             dense_backward=args.dense_backward, workspace=wsh)
-            if world > 1:
-                dist.all_reduce(dw)
-
-        for _ in range(max(1, args.warmup)):
-            hstep()
-        torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
-        t0 = time.perf_counter()
-        for _ in range(args.steps):
-            hstep()
-        torch.cuda.synchronize()
-        el = (time.perf_counter() - t0) / args.steps
-        t = torch.tensor([el], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        el = float(t.item())
-        h2d = T * H * 2 + T * 4 + T * 4 + R * 4 + (R + 1) * 4 + T
-        e2e = {"value": T * world / el, "unit": "tokens/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 48,
-               "ms_per_step": el * 1e3, "api": "rl_policy_loss_fwd_bwd_hostio"}
-    elif vocab_par and not args.no_e2e:
-        # vocab-parallel end to end: every rank uploads the (replicated) step inputs from
-        # pinned host memory, runs the split-phase engine and reads the report back
-        pins = {"hidden": b["hidden"].cpu().pin_memory(), "targets": targets.cpu().pin_memory(),
-                "infer": infer.cpu().pin_memory(), "rewards": rewards.cpu().pin_memory(),
-                "offsets": offsets.cpu().pin_memory(), "loss_mask": loss_mask.cpu().pin_memory()}
-        devs = {k: torch.empty_like(v, device=dev) for k, v in pins.items()}
-        rep_h = torch.empty(48, dtype=torch.uint8).pin_memory()
-
-        def hstep():
-            for k, v in pins.items():
-                devs[k].copy_(v, non_blocking=True)
-            engine.step(devs["hidden"], w_loc, devs["targets"], devs["infer"], devs["rewards"], devs["offsets"],
-                        devs["loss_mask"], dw)
-            rep_h.copy_(engine.report, non_blocking=True)
-            torch.cuda.current_stream().synchronize()
-
-        for _ in range(max(1, args.warmup)):
-            hstep()
+    for _ in range(max(1, args.warmup)):
+        hstep()
+    torch.cuda.synchronize()
+    if r.world > 1:
         dist.barrier()
-        t0 = time.perf_counter()
-        for _ in range(args.steps):
-            hstep()
-        torch.cuda.synchronize()
-        el = (time.perf_counter() - t0) / args.steps
-        t = torch.tensor([el], dtype=torch.float64, device=dev)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        hstep()
+    torch.cuda.synchronize()
+    el = (time.perf_counter() - t0) / args.steps
+    t = torch.tensor([el], dtype=torch.float64, device=r.dev)
+    if r.world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        el = float(t.item())
-        e2e = {"value": T / el, "unit": "tokens/s",
-               "h2d_bytes_per_step": int(sum(v.numel() * v.element_size() for v in pins.values())),
-               "d2h_bytes_per_step": 48, "ms_per_step": el * 1e3,
-               "api": "parallel.VocabParallelPolicyLoss.step (host inputs, per rank)"}
+    return float(t.item())
 
-    out = None
-    if rank == 0:
-        cfg = {"workload": name, "T_per_rank": T, "H": H, "V": Vt, "V_local": V_local, "rollouts_per_rank": R,
-               "group_size": wl_rank.group_size, "parallelism": f"{mode}{world}",
-               "l2": "inputs exceed L2 (W %.2f GB, hidden %.0f MB > 126 MB); no flush needed" % (
-                   V_local * H * 2 / 1e9, T * H * 2 / 1e6),
-               "dz_chunk_rows": (T if (vocab_par and args.collective == "nvls") else (chunk or T)),
-               "collectives": ([] if world == 1 else
-                               (["all_gather partials (NCCL)", "dH fp32 all-reduce " +
-                                 ("fused in K5 epilogue (NVLS multimem)" if args.collective == "nvls" else "(NCCL)")]
-                                if vocab_par else
-                                ["dW fp32 all-reduce " + ("fused in K6 epilogue (NVLS multimem)"
-                                                          if args.collective == "nvls" else "(NCCL)")]))}
-        if world > 1:
-            # the step's exchange and its NVLink roofline (900 GB/s per direction): NVLS moves
-            # about 1x the buffer per GPU and direction, a ring all-reduce 2(N-1)/N x
-            nb = (T * H * 4) if vocab_par else (V_local * H * 4)
-            rs = (not vocab_par) and args.dw_reduce_scatter and args.collective == "nvls"
-            per_dir = (nb * (world - 1) / world if rs else nb) if args.collective == "nvls" \
-                else 2 * (world - 1) / world * nb
-            cfg["collective"] = {"op": ("dH" if vocab_par else "dW") + " fp32 " +
-                                 ("reduce-scatter (vocab rows)" if rs else "all-reduce"),
-                                 "buffer_bytes": nb, "bytes_per_gpu_per_direction": per_dir,
-                                 "nvlink_roofline_ms": per_dir / 900e9 * 1e3}
-        out = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
-               "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,
-               "scaling": "strong" if vocab_par else "weak", "vs_baseline": None, "dtype": "bf16",
-               "data": "synthetic (seeded; GLM-4.5-Air-shaped rollouts, random-init W)", "config": cfg,
-               "roofline": roof, "e2e": e2e, "gpu_launches": launches[0] * args.steps,
-               "clocks": clk.summary(), "kernels": kern, "impl": "ours"}
-        if world == 1 and not args.no_cpu_baseline:
-            out["cpu_baseline"] = cpu_baseline(wl, budget_s=args.cpu_budget)
-        emit(out)
+
+def _e2e_dp(r, args):
+    """e2e through the host-I/O C call (pinned inputs in, report out, every step)."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2512_16144_b200 as rl
+
+    b = r.b
+    hpin = b["hidden"].view(torch.int16).cpu().pin_memory()
+    tpin = r.targets.cpu().pin_memory()
+    ipin = r.infer.cpu().pin_memory()
+    rpin = torch.from_numpy(b["rewards"]).pin_memory()
+    opin = torch.from_numpy(b["offsets"]).pin_memory()
+    mpin = torch.from_numpy(b["loss_mask"]).pin_memory()
+    r.ws = None                     # the host-I/O call needs its own (larger) workspace
+    if r.engine is not None:
+        r.engine.ws = None
+    wsh = rl.alloc_workspace(rl.rl_workspace_bytes_hostio(r.shape, r.R, r.chunk), r.dev)
+    nvls_dp = r.engine is not None and getattr(r.engine, "nvls", None) is not None
+
+    def hstep():
+        if nvls_dp:
+            rl.rl_policy_loss_fwd_bwd_hostio(r.shape, r.params, r.wl_rank.group_size, hpin, b["w"], tpin, ipin, rpin,
+                                             opin, mpin, report=r.report, d_hidden=r.dh, d_w_vocab=r.engine.nvls.buf,
+                                             d_w_vocab_nvls=r.engine.nvls.descriptor(
+                                                 mode=1 if r.engine.reduce_scatter else 0),
+                                             dz_chunk_rows=r.chunk, dense_backward=args.dense_backward,
+                                             workspace=wsh)
+            r.engine.nvls.barrier()
+            return
+        rl.rl_policy_loss_fwd_bwd_hostio(r.shape, r.params, r.wl_rank.group_size, hpin, b["w"], tpin, ipin, rpin,
+                                         opin, mpin, report=r.report, d_hidden=r.dh, d_w_vocab=r.dw,
+                                         dz_chunk_rows=r.chunk, dense_backward=args.dense_backward, workspace=wsh)
+        if r.world > 1:
+            dist.all_reduce(r.dw)
+
+    el = _timed_host_steps(r, args, hstep)
+    T, H, R = r.T, r.H, r.R
+    h2d = T * H * 2 + T * 4 + T * 4 + R * 4 + (R + 1) * 4 + T
+    return {"value": T * r.world / el, "unit": "tokens/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 48,
+            "ms_per_step": el * 1e3, "api": "rl_policy_loss_fwd_bwd_hostio"}
+
+
+def _e2e_vocab(r, args):
+    """Vocab-parallel end to end: every rank uploads the (replicated) step inputs from
+    pinned host memory, runs the split-phase engine and reads the report back."""
+    import torch
+
+    pins = {"hidden": r.b["hidden"].cpu().pin_memory(), "targets": r.targets.cpu().pin_memory(),
+            "infer": r.infer.cpu().pin_memory(), "rewards": r.rewards.cpu().pin_memory(),
+            "offsets": r.offsets.cpu().pin_memory(), "loss_mask": r.loss_mask.cpu().pin_memory()}
+    devs = {k: torch.empty_like(v, device=r.dev) for k, v in pins.items()}
+    rep_h = torch.empty(48, dtype=torch.uint8).pin_memory()
+
+    def hstep():
+        for k, v in pins.items():
+            devs[k].copy_(v, non_blocking=True)
+        r.engine.step(devs["hidden"], r.b["w"], devs["targets"], devs["infer"], devs["rewards"], devs["offsets"],
+                      devs["loss_mask"], r.dw)
+        rep_h.copy_(r.engine.report, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+
+    el = _timed_host_steps(r, args, hstep)
+    return {"value": r.T / el, "unit": "tokens/s",
+            "h2d_bytes_per_step": int(sum(v.numel() * v.element_size() for v in pins.values())),
+            "d2h_bytes_per_step": 48, "ms_per_step": el * 1e3,
+            "api": "parallel.VocabParallelPolicyLoss.step (host inputs, per rank)"}
+
+
+def _config(r, args):
+    T, H, V_local, world = r.T, r.H, r.V_local, r.world
+    nv = args.collective == "nvls"
+    cfg = {"workload": r.name, "T_per_rank": T, "H": H, "V": r.Vt, "V_local": V_local, "rollouts_per_rank": r.R,
+           "group_size": r.wl_rank.group_size, "parallelism": f"{r.mode}{world}",
+           "l2": "inputs exceed L2 (W %.2f GB, hidden %.0f MB > 126 MB); no flush needed" % (
+               V_local * H * 2 / 1e9, T * H * 2 / 1e6),
+           "dz_chunk_rows": (T if (r.vocab_par and nv) else (r.chunk or T)),
+           "collectives": ([] if world == 1 else
+                           (["all_gather partials (NCCL)", "dH fp32 all-reduce " +
+                             ("fused in K5 epilogue (NVLS multimem)" if nv else "(NCCL)")]
+                            if r.vocab_par else
+                            ["dW fp32 all-reduce " + ("fused in K6 epilogue (NVLS multimem)" if nv else "(NCCL)")]))}
     if world > 1:
+        # the step's exchange and its NVLink roofline (900 GB/s per direction): NVLS moves
+        # about 1x the buffer per GPU and direction, a ring all-reduce 2(N-1)/N x
+        nb = (T * H * 4) if r.vocab_par else (V_local * H * 4)
+        rs = (not r.vocab_par) and args.dw_reduce_scatter and nv
+        per_dir = (nb * (world - 1) / world if rs else nb) if nv else 2 * (world - 1) / world * nb
+        cfg["collective"] = {"op": ("dH" if r.vocab_par else "dW") + " fp32 " +
+                             ("reduce-scatter (vocab rows)" if rs else "all-reduce"),
+                             "buffer_bytes": nb, "bytes_per_gpu_per_direction": per_dir,
+                             "nvlink_roofline_ms": per_dir / 900e9 * 1e3}
+    return cfg
+
+
+def main_ours(args):
+    import torch.distributed as dist
+
+    r = _setup(args)
+    r.infer = _stored_infer_logprobs(r)
+    step = _make_engine(r, args)
+    _time_steps(r, args, step)
+    kern, roof = _kernel_report(r, args)
+    e2e = None
+    if not args.no_e2e:
+        e2e = _e2e_vocab(r, args) if r.vocab_par else _e2e_dp(r, args)
+    if r.rank == 0:
+        out = {"metric": METRIC, "value": r.value, "unit": "tokens/s", "n_gpus": r.world, "steps": args.steps,
+               "warmup": args.warmup, "ms_per_step": r.ms_max, "higher_is_better": True,
+               "scaling": "strong" if r.vocab_par else "weak", "vs_baseline": None, "dtype": "bf16",
+               "data": "synthetic (seeded; GLM-4.5-Air-shaped rollouts, random-init W)", "config": _config(r, args),
+               "roofline": roof, "e2e": e2e, "gpu_launches": r.launches * args.steps,
+               "clocks": r.clk.summary(), "kernels": kern, "impl": "ours"}
+        if r.world == 1 and not args.no_cpu_baseline:
+            out["cpu_baseline"] = cpu_baseline(r.wl, budget_s=args.cpu_budget)
+        emit(out)
+    if r.world > 1:
         dist.barrier()
         dist.destroy_process_group()
     return 0
