@@ -60,6 +60,11 @@ int cta_group() {
 // Raster group (in m-blocks) per GEMM: tiles walk n inside groups of this many
 // m-blocks. Defaults chosen from the sweep in DESIGN.md §5; RL_GROUP_M_<K>
 // overrides (K in FWD, DZ, DH, DW) for measurements.
+// Raster group of the wide dH / dW GEMMs: tiles walk n inside groups of 2 m-blocks.
+// DRAM reads per launch at GLM-16k: 8 -> 17.3 GB, 4 -> 15.6, 2 -> 14.7; step -0.8 ms
+// (profiles/r01/raster_traffic/, bwd_group_ab/).
+constexpr int kGroupMBwd = 2;
+
 int group_m_for(int kid, int dflt) {
   static int cache[16];
   static bool init[16] = {};

@@ -187,13 +187,13 @@ rl_status bwd_sparse_impl(const rl_lm_shape* s, const uint16_t* hidden, const ui
       if (dw_nvls) {
         set_nvls(e6, dw_nvls, dw);
         RL_TRY((launch_gemm<rl::EPI_F32_NVLS, true, true>(RL_K_DW_GEMM, t_dz_mn, t_h_mn, t_dw, V, H, rows,
-                                                            group_m_for(RL_K_DW_GEMM, 8), e6, sms, st, 1, 0, cnt, 2)));
+                                                            group_m_for(RL_K_DW_GEMM, kGroupMBwd), e6, sms, st, 1, 0, cnt, 2)));
       } else if (ch == 0 && !accumulate_dw) {
         RL_TRY((launch_gemm<rl::EPI_F32, true, true>(RL_K_DW_GEMM, t_dz_mn, t_h_mn, t_dw, V, H, rows,
-                                                     group_m_for(RL_K_DW_GEMM, 8), e6, sms, st, 1, 0, cnt, 2)));
+                                                     group_m_for(RL_K_DW_GEMM, kGroupMBwd), e6, sms, st, 1, 0, cnt, 2)));
       } else {
         RL_TRY((launch_gemm<rl::EPI_F32_ADD, true, true>(RL_K_DW_GEMM, t_dz_mn, t_h_mn, t_dw, V, H, rows,
-                                                         group_m_for(RL_K_DW_GEMM, 8), e6, sms, st, 1, 0, cnt, 2)));
+                                                         group_m_for(RL_K_DW_GEMM, kGroupMBwd), e6, sms, st, 1, 0, cnt, 2)));
       }
     }
     if ((phases & RL_BWD_DH) && (dh || dh32)) {
@@ -204,11 +204,11 @@ rl_status bwd_sparse_impl(const rl_lm_shape* s, const uint16_t* hidden, const ui
       if (dh) {
         RL_TRY(make_map(&t_dh, dh_c, false, H, rows, H, 64, 32));
         RL_TRY((launch_gemm<rl::EPI_BF16, false, true>(RL_K_DH_GEMM, t_dz_k, t_w_mn, t_dh, rows, H, V,
-                                                       group_m_for(RL_K_DH_GEMM, 8), e5, sms, st, 1, 0, cnt, 1)));
+                                                       group_m_for(RL_K_DH_GEMM, kGroupMBwd), e5, sms, st, 1, 0, cnt, 1)));
       } else {
         RL_TRY(make_map(&t_dh, dh_c, true, H, rows, H, 32, 32));
         RL_TRY((launch_gemm<rl::EPI_F32, false, true>(RL_K_DH_GEMM, t_dz_k, t_w_mn, t_dh, rows, H, V,
-                                                      group_m_for(RL_K_DH_GEMM, 8), e5, sms, st, 1, 0, cnt, 1)));
+                                                      group_m_for(RL_K_DH_GEMM, kGroupMBwd), e5, sms, st, 1, 0, cnt, 1)));
       }
       {
         ProfScope ps(RL_K_COMPACT, st);
@@ -271,11 +271,11 @@ rl_status bwd_impl(const rl_lm_shape* s, const uint16_t* hidden, const uint16_t*
       if (dw_nvls) {
         set_nvls(e6, dw_nvls, dw);
         RL_TRY((launch_gemm<rl::EPI_F32_NVLS, true, true>(RL_K_DW_GEMM, t_dz_mn, t_h_mn, t_dw, V, H, rows,
-                                                            group_m_for(RL_K_DW_GEMM, 8), e6, sms, st)));
+                                                            group_m_for(RL_K_DW_GEMM, kGroupMBwd), e6, sms, st)));
       } else if (c0 == 0 && !accumulate_dw) {
-        RL_TRY((launch_gemm<rl::EPI_F32, true, true>(RL_K_DW_GEMM, t_dz_mn, t_h_mn, t_dw, V, H, rows, group_m_for(RL_K_DW_GEMM, 8), e6, sms, st)));
+        RL_TRY((launch_gemm<rl::EPI_F32, true, true>(RL_K_DW_GEMM, t_dz_mn, t_h_mn, t_dw, V, H, rows, group_m_for(RL_K_DW_GEMM, kGroupMBwd), e6, sms, st)));
       } else {
-        RL_TRY((launch_gemm<rl::EPI_F32_ADD, true, true>(RL_K_DW_GEMM, t_dz_mn, t_h_mn, t_dw, V, H, rows, group_m_for(RL_K_DW_GEMM, 8), e6, sms, st)));
+        RL_TRY((launch_gemm<rl::EPI_F32_ADD, true, true>(RL_K_DW_GEMM, t_dz_mn, t_h_mn, t_dw, V, H, rows, group_m_for(RL_K_DW_GEMM, kGroupMBwd), e6, sms, st)));
       }
     }
     // K5: dH chunk = dU W
@@ -286,15 +286,15 @@ rl_status bwd_impl(const rl_lm_shape* s, const uint16_t* hidden, const uint16_t*
       e5.cols = H;
       if (dh) {
         RL_TRY(make_map(&t_dh, dh + c0 * H, false, H, rows, H, 64, 32));
-        RL_TRY((launch_gemm<rl::EPI_BF16, false, true>(RL_K_DH_GEMM, t_dz_k, t_w_mn, t_dh, rows, H, V, group_m_for(RL_K_DH_GEMM, 8), e5, sms, st)));
+        RL_TRY((launch_gemm<rl::EPI_BF16, false, true>(RL_K_DH_GEMM, t_dz_k, t_w_mn, t_dh, rows, H, V, group_m_for(RL_K_DH_GEMM, kGroupMBwd), e5, sms, st)));
       } else {
         RL_TRY(make_map(&t_dh, dh32 + c0 * H, true, H, rows, H, 32, 32));
         if (dh_nvls) {
           set_nvls(e5, dh_nvls, dh32 + c0 * H);
           RL_TRY((launch_gemm<rl::EPI_F32_NVLS, false, true>(RL_K_DH_GEMM, t_dz_k, t_w_mn, t_dh, rows, H, V,
-                                                               group_m_for(RL_K_DH_GEMM, 8), e5, sms, st)));
+                                                               group_m_for(RL_K_DH_GEMM, kGroupMBwd), e5, sms, st)));
         } else
-        RL_TRY((launch_gemm<rl::EPI_F32, false, true>(RL_K_DH_GEMM, t_dz_k, t_w_mn, t_dh, rows, H, V, group_m_for(RL_K_DH_GEMM, 8), e5, sms, st)));
+        RL_TRY((launch_gemm<rl::EPI_F32, false, true>(RL_K_DH_GEMM, t_dz_k, t_w_mn, t_dh, rows, H, V, group_m_for(RL_K_DH_GEMM, kGroupMBwd), e5, sms, st)));
       }
     }
   }
