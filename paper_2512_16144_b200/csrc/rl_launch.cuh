@@ -70,7 +70,7 @@ int group_m_for(int kid, int dflt) {
   static bool init[16] = {};
   if (!init[kid]) {
     const char* names[16] = {nullptr, "RL_GROUP_M_FWD", nullptr, nullptr, nullptr, "RL_GROUP_M_DZ",
-                             "RL_GROUP_M_DH", "RL_GROUP_M_DW"};
+                             "RL_GROUP_M_DH", "RL_GROUP_M_DW", nullptr, "RL_GROUP_M_NS"};
     const char* e = names[kid] ? getenv(names[kid]) : nullptr;
     cache[kid] = (e && atoi(e) > 0) ? atoi(e) : dflt;
     init[kid] = true;
