@@ -539,21 +539,19 @@ def _e2e_dp(r, args):
 
 
 def _e2e_vocab(r, args):
-    """Vocab-parallel end to end: every rank uploads the (replicated) step inputs from
-    pinned host memory, runs the split-phase engine and reads the report back."""
+    """Vocab-parallel end to end through VocabParallelPolicyLoss.step_host: every rank
+    uploads the (replicated) step inputs from pinned host memory, the hidden rows in
+    slabs under the forward, and reads the report back."""
     import torch
 
-    pins = {"hidden": r.b["hidden"].cpu().pin_memory(), "targets": r.targets.cpu().pin_memory(),
+    pins = {"hidden": r.b["hidden"].view(torch.int16).cpu().pin_memory(), "targets": r.targets.cpu().pin_memory(),
             "infer": r.infer.cpu().pin_memory(), "rewards": r.rewards.cpu().pin_memory(),
             "offsets": r.offsets.cpu().pin_memory(), "loss_mask": r.loss_mask.cpu().pin_memory()}
-    devs = {k: torch.empty_like(v, device=r.dev) for k, v in pins.items()}
     rep_h = torch.empty(48, dtype=torch.uint8).pin_memory()
 
     def hstep():
-        for k, v in pins.items():
-            devs[k].copy_(v, non_blocking=True)
-        r.engine.step(devs["hidden"], r.b["w"], devs["targets"], devs["infer"], devs["rewards"], devs["offsets"],
-                      devs["loss_mask"], r.dw)
+        r.engine.step_host(pins["hidden"], r.b["w"], pins["targets"], pins["infer"], pins["rewards"],
+                           pins["offsets"], pins["loss_mask"], r.dw)
         rep_h.copy_(r.engine.report, non_blocking=True)
         torch.cuda.current_stream().synchronize()
 
@@ -561,7 +559,7 @@ def _e2e_vocab(r, args):
     return {"value": r.T / el, "unit": "tokens/s",
             "h2d_bytes_per_step": int(sum(v.numel() * v.element_size() for v in pins.values())),
             "d2h_bytes_per_step": 48, "ms_per_step": el * 1e3,
-            "api": "parallel.VocabParallelPolicyLoss.step (host inputs, per rank)"}
+            "api": "parallel.VocabParallelPolicyLoss.step_host (pinned host inputs, per rank)"}
 
 
 def _config(r, args):

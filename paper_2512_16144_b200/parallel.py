@@ -208,6 +208,66 @@ class VocabParallelPolicyLoss:
         dist.all_reduce(self.d_hidden, group=self.group)                                  # exchange 2
         return self.d_hidden
 
+    def step_host(self, hidden_host, w_shard, targets_host, infer_host, rewards_host, offsets_host,
+                  loss_mask_host, d_w_vocab, slab_ends=None):
+        """step() with the per-step inputs in pinned HOST memory: the small inputs, then the
+        hidden rows in slabs, go up on a copy stream, and the forward partials run slab by
+        slab as the rows arrive (each row's partial is independent), so the upload hides
+        under K1. Returns d_hidden like step()."""
+        dev = w_shard.device
+        if getattr(self, "_host_in", None) is None:
+            self._host_in = {"hidden": torch.empty(self.T, self.H, dtype=torch.bfloat16, device=dev),
+                             "targets": torch.empty(self.T, dtype=torch.int32, device=dev),
+                             "infer": torch.empty(self.T, dtype=torch.float32, device=dev),
+                             "rewards": torch.empty(self.R, dtype=torch.float32, device=dev),
+                             "offsets": torch.empty(self.R + 1, dtype=torch.int32, device=dev),
+                             "loss_mask": torch.empty(self.T, dtype=torch.uint8, device=dev)}
+            self._copy = torch.cuda.Stream(device=dev)
+        d = self._host_in
+        ends = slab_ends or [e for e in (1024, 4096) if e < self.T] + list(range(8192, self.T, 8192)) + [self.T]
+        main = torch.cuda.current_stream(dev)
+        self._copy.wait_stream(main)                      # the previous step is done with the inputs
+        small_ev = torch.cuda.Event()
+        slab_evs = []
+        with torch.cuda.stream(self._copy):
+            for k, v in (("targets", targets_host), ("infer", infer_host), ("rewards", rewards_host),
+                         ("offsets", offsets_host), ("loss_mask", loss_mask_host)):
+                d[k].copy_(v, non_blocking=True)
+            small_ev.record()
+            r0 = 0
+            hidden_view = d["hidden"].view(hidden_host.dtype)
+            for r1 in ends:
+                hidden_view[r0:r1].copy_(hidden_host[r0:r1], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record()
+                slab_evs.append((r0, r1, ev))
+                r0 = r1
+        ph = self.ph
+        main.wait_event(small_ev)
+        ph.group_advantages(d["rewards"], self.G, self.adv)
+        mine = self.parts[self.rank]
+        for r0, r1, ev in slab_evs:                        # K1 (+ its one-partial-per-row merge) per slab
+            main.wait_event(ev)
+            sub = make_shape(r1 - r0, self.H, self.V_local, self.vocab_offset, self.V_global,
+                             self.shape.inv_temperature,
+                             inv_temperature_rows=None if self.invt_rows is None else self.invt_rows[r0:r1])
+            ph.fwd_partials(sub, d["hidden"][r0:r1], w_shard, d["targets"][r0:r1], mine[r0:r1], workspace=self.ws)
+        _all_gather_rows(self.parts, mine, self.group)                                    # exchange 1
+        ph.merge_partials(self.parts, self.world, self.T, self.logprob, self.entropy, self.lse)
+        ph.loss_coef(self.params, self.T, self.V_global, self.logprob, d["infer"], d["targets"], self.adv,
+                     d["offsets"], d["loss_mask"], self.coef, self.keep, self.guarded, self.report,
+                     workspace=self.loss_ws)
+        hidden, targets = d["hidden"], d["targets"]
+        if self.nvls is not None:
+            ph.bwd(self.shape, hidden, w_shard, targets, self.lse, self.coef, self.d_hidden, d_w_vocab,
+                   dz_chunk_rows=self.chunk, workspace=self.ws, dh_nvls=self.nvls.descriptor())
+            self.nvls.barrier()
+            return self.d_hidden
+        ph.bwd(self.shape, hidden, w_shard, targets, self.lse, self.coef, self.d_hidden, d_w_vocab,
+               dz_chunk_rows=self.chunk, workspace=self.ws)
+        dist.all_reduce(self.d_hidden, group=self.group)
+        return self.d_hidden
+
 
 class DataParallelPolicyLoss:
     """S0..S6 on each rank's own rollouts; dW summed over the ranks of `group`."""

@@ -97,3 +97,45 @@ def test_nvls_reduce_scatter_matches_nccl_rows(tmp_path):
         ref = full[r * S:(r + 1) * S]
         assert shard.shape == ref.shape and np.abs(ref).max() > 0
         np.testing.assert_allclose(shard, ref, rtol=1e-5, atol=1e-6 * np.abs(full).max())
+
+
+def _host_worker(rank, port, out_dir):
+    import synth
+    from paper_2512_16144_b200 import parallel
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(rank)
+    dev = torch.device("cuda", rank)
+    dist.init_process_group("nccl", rank=rank, world_size=WORLD, device_id=dev)
+    wl = synth.Workload("nv", 1, 4, 1500, 512, 3008, ragged=True, delta_sigma=0.5)   # T = 6000: three slabs
+    T = wl.tokens
+    Vl = wl.vocab // WORLD
+    b = synth.make_batch_device(wl, 60, device=dev, tokens=T, vocab=Vl, vocab_offset=rank * Vl, vocab_total=wl.vocab)
+    offs = torch.from_numpy(b["offsets"]).to(dev)
+    lm = torch.from_numpy(b["loss_mask"]).to(dev)
+    rw = torch.from_numpy(b["rewards"]).to(dev)
+    inf = torch.full((T,), -1.0, device=dev)
+    ok = []
+    for nv in (False, True):
+        eng = parallel.VocabParallelPolicyLoss(parallel.LibrlPhases(), T=T, H=wl.hidden, V_global=wl.vocab,
+                                               num_rollouts=wl.num_rollouts, group_size=wl.group_size,
+                                               loss_denominator=float(T), device=dev, nvls=nv)
+        dw1 = torch.empty(eng.V_local, wl.hidden, device=dev)
+        dw2 = torch.empty_like(dw1)
+        a = eng.step(b["hidden"], b["w"], b["targets"], inf, rw, offs, lm, dw1).clone()
+        lp1 = eng.logprob.clone()
+        pin = lambda t: t.cpu().pin_memory()  # noqa: E731
+        c = eng.step_host(pin(b["hidden"].view(torch.int16)), b["w"], pin(b["targets"]), pin(inf), pin(rw),
+                          pin(offs), pin(lm), dw2).clone()
+        torch.cuda.synchronize()
+        ok.append(bool(torch.equal(a, c) and torch.equal(dw1, dw2) and torch.equal(lp1, eng.logprob)))
+    np.save(os.path.join(out_dir, f"host{rank}.npy"), np.array(ok))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_vocab_parallel_step_host_equals_step(tmp_path):
+    """step_host (pinned host inputs, hidden rows uploaded in slabs under the forward)
+    gives step()'s outputs bit for bit, with NCCL and with the NVLS dH reduction."""
+    mp.start_processes(_host_worker, args=(_port(), str(tmp_path)), nprocs=WORLD, start_method="spawn")
+    for r in range(WORLD):
+        assert np.load(tmp_path / f"host{r}.npy").all()
