@@ -21,7 +21,8 @@ max and sum.
 Pins (tests/test_oracle_pins.py, `-m "not gpu"`): SPEC example tables, closed
 forms (uniform logits, two-level logits), normalisation, scipy/torch float64
 library cross-checks, on-policy closed form, finite differences, autograd,
-and the dZ/dW row-sum invariants. No function here is "parity unpinned".
+the dZ/dW row-sum invariants, bf16 decode of hand-worked bit patterns, and the
+hand-summed mismatch_kl_sum of tests/golden/hand_loss_example.json.
 """
 from __future__ import annotations
 

@@ -55,3 +55,28 @@ def test_muon_step_special_cases():
     np.testing.assert_allclose(m2, g)
     th3, _ = muon.muon_step(th, g, m, lr=0.1, weight_decay=0.5, nesterov=False)
     np.testing.assert_allclose(th3, th * 0.95 - 0.1 * (6 / 4) ** 0.5 * muon.newton_schulz(g), atol=1e-12)
+
+
+def test_muon_nesterov_branch_by_hand():
+    """Nesterov look-ahead u = g + mu m' with m' = mu m + g (reading R18), pinned on a
+    2 x 2 case worked by hand: mu = 0.5, g = diag(2/3, 0), m = diag(0, 4) give
+    m' = diag(2/3, 2) and u = diag(2/3 + 1/3, 0 + 1) = I. The orthogonalisation of a
+    multiple of the identity is a multiple of the identity (both singular values equal),
+    so theta - theta' must be c*I with c in the quintic's band [0.67, 1.15] * lr.
+    Every plausible slip breaks the proportionality: u = m' -> diag(2/3, 2); u = g + m'
+    -> diag(4/3, 2); u = mu g + m' -> diag(1, 2); u = g + mu m -> diag(2/3, 2)."""
+    g = np.diag([2.0 / 3.0, 0.0])
+    m = np.diag([0.0, 4.0])
+    th = np.array([[1.0, -2.0], [0.5, 3.0]])
+    lr = 0.01
+    th2, m2 = muon.muon_step(th, g, m, lr=lr, mu=0.5, nesterov=True)
+    np.testing.assert_allclose(m2, np.diag([2.0 / 3.0, 2.0]), atol=1e-15)
+    d = (th - th2) / lr
+    assert abs(d[0, 1]) < 1e-12 and abs(d[1, 0]) < 1e-12
+    assert d[0, 0] == pytest.approx(d[1, 1], rel=1e-12)
+    assert 0.67 < d[0, 0] < 1.15
+    # the plain-momentum branch on the same inputs orthogonalises diag(2/3, 2): unequal
+    th3, m3 = muon.muon_step(th, g, m, lr=lr, mu=0.5, nesterov=False)
+    np.testing.assert_allclose(m3, m2, atol=0)
+    d3 = (th - th3) / lr
+    assert abs(d3[0, 0] - d3[1, 1]) > 1e-3

@@ -59,6 +59,30 @@ def test_hand_loss_example(golden_dir):
     np.testing.assert_allclose(rep.coef * ex["D"], ex["coef_times_D"], atol=1e-13)
     for key in ("masked_low", "masked_high", "guarded_rollouts", "guarded_tokens", "kept_tokens"):
         assert getattr(rep, key) == ex[key], key
+    # k - ln k - 1 summed by hand over every valid token (catches a sum over kept tokens
+    # only, a dropped -1, or ln k taken with the wrong sign)
+    assert rep.mismatch_kl_sum == pytest.approx(ex["mismatch_kl_sum"], rel=1e-12)
+
+
+# --------------------------------------------------------------- input decode
+@pytest.mark.parametrize("bits,value", [
+    (0x3F80, 1.0), (0xC000, -2.0), (0x3F81, 1.0 + 2.0 ** -7), (0x4049, 3.140625),
+    (0x0001, 2.0 ** -133),                     # smallest subnormal: 2^-126 * 2^-7
+    (0x0080, 2.0 ** -126),                     # smallest normal
+    (0x7F7F, (2.0 - 2.0 ** -7) * 2.0 ** 127),  # largest finite
+    (0x7F80, math.inf), (0xFF80, -math.inf),
+])
+def test_bf16_decode_known_bit_patterns(bits, value):
+    """bf16 = the top 16 bits of an IEEE binary32 (sign, 8-bit exponent, 7-bit
+    mantissa); each value above is worked out from that layout by hand. A wrong
+    shift, a sign-extension of the uint16 or a float16 reinterpretation fails."""
+    assert oracle.bf16_to_f64(np.array([bits], dtype=np.uint16))[0] == value
+
+
+def test_bf16_decode_signed_zero_and_nan():
+    z = oracle.bf16_to_f64(np.array([0x8000, 0x0000], dtype=np.uint16))
+    assert z[0] == 0.0 and math.copysign(1.0, z[0]) == -1.0 and math.copysign(1.0, z[1]) == 1.0
+    assert np.isnan(oracle.bf16_to_f64(np.array([0x7FC0, 0xFFC1], dtype=np.uint16))).all()
 
 
 # ---------------------------------------------------------- closed forms
