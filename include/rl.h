@@ -50,7 +50,7 @@
 extern "C" {
 #endif
 
-#define RL_ABI_VERSION 2
+#define RL_ABI_VERSION 3
 
 typedef enum rl_status {
   RL_OK = 0,
@@ -134,8 +134,18 @@ typedef struct rl_loss_report {
  *     its other rows keep its own contribution.
  * Requirements: the output pointer is this rank's view of the symmetric buffer
  * whose multicast VA is `multicast`; each flag array holds rl_nvls_flag_count()
- * uint32 entries, zeroed once at allocation; `epoch` increases on every call;
- * all ranks make the same call with the same shapes. */
+ * uint32 entries, zeroed once at allocation; `epoch` increases on every call
+ * (0 < epoch < 2^24; a flag holds epoch * 256 + dU chunk, so a call may run up to
+ * 256 dU chunks); all ranks make the same call with the same shapes. A rank with
+ * T = 0 still takes part (its dW GEMM runs with an empty K range), so DP ranks may
+ * hold different row counts.
+ * Accumulation (d_w_vocab): with accumulate_dw = 1 the rank's new gradient is
+ * added to what its replica already holds (earlier micro-batches, each run with
+ * accumulate_dw and no descriptor) and the SUM is reduced, once, in the dW GEMM of
+ * the last dU chunk: the deferred reduction of a gradient-accumulation step.
+ * Sparse backward (d_hidden_f32, vocab-parallel): the compacted rows are stored
+ * straight into their own rows of the replica, which is zeroed first, and reduced
+ * there; every rank must hold the same coefficients (S3 on identical inputs). */
 #define RL_NVLS_MAX_RANKS 8
 typedef struct rl_nvls_reduce {
   void* multicast;                    /* multicast VA of the symmetric fp32 output buffer  */
@@ -168,8 +178,9 @@ typedef struct rl_loss_outputs {
   int32_t dense_backward;  /* 0 (default): the backward GEMMs run over the rows with a
                               non-zero coef only (RL_BWD_DENSE); 1: over all T rows     */
   const rl_nvls_reduce* d_w_vocab_nvls; /* non-NULL: d_w_vocab is all-reduced in the dW
-                             GEMM epilogue over NVLS (data-parallel ranks); needs
-                             accumulate_dw = 0 and one dU chunk                          */
+                             GEMM epilogue of the last dU chunk over NVLS (data-parallel
+                             ranks); with accumulate_dw = 1 the sum of the replica's old
+                             contents and this step's gradient is reduced                */
   int64_t dz_chunk_rows;   /* rows of the bf16 dU buffer per backward pass; 0 = T (size
                               the workspace with the same value)                         */
 } rl_loss_outputs;
@@ -272,7 +283,8 @@ rl_status rl_bwd(const rl_lm_shape* shape, const uint16_t* hidden, const uint16_
  *   max_sms = 0 for the whole GPU, else the persistent GEMM grids use at most
  *             this many SMs (leaving the rest to a concurrent collective).
  *   dw_nvls / dh_nvls = NULL, or all-reduce d_w_vocab / d_hidden_f32 over an NVLS
- *             group inside the K6 / K5 epilogue (see rl_nvls_reduce; one dU chunk). */
+ *             group inside the K6 / K5 epilogue (see rl_nvls_reduce: dW once, in the
+ *             last dU chunk; dH chunk by chunk, dense or sparse). */
 #define RL_BWD_DU 1
 #define RL_BWD_DW 2
 #define RL_BWD_DH 4
@@ -282,7 +294,7 @@ rl_status rl_bwd(const rl_lm_shape* shape, const uint16_t* hidden, const uint16_
  * row): K3's coef is compacted on the device (order kept), the hidden rows are
  * gathered, and d_hidden rows of skipped tokens are written as zeros. OR
  * RL_BWD_DENSE into `phases` to run over every row (bitwise-reproducible either
- * way; the two differ only in fp32 summation order of dW). dh_nvls forces dense. */
+ * way; the two differ only in fp32 summation order of dW). */
 #define RL_BWD_DENSE 8
 rl_status rl_bwd_ex(const rl_lm_shape* shape, const uint16_t* hidden, const uint16_t* w_vocab,
                     const int32_t* targets, const float* lse, const float* coef, uint16_t* d_hidden,

@@ -20,8 +20,23 @@ NVCC_FLAGS = [
 EXTRA = os.environ.get("RL_NVCC_DEFINES", "").split()
 
 
+STAMP = LIB + ".flags"   # the nvcc flags the current librl.so was built with
+
+
+def _flags_text():
+    return " ".join(NVCC_FLAGS + EXTRA)
+
+
 def _stale():
     if not os.path.exists(LIB):
+        return True
+    # an A/B build (RL_NVCC_DEFINES) and the product build differ only in flags:
+    # rebuild whenever the flags differ from the ones recorded next to the library
+    try:
+        with open(STAMP) as f:
+            if f.read().strip() != _flags_text():
+                return True
+    except OSError:
         return True
     t = os.path.getmtime(LIB)
     deps = [os.path.join(CSRC, d) for d in DEPS] + [os.path.join(ROOT, "include", "rl.h"), __file__]
@@ -41,6 +56,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if verbose:
         sys.stderr.write(r.stderr)
     os.replace(LIB + ".tmp", LIB)
+    with open(STAMP, "w") as f:
+        f.write(_flags_text() + "\n")
     return LIB
 
 

@@ -7,6 +7,8 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <array>
+#include <atomic>
 #include <mutex>
 #include <vector>
 
@@ -223,7 +225,7 @@ rl_status rl_bwd_ex(const rl_lm_shape* shape, const uint16_t* hidden, const uint
   g_launches = 0;
   RL_TRY(check_nvls(dw_nvls, "dw_nvls"));
   RL_TRY(check_nvls(dh_nvls, "dh_nvls"));
-  if (dw_nvls && accumulate_dw) return fail(RL_ERR_INVALID_ARGUMENT, "dw_nvls needs accumulate_dw = 0");
+  if (dw_nvls && !d_w_vocab) return fail(RL_ERR_INVALID_ARGUMENT, "dw_nvls reduces d_w_vocab");
   if (dh_nvls && !d_hidden_f32) return fail(RL_ERR_INVALID_ARGUMENT, "dh_nvls reduces d_hidden_f32");
   if ((phases & RL_BWD_ALL) == 0 || (phases & ~(RL_BWD_ALL | RL_BWD_DENSE)) != 0)
     return fail(RL_ERR_INVALID_ARGUMENT, "phases must be a non-empty RL_BWD_* mask");
@@ -245,8 +247,8 @@ rl_status rl_bwd_ex(const rl_lm_shape* shape, const uint16_t* hidden, const uint
     return fail(RL_ERR_WORKSPACE, "workspace needs %zu bytes, got %zu", L.end, workspace_bytes);
   if ((phases & RL_BWD_ALL) != RL_BWD_ALL && L.chunk < shape->T)
     return fail(RL_ERR_INVALID_ARGUMENT, "partial backward phases need one dU chunk (dz_chunk_rows = 0 or >= T)");
-  if ((dw_nvls || dh_nvls) && L.chunk < shape->T)
-    return fail(RL_ERR_INVALID_ARGUMENT, "NVLS reduction needs one dU chunk (dz_chunk_rows = 0 or >= T)");
+  if ((dw_nvls || dh_nvls) && shape->T > 0 && (shape->T + L.chunk - 1) / L.chunk > kNvlsChunkEpochs)
+    return fail(RL_ERR_INVALID_ARGUMENT, "NVLS reduction supports at most %d dU chunks", kNvlsChunkEpochs);
   DevInfo d;
   RL_TRY(device_info(d));
   int sms = d.sms;
@@ -302,11 +304,9 @@ static rl_status check_step_args(const rl_lm_shape* shape, const rl_loss_params*
     return fail(RL_ERR_ALIGNMENT, "matrix pointers must be 16-byte aligned");
   if (need_logprob && shape->T > 0) RL_NONNULL(out->logprob);
   RL_TRY(check_nvls(out->d_w_vocab_nvls, "d_w_vocab_nvls"));
-  if (out->d_w_vocab_nvls && (out->accumulate_dw || !out->d_w_vocab))
-    return fail(RL_ERR_INVALID_ARGUMENT, "d_w_vocab_nvls needs d_w_vocab and accumulate_dw = 0");
+  if (out->d_w_vocab_nvls && !out->d_w_vocab)
+    return fail(RL_ERR_INVALID_ARGUMENT, "d_w_vocab_nvls reduces d_w_vocab");
   if (out->dz_chunk_rows < 0) return fail(RL_ERR_INVALID_ARGUMENT, "dz_chunk_rows must be >= 0");
-  if (out->d_w_vocab_nvls && out->dz_chunk_rows > 0 && out->dz_chunk_rows < shape->T)
-    return fail(RL_ERR_INVALID_ARGUMENT, "d_w_vocab_nvls needs one dU chunk (dz_chunk_rows = 0 or >= T)");
   return RL_OK;
 }
 
@@ -384,7 +384,9 @@ rl_status rl_policy_loss_fwd_bwd_hostio(const rl_lm_shape* shape, const rl_loss_
     if (e >= T) break;
   }
   const int n_slabs = static_cast<int>(ends.size());
-  HostioStreams& hs = hostio_streams();
+  HostioStreams* hsp = nullptr;
+  RL_TRY(hostio_streams(hsp));
+  HostioStreams& hs = *hsp;
   RL_TRY(hs.ensure(n_slabs));
   // every upload goes through the copy stream, in the order the compute needs it:
   // the small per-token/per-rollout vectors first (event `small`), then the

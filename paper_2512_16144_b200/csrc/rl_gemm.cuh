@@ -120,7 +120,13 @@ struct EpiParams {
   int nvls_lag;                            // reduce the slab finished this many tiles ago
   int nvls_mode;                           // 0 all-reduce (owner tile % world), 1 reduce-scatter by rows
   int64_t nvls_shard;                      // mode 1: rows per rank (a multiple of 32)
-  float* nvls_local;                       // mode 1: this rank's replica (plain stores)
+  float* nvls_local;                       // mode 1 / row_map: this rank's replica (plain stores)
+  int nvls_add;                            // the local store adds to D (TMA reduce-add): D already
+                                           // holds earlier chunks / micro-batches of this rank
+  // EPI_F32_NVLS with a row map (sparse backward, compacted rows): D row r is output
+  // row row_map[r] of nvls_local / nvls_mc (rows >= the device row count are skipped);
+  // the store is a plain per-row global store instead of TMA
+  const int32_t* row_map;
 };
 
 __device__ __forceinline__ void red_release_add(uint32_t* p, uint32_t v) {
@@ -169,9 +175,12 @@ __device__ __forceinline__ int grp_end(const EpiParams& ep, int g) {
 __device__ __forceinline__ int nvls_slab(int tile, uint32_t rank, int q) { return tile * 8 + rank * 4 + q; }
 
 // Owner-side reduction of one slab over the multicast group (see EpiParams::nvls_*).
+// Flags hold the epoch of the last call that published the slab; epochs increase
+// from call to call (and chunk to chunk), so a rank that already moved on to a later
+// chunk still satisfies the wait (its later chunk writes other rows).
 template <int TILE_M, int TN>
 __device__ __noinline__ void nvls_reduce_slab_impl(const EpiParams& ep, const GemmShape& sh, int tile, uint32_t rank,
-                                                   int q, int lane) {
+                                                   int q, int lane, int64_t rows_valid) {
   int m, n;
   tile_coords(tile, sh, m, n);
   const int64_t r0 = static_cast<int64_t>(m) * TILE_M + rank * 128 + q * 32;
@@ -185,16 +194,19 @@ __device__ __noinline__ void nvls_reduce_slab_impl(const EpiParams& ep, const Ge
   if (lane < ep.nvls_world) {
     const uint32_t* f = ep.nvls_flags[lane] + slab;
     const long long t0 = clock64();
-    while (ld_acquire_sys(f) != ep.nvls_epoch) {
+    while (ld_acquire_sys(f) < ep.nvls_epoch) {
       __nanosleep(128);
       if (clock64() - t0 > (1ll << 36)) __trap();
     }
   }
   __syncwarp();
   const int64_t c0 = static_cast<int64_t>(n) * TN;
-  const int64_t rleft = ep.rows - r0, cleft = ep.cols - c0;
+  const int64_t rleft = rows_valid - r0, cleft = ep.cols - c0;
+  if (rleft <= 0) return;
   const int rmax = rleft < 32 ? static_cast<int>(rleft) : 32;
   const int cmax = cleft < TN ? static_cast<int>(cleft) : TN;
+  // output row of slab row i (compacted rows are scattered through the row map)
+  auto orow = [&](int i) -> int64_t { return ep.row_map ? static_cast<int64_t>(ep.row_map[r0 + i]) : r0 + i; };
   // lane l covers columns 4l..4l+3, 128+4l.., ...: TN/128 x 16 B per row, 16 loads in flight
   constexpr int H = TN / 128, RB = 16 / H;
   for (int rb = 0; rb < rmax; rb += RB) {
@@ -204,7 +216,7 @@ __device__ __noinline__ void nvls_reduce_slab_impl(const EpiParams& ep, const Ge
 #pragma unroll
       for (int h = 0; h < H; ++h) {
         const int c = h * 128 + lane * 4;
-        if (rb + i < rmax && c < cmax) mc_ld_reduce_v4(ep.nvls_mc + (r0 + rb + i) * ep.cols + c0 + c, v[i][h]);
+        if (rb + i < rmax && c < cmax) mc_ld_reduce_v4(ep.nvls_mc + orow(rb + i) * ep.cols + c0 + c, v[i][h]);
       }
 #pragma unroll
     for (int i = 0; i < RB; ++i)
@@ -212,7 +224,7 @@ __device__ __noinline__ void nvls_reduce_slab_impl(const EpiParams& ep, const Ge
       for (int h = 0; h < H; ++h) {
         const int c = h * 128 + lane * 4;
         if (rb + i < rmax && c < cmax) {
-          const int64_t off = (r0 + rb + i) * ep.cols + c0 + c;
+          const int64_t off = orow(rb + i) * ep.cols + c0 + c;
           if (ep.nvls_mode == 0)
             mc_st_v4(ep.nvls_mc + off, v[i][h]);
           else
@@ -233,10 +245,12 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   constexpr int NACC = NB == 1 ? 2 : 1;       // TMEM accumulators (512 columns in total)
   constexpr int B_STAGE_ALL = NB * TL::B_STAGE;
   GemmShape sh = sh_in;
+  int64_t rows_valid = ep.rows;  // D rows that hold data (dyn_mode 1: the device row count)
   if (sh.dyn_mode != 0) {
     const int cnt = *sh.dyn_count;
     if (sh.dyn_mode == 1) {
       sh.m_blocks = (cnt + TL::TILE_M - 1) / TL::TILE_M;
+      if (cnt < rows_valid) rows_valid = cnt;
     } else {
       sh.k_blocks = (cnt + BK - 1) / BK;
       sh.k_per_split = sh.k_blocks;
@@ -553,7 +567,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     int chunk_ctr = 0;
     int it = 0;  // tile iteration of this CTA
     auto nvls_reduce_slab = [&](const EpiParams& e, const GemmShape& g, int t, uint32_t r, int qq, int l) {
-      nvls_reduce_slab_impl<TL::TILE_M, TN>(e, g, t, r, qq, l);
+      nvls_reduce_slab_impl<TL::TILE_M, TN>(e, g, t, r, qq, l, rows_valid);
     };
     auto release_tmem = [&](int a) {
       tc_fence_before();
@@ -731,6 +745,24 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   #pragma unroll
               for (int j = 0; j < 32; ++j) w[j] = empty_k ? 0u : r0[j];
             }
+            if constexpr (MODE == EPI_F32_NVLS) {
+              if (ep.row_map != nullptr) {
+                // compacted rows: this thread's 128-byte piece of its row goes straight to
+                // output row row_map[row] of the local replica
+                const int64_t col = static_cast<int64_t>(n0) + c * 32;
+                if (row < rows_valid && col < ep.cols) {
+                  float* dst = ep.nvls_local + static_cast<int64_t>(ep.row_map[row]) * ep.cols + col;
+                  if (col + 32 <= ep.cols) {
+  #pragma unroll
+                    for (int j = 0; j < 8; ++j)
+                      reinterpret_cast<uint4*>(dst)[j] = make_uint4(w[4 * j], w[4 * j + 1], w[4 * j + 2], w[4 * j + 3]);
+                  } else {
+                    for (int j = 0; j < static_cast<int>(ep.cols - col); ++j) dst[j] = __uint_as_float(w[j]);
+                  }
+                }
+                continue;
+              }
+            }
             const uint32_t buf = buf0 + (chunk_ctr & 1) * EPI_BUF_BYTES;
             if (lane == 0) bulk_wait_read<1>();
             __syncwarp();
@@ -742,7 +774,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
               const int c1 = GROUPED ? tile_row0 + rank * 128 + q * 32
                                      : m * TL::TILE_M + rank * 128 + q * 32 +
                                            (tile / (sh.m_blocks * sh.n_blocks)) * sh.split_rows;
-              if constexpr (MODE == EPI_F32_ADD)
+              if (MODE == EPI_F32_ADD || (MODE == EPI_F32_NVLS && ep.nvls_add))
                 tma_reduce_add_2d(&tmC, sEpi + (buf - smem_u32(sEpi)), c0, c1);
               else
                 tma_store_2d(&tmC, sEpi + (buf - smem_u32(sEpi)), c0, c1);
@@ -754,6 +786,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       }
       if constexpr (MODE == EPI_F32_NVLS) {
         // publish this warp's slab once its stores are globally visible
+        if (ep.row_map != nullptr) fence_sys();  // every lane's plain row stores
+        __syncwarp();
         if (lane == 0) {
           bulk_wait_all();
           fence_async_global();

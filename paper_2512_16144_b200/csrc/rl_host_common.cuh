@@ -69,6 +69,15 @@ rl_status fail(rl_status s, const char* fmt, ...) {
     ++g_launches;                                                                              \
   } while (0)
 
+#define RL_TRY(x)                  \
+  do {                             \
+    rl_status s_ = (x);            \
+    if (s_ != RL_OK) return s_;    \
+  } while (0)
+
+#define RL_NONNULL(p) \
+  if (!(p)) return fail(RL_ERR_INVALID_ARGUMENT, "%s is NULL", #p)
+
 // ------------------------------------------------------------- device info
 struct DevInfo {
   int sms = 0;

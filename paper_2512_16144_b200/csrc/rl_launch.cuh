@@ -47,43 +47,24 @@ rl_status make_map(CUtensorMap* m, const void* ptr, bool f32, int64_t inner, int
 }
 
 // ----------------------------------------------------------------- GEMMs
+// Tuning knobs are read from the environment once per process, in thread-safe
+// static initialisers (C++11 magic statics), and never change afterwards.
+
 // CTA-pair (cta_group::2, 256x256 tiles) by default; RL_CTA_GROUP=1 selects the
 // single-CTA 128x256 variant (kept for A/B measurements and as a fallback).
 int cta_group() {
-  static int cg = [] {
+  static const int cg = [] {
     const char* e = getenv("RL_CTA_GROUP");
     return (e && atoi(e) == 1) ? 1 : 2;
   }();
   return cg;
 }
 
-// Raster group (in m-blocks) per GEMM: tiles walk n inside groups of this many
-// m-blocks. Defaults chosen from the sweep in DESIGN.md §5; RL_GROUP_M_<K>
-// overrides (K in FWD, DZ, DH, DW) for measurements.
 // Raster group of the wide dH / dW GEMMs: tiles walk n inside groups of 2 m-blocks.
 // DRAM reads per launch at GLM-16k: 8 -> 17.3 GB, 4 -> 15.6, 2 -> 14.7; step -0.8 ms
 // (profiles/r01/raster_traffic/, bwd_group_ab/).
 constexpr int kGroupMBwd = 2;
 
-int group_m_for(int kid, int dflt) {
-  static int cache[16];
-  static bool init[16] = {};
-  if (!init[kid]) {
-    const char* names[16] = {nullptr, "RL_GROUP_M_FWD", nullptr, nullptr, nullptr, "RL_GROUP_M_DZ",
-                             "RL_GROUP_M_DH", "RL_GROUP_M_DW", nullptr, "RL_GROUP_M_NS"};
-    const char* e = names[kid] ? getenv(names[kid]) : nullptr;
-    cache[kid] = (e && atoi(e) > 0) ? atoi(e) : dflt;
-    init[kid] = true;
-  }
-  return cache[kid];
-}
-
-// Soft k-barrier between producers (see EpiParams::sync_*): every RL_SYNC_EVERY
-// k-blocks (default 32, 16 for the wide dH/dW GEMMs; 0 = off), at most RL_SYNC_SLACK sync points of lead
-// (default 2). Keeping the CTAs that share operands inside one L2 window cuts
-// K5/K6 DRAM reads by ~1/3 and lets the power-capped clock rise (~6% per step,
-// profiles/r01/). Correctness never depends on it (the wait is bounded).
-// Per-GEMM overrides: RL_SYNC_EVERY_<K>, RL_SYNC_SLACK_<K> (K in FWD, DZ, DH, DW, NS).
 const char* kid_suffix(int kid) {
   switch (kid) {
     case RL_K_FWD_GEMM: return "FWD";
@@ -94,25 +75,52 @@ const char* kid_suffix(int kid) {
     default: return "OTHER";
   }
 }
-int env_int(const char* base, int kid, int dflt) {
-  char name[64];
-  snprintf(name, sizeof(name), "%s_%s", base, kid_suffix(kid));
-  const char* e = getenv(name);
-  if (!e) e = getenv(base);
-  return e ? atoi(e) : dflt;
-}
-int sync_every_for(int kid) {
-  static int cache[32];
-  static bool init[32] = {};
-  if (kid < 0 || kid >= 32) return 0;
-  if (!init[kid]) {
-    // 16 for the wide dH / dW GEMMs (their 48 KB k-blocks move twice the bytes per
-    // window): DRAM reads 23.4 -> 17.3 GB each, step 60.7 -> 59.6 ms
-    // (profiles/r01/sync_window_ab/); 32 elsewhere
-    cache[kid] = env_int("RL_SYNC_EVERY", kid, (kid == RL_K_DH_GEMM || kid == RL_K_DW_GEMM) ? 16 : 32);
-    init[kid] = true;
+constexpr int kKnobKids = 32;
+// getenv("<base>_<K>"), else getenv("<base>"), else `unset`, for every kernel id
+std::array<int, kKnobKids> env_table(const char* base, int unset) {
+  std::array<int, kKnobKids> t;
+  for (int kid = 0; kid < kKnobKids; ++kid) {
+    char name[64];
+    snprintf(name, sizeof(name), "%s_%s", base, kid_suffix(kid));
+    const char* e = getenv(name);
+    if (!e) e = getenv(base);
+    t[kid] = e ? atoi(e) : unset;
   }
-  return cache[kid];
+  return t;
+}
+
+// Raster group (in m-blocks) per GEMM: tiles walk n inside groups of this many
+// m-blocks. Defaults chosen from the sweep in DESIGN.md §5 (passed by the call
+// site); RL_GROUP_M_<K> (K in FWD, DZ, DH, DW, NS) overrides for measurements.
+int group_m_for(int kid, int dflt) {
+  static const std::array<int, kKnobKids> env = [] {
+    std::array<int, kKnobKids> t;
+    for (int kid = 0; kid < kKnobKids; ++kid) {
+      char name[64];
+      snprintf(name, sizeof(name), "RL_GROUP_M_%s", kid_suffix(kid));
+      const char* e = getenv(name);
+      t[kid] = e ? atoi(e) : 0;
+    }
+    return t;
+  }();
+  if (kid < 0 || kid >= kKnobKids) return dflt;
+  return env[kid] > 0 ? env[kid] : dflt;
+}
+
+// Soft k-barrier between producers (see EpiParams::sync_*): every RL_SYNC_EVERY
+// k-blocks (default 32, 16 for the wide dH/dW GEMMs; 0 = off), at most RL_SYNC_SLACK sync points of lead
+// (default 2). Keeping the CTAs that share operands inside one L2 window cuts
+// K5/K6 DRAM reads by ~1/3 and lets the power-capped clock rise (~6% per step,
+// profiles/r01/). Correctness never depends on it (the wait is bounded).
+// Per-GEMM overrides: RL_SYNC_EVERY_<K>, RL_SYNC_SLACK_<K> (K in FWD, DZ, DH, DW, NS).
+int sync_every_for(int kid) {
+  static const std::array<int, kKnobKids> env = env_table("RL_SYNC_EVERY", -1);
+  if (kid < 0 || kid >= kKnobKids) return 0;
+  // 16 for the wide dH / dW GEMMs (their 48 KB k-blocks move twice the bytes per
+  // window): DRAM reads 23.4 -> 17.3 GB each, step 60.7 -> 59.6 ms
+  // (profiles/r01/sync_window_ab/); 32 elsewhere
+  if (env[kid] >= 0) return env[kid];
+  return (kid == RL_K_DH_GEMM || kid == RL_K_DW_GEMM) ? 16 : 32;
 }
 // Wide 256 x 512 pair tiles (NB = 2, rl_gemm.cuh): RL_WIDE[_<K>] = 0/1, default on
 // for K1 (FWD), K5 (DH), K6 (DW) and the Newton-Schulz GEMMs (NS: 41.0 -> 38.6 ms); RL_SKEW = 0/2/3 k-blocks of block-0-first MMA
@@ -120,35 +128,38 @@ int sync_every_for(int kid) {
 // half. K4 (DZ) stays narrow: its exp + bf16-store epilogue per half is longer
 // than that cover (measured: K4 15.6 -> 17.9 ms wide, K1 15.6 -> 15.2 ms).
 bool wide_for(int kid) {
-  static int cache[32];
-  static bool init[32] = {};
-  if (kid < 0 || kid >= 32) return false;
-  if (!init[kid]) {
-    const bool dflt = kid == RL_K_FWD_GEMM || kid == RL_K_DH_GEMM || kid == RL_K_DW_GEMM || kid == RL_K_NS_GEMM;
-    cache[kid] = env_int("RL_WIDE", kid, dflt ? 1 : 0);
-    init[kid] = true;
-  }
-  return cache[kid] != 0;
+  static const std::array<int, kKnobKids> env = env_table("RL_WIDE", -1);
+  if (kid < 0 || kid >= kKnobKids) return false;
+  if (env[kid] >= 0) return env[kid] != 0;
+  return kid == RL_K_FWD_GEMM || kid == RL_K_DH_GEMM || kid == RL_K_DW_GEMM || kid == RL_K_NS_GEMM;
 }
 int skew() {
-  static int v = -1;
-  if (v < 0) {
+  static const int v = [] {
     const char* e = getenv("RL_SKEW");
-    v = e ? atoi(e) : 3;
-    if (v != 0 && v != 2) v = 3;
-  }
+    const int x = e ? atoi(e) : 3;
+    return (x == 0 || x == 2) ? x : 3;
+  }();
   return v;
 }
 int sync_slack_for(int kid) {
-  static int cache[32];
-  static bool init[32] = {};
-  if (kid < 0 || kid >= 32) return 2;
-  if (!init[kid]) {
-    cache[kid] = env_int("RL_SYNC_SLACK", kid, 2);
-    init[kid] = true;
-  }
-  return cache[kid];
+  static const std::array<int, kKnobKids> env = env_table("RL_SYNC_SLACK", -1);
+  if (kid < 0 || kid >= kKnobKids) return 2;
+  return env[kid] >= 0 ? env[kid] : 2;
 }
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) is per device: one bit per
+// device and kernel instantiation records that it was set.
+template <typename K>
+rl_status ensure_smem_attr(K kern, int smem, std::atomic<uint64_t>& done) {
+  int dev = 0;
+  RL_CUDA(cudaGetDevice(&dev));
+  const uint64_t bit = dev < 64 ? (uint64_t(1) << dev) : 0;
+  if (bit && (done.load(std::memory_order_acquire) & bit)) return RL_OK;
+  RL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  done.fetch_or(bit, std::memory_order_release);
+  return RL_OK;
+}
+
 constexpr int kMaxSyncPoints = 1 << 16;
 thread_local uint32_t* g_sync_ctr = nullptr;  // set per call from the workspace
 
@@ -165,22 +176,21 @@ rl_status launch_gemm_cg(int kid, const CUtensorMap& a, const CUtensorMap& b, co
   auto kern = rl::gemm_kernel<MODE, A_MN, B_MN, CG, S, NB, SKEW>;
   constexpr int smem = rl::gemm_smem_bytes<CG, S, false, NB>();
   static_assert(smem <= 232448, "dynamic shared memory over 227 KB");
-  static bool attr_set = false;  // per instantiation
-  if (!attr_set) {
-    RL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    attr_set = true;
-  }
+  static std::atomic<uint64_t> attr_done{0};  // per instantiation, one bit per device
+  RL_TRY(ensure_smem_attr(kern, smem, attr_done));
   using TL = rl::Tiling<CG>;
   rl::GemmShape sh;
   sh.m_blocks = static_cast<int>((M + TL::TILE_M - 1) / TL::TILE_M);
   sh.n_blocks = static_cast<int>((N + rl::BN * NB - 1) / (rl::BN * NB));
   sh.k_blocks = static_cast<int>((K + rl::BK - 1) / rl::BK);
   sh.group_m = group_m;
-  if (sh.k_blocks == 0) return fail(RL_ERR_SHAPE, "GEMM with K = 0");
-  if (k_splits < 1) k_splits = 1;
-  if (k_splits > sh.k_blocks) k_splits = sh.k_blocks;
-  sh.k_per_split = (sh.k_blocks + k_splits - 1) / k_splits;
-  sh.k_splits = (sh.k_blocks + sh.k_per_split - 1) / sh.k_per_split;
+  // K = 0 only for the NVLS epilogue (a rank with no rows still stores zeros, or adds
+  // nothing, and takes part in the reduction of every slab)
+  if (sh.k_blocks == 0 && MODE != rl::EPI_F32_NVLS) return fail(RL_ERR_SHAPE, "GEMM with K = 0");
+  if (k_splits < 1 || sh.k_blocks == 0) k_splits = 1;
+  if (k_splits > sh.k_blocks && sh.k_blocks > 0) k_splits = sh.k_blocks;
+  sh.k_per_split = sh.k_blocks > 0 ? (sh.k_blocks + k_splits - 1) / k_splits : 0;
+  sh.k_splits = sh.k_blocks > 0 ? (sh.k_blocks + sh.k_per_split - 1) / sh.k_per_split : 1;
   sh.split_rows = split_rows;
   sh.dyn_count = dyn_count;
   sh.dyn_mode = dyn_count ? dyn_mode : 0;
@@ -256,11 +266,8 @@ rl_status launch_grouped_cg(const CUtensorMap& a, const CUtensorMap& b, const CU
   constexpr int S = CG == 2 ? 5 : 3;
   auto kern = rl::gemm_kernel<rl::EPI_BF16_GROUPED, false, false, CG, S>;
   constexpr int smem = rl::gemm_smem_bytes<CG, S, true>();
-  static bool attr_set = false;
-  if (!attr_set) {
-    RL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    attr_set = true;
-  }
+  static std::atomic<uint64_t> attr_done{0};
+  RL_TRY(ensure_smem_attr(kern, smem, attr_done));
   using TL = rl::Tiling<CG>;
   rl::GemmShape sh = {};
   sh.n_blocks = static_cast<int>((N + rl::BN - 1) / rl::BN);

@@ -94,10 +94,10 @@ rl_status ns_impl(const float* g, int64_t M, int64_t N, int32_t steps, uint16_t*
     e.rows = K;
     e.cols = K;
     if (tall) {  // A = X^T X : [N x N], K-dim = M
-      RL_TRY((launch_gemm<rl::EPI_F32, true, true>(RL_K_NS_GEMM, t_xm, t_xm, t_g32, N, N, M, 8, e, sms, st,
+      RL_TRY((launch_gemm<rl::EPI_F32, true, true>(RL_K_NS_GEMM, t_xm, t_xm, t_g32, N, N, M, group_m_for(RL_K_NS_GEMM, 8), e, sms, st,
                                                    l.splits, static_cast<int>(K))));
     } else {     // A = X X^T : [M x M], K-dim = N
-      RL_TRY((launch_gemm<rl::EPI_F32, false, false>(RL_K_NS_GEMM, t_xk, t_xb, t_g32, M, M, N, 8, e, sms, st,
+      RL_TRY((launch_gemm<rl::EPI_F32, false, false>(RL_K_NS_GEMM, t_xk, t_xb, t_g32, M, M, N, group_m_for(RL_K_NS_GEMM, 8), e, sms, st,
                                                      l.splits, static_cast<int>(K))));
     }
     {
@@ -105,7 +105,7 @@ rl_status ns_impl(const float* g, int64_t M, int64_t N, int32_t steps, uint16_t*
       rl::split_reduce_cast_kernel<<<eblocks, 256, 0, st>>>(parts, l.splits, K * K, g32, g16);
     }
     RL_CHECK_LAUNCH();
-    RL_TRY((launch_gemm<rl::EPI_F32, false, true>(RL_K_NS_GEMM, t_g16k, t_g16m, t_g2, K, K, K, 8, e, sms, st)));
+    RL_TRY((launch_gemm<rl::EPI_F32, false, true>(RL_K_NS_GEMM, t_g16k, t_g16m, t_g2, K, K, K, group_m_for(RL_K_NS_GEMM, 8), e, sms, st)));
     {
       ProfScope ps(RL_K_NS_AUX, st);
       rl::ns_poly_kernel<<<eblocks, 256, 0, st>>>(g32, g2, K, ca, cb, cc, c16);
@@ -114,9 +114,9 @@ rl_status ns_impl(const float* g, int64_t M, int64_t N, int32_t steps, uint16_t*
     e.rows = M;
     e.cols = N;
     if (tall) {  // X' = X C : [M x N], K-dim = N
-      RL_TRY((launch_gemm<rl::EPI_BF16, false, true>(RL_K_NS_GEMM, t_xk, t_c16m, t_out, M, N, N, 8, e, sms, st)));
+      RL_TRY((launch_gemm<rl::EPI_BF16, false, true>(RL_K_NS_GEMM, t_xk, t_c16m, t_out, M, N, N, group_m_for(RL_K_NS_GEMM, 8), e, sms, st)));
     } else {     // X' = C X : [M x N], K-dim = M
-      RL_TRY((launch_gemm<rl::EPI_BF16, false, true>(RL_K_NS_GEMM, t_c16k, t_xm, t_out, M, N, M, 8, e, sms, st)));
+      RL_TRY((launch_gemm<rl::EPI_BF16, false, true>(RL_K_NS_GEMM, t_c16k, t_xm, t_out, M, N, M, group_m_for(RL_K_NS_GEMM, 8), e, sms, st)));
     }
     src = dst;
   }
@@ -162,7 +162,7 @@ rl_status ns_shard_gram_impl(int j, const float* g, const double* sumsq, int64_t
   rl::EpiParams e = {};
   e.rows = K;
   e.cols = K;
-  RL_TRY((launch_gemm<rl::EPI_F32, true, true>(RL_K_NS_GEMM, t_xm, t_xm, t_g32, N, N, M, 8, e, sms, st, l.splits,
+  RL_TRY((launch_gemm<rl::EPI_F32, true, true>(RL_K_NS_GEMM, t_xm, t_xm, t_g32, N, N, M, group_m_for(RL_K_NS_GEMM, 8), e, sms, st, l.splits,
                                                static_cast<int>(K))));
   {
     ProfScope ps(RL_K_NS_AUX, st);
@@ -199,7 +199,7 @@ rl_status ns_shard_apply_impl(int j, int steps, const float* gram, int64_t M, in
   rl::EpiParams e = {};
   e.rows = K;
   e.cols = K;
-  RL_TRY((launch_gemm<rl::EPI_F32, false, true>(RL_K_NS_GEMM, t_g16k, t_g16m, t_g2, K, K, K, 8, e, sms, st)));
+  RL_TRY((launch_gemm<rl::EPI_F32, false, true>(RL_K_NS_GEMM, t_g16k, t_g16m, t_g2, K, K, K, group_m_for(RL_K_NS_GEMM, 8), e, sms, st)));
   {
     ProfScope ps(RL_K_NS_AUX, st);
     rl::ns_poly_kernel<<<8 * sms, 256, 0, st>>>(gram, g2, K, ca, cb, cc, c16);
@@ -207,26 +207,18 @@ rl_status ns_shard_apply_impl(int j, int steps, const float* gram, int64_t M, in
   RL_CHECK_LAUNCH();
   e.rows = M;
   e.cols = N;
-  RL_TRY((launch_gemm<rl::EPI_BF16, false, true>(RL_K_NS_GEMM, t_xk, t_c16m, t_out, M, N, N, 8, e, sms, st)));
+  RL_TRY((launch_gemm<rl::EPI_BF16, false, true>(RL_K_NS_GEMM, t_xk, t_c16m, t_out, M, N, N, group_m_for(RL_K_NS_GEMM, 8), e, sms, st)));
   return RL_OK;
 }
 
-// Side stream + events of the host-I/O call (per host thread and device).
+// Side stream + events of the host-I/O call, one set per host thread and device
+// (streams and events belong to the device that was current when they were made,
+// so a thread that switches devices gets another set instead of dropping this one).
 struct HostioStreams {
-  int dev = -1;
   cudaStream_t copy = nullptr;
   cudaEvent_t start = nullptr, small = nullptr;
   std::vector<cudaEvent_t> slab;
   rl_status ensure(int n) {
-    int d = 0;
-    RL_CUDA(cudaGetDevice(&d));
-    if (d != dev) {
-      copy = nullptr;
-      start = nullptr;
-      small = nullptr;
-      slab.clear();
-      dev = d;
-    }
     if (!copy) RL_CUDA(cudaStreamCreateWithFlags(&copy, cudaStreamNonBlocking));
     if (!start) RL_CUDA(cudaEventCreateWithFlags(&start, cudaEventDisableTiming));
     if (!small) RL_CUDA(cudaEventCreateWithFlags(&small, cudaEventDisableTiming));
@@ -238,9 +230,14 @@ struct HostioStreams {
     return RL_OK;
   }
 };
-HostioStreams& hostio_streams() {
-  thread_local HostioStreams h;
-  return h;
+constexpr int kMaxDevices = 64;
+rl_status hostio_streams(HostioStreams*& out) {
+  thread_local std::array<HostioStreams, kMaxDevices> per_device;
+  int d = 0;
+  RL_CUDA(cudaGetDevice(&d));
+  if (d < 0 || d >= kMaxDevices) return fail(RL_ERR_UNSUPPORTED, "device index %d out of range", d);
+  out = &per_device[d];
+  return RL_OK;
 }
 
 }  // namespace

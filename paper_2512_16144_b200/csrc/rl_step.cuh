@@ -82,16 +82,21 @@ int64_t nvls_shard_rows(int64_t rows, int32_t world) {
   return world > 0 ? (rows + 32 * int64_t(world) - 1) / (32 * int64_t(world)) * 32 : rows;
 }
 
-// e.rows must be set first (the reduce-scatter shard is a row range of D)
-void set_nvls(rl::EpiParams& e, const rl_nvls_reduce* n, const float* local) {
-  e.nvls_local = const_cast<float*>(local);
+// e.rows must be set first (the reduce-scatter shard is a row range of D).
+// `local` is this rank's replica at D's row 0 and `mc_off` the same offset (in
+// floats) into the multicast VA. Each call's flags carry epoch * 256 + chunk, so
+// epochs increase from chunk to chunk and from call to call (rl_nvls_reduce.epoch
+// < 2^24, at most 256 chunks per call).
+constexpr int kNvlsChunkEpochs = 256;
+void set_nvls(rl::EpiParams& e, const rl_nvls_reduce* n, float* local, int64_t mc_off = 0, int chunk = 0) {
+  e.nvls_local = local;
   e.nvls_mode = n->mode;
   e.nvls_shard = nvls_shard_rows(e.rows, n->world);
-  e.nvls_mc = static_cast<float*>(n->multicast);
+  e.nvls_mc = static_cast<float*>(n->multicast) + mc_off;
   for (int r = 0; r < rl::NVLS_MAX_RANKS; ++r) e.nvls_flags[r] = n->flags[r];
   e.nvls_rank = n->rank;
   e.nvls_world = n->world;
-  e.nvls_epoch = n->epoch;
+  e.nvls_epoch = n->epoch * kNvlsChunkEpochs + static_cast<uint32_t>(chunk);
   e.nvls_lag = n->lag > 0 ? n->lag : 2;
 }
 
@@ -102,10 +107,28 @@ rl_status check_nvls(const rl_nvls_reduce* n, const char* what) {
     return fail(RL_ERR_INVALID_ARGUMENT, "%s: need 2 <= world <= %d and 0 <= rank < world", what, RL_NVLS_MAX_RANKS);
   for (int r = 0; r < n->world; ++r)
     if (!n->flags[r]) return fail(RL_ERR_INVALID_ARGUMENT, "%s: flags[%d] is NULL", what, r);
-  if (n->epoch == 0) return fail(RL_ERR_INVALID_ARGUMENT, "%s: epoch must be > 0 (flags start at 0)", what);
+  if (n->epoch == 0 || n->epoch >= (1u << 24))
+    return fail(RL_ERR_INVALID_ARGUMENT, "%s: need 0 < epoch < 2^24 (flags start at 0)", what);
   if (n->mode != RL_NVLS_ALL_REDUCE && n->mode != RL_NVLS_REDUCE_SCATTER)
     return fail(RL_ERR_INVALID_ARGUMENT, "%s: unknown mode %d", what, n->mode);
   return RL_OK;
+}
+
+// K6 of the last dU chunk, with the NVLS dW reduction fused: adds to d_w_vocab when it
+// already holds earlier chunks or micro-batches (`add`). With K = 0 (a rank with no
+// rows) the epilogue stores zeros (or adds nothing) and still takes part in the
+// reduction of every slab, so the other ranks never wait for it.
+rl_status launch_dw_nvls(const CUtensorMap& t_dz_mn, const CUtensorMap& t_h_mn, const CUtensorMap& t_dw, int64_t V,
+                         int64_t H, int64_t K, float* dw, const rl_nvls_reduce* n, bool add, int sms, cudaStream_t st,
+                         const int* dyn_count = nullptr) {
+  rl::EpiParams e6 = {};
+  e6.rows = V;
+  e6.cols = H;
+  set_nvls(e6, n, dw);
+  e6.nvls_add = add ? 1 : 0;
+  return launch_gemm<rl::EPI_F32_NVLS, true, true>(RL_K_DW_GEMM, t_dz_mn, t_h_mn, t_dw, V, H, K,
+                                                    group_m_for(RL_K_DW_GEMM, kGroupMBwd), e6, sms, st, 1, 0,
+                                                    dyn_count, dyn_count ? 2 : 0);
 }
 
 // Sparse backward: the same K4 -> K6 -> K5 over the rows whose coefficient is
@@ -114,7 +137,7 @@ rl_status check_nvls(const rl_nvls_reduce* n, const char* what) {
 rl_status bwd_sparse_impl(const rl_lm_shape* s, const uint16_t* hidden, const uint16_t* w, const int32_t* targets,
                           const float* lse, const float* coef, uint16_t* dh, float* dh32, float* dw,
                           int accumulate_dw, uint8_t* ws, const WsLayout& L, int sms, cudaStream_t st, int phases,
-                          const rl_nvls_reduce* dw_nvls) {
+                          const rl_nvls_reduce* dw_nvls, const rl_nvls_reduce* dh_nvls) {
   const int64_t T = s->T, H = s->H, V = s->V_local;
   const int64_t chunk = L.chunk;
   const int n_chunks = static_cast<int>((T + chunk - 1) / chunk);
@@ -184,10 +207,8 @@ rl_status bwd_sparse_impl(const rl_lm_shape* s, const uint16_t* hidden, const ui
       rl::EpiParams e6 = {};
       e6.rows = V;
       e6.cols = H;
-      if (dw_nvls) {
-        set_nvls(e6, dw_nvls, dw);
-        RL_TRY((launch_gemm<rl::EPI_F32_NVLS, true, true>(RL_K_DW_GEMM, t_dz_mn, t_h_mn, t_dw, V, H, rows,
-                                                            group_m_for(RL_K_DW_GEMM, kGroupMBwd), e6, sms, st, 1, 0, cnt, 2)));
+      if (dw_nvls && ch == n_chunks - 1) {
+        RL_TRY(launch_dw_nvls(t_dz_mn, t_h_mn, t_dw, V, H, rows, dw, dw_nvls, ch > 0 || accumulate_dw, sms, st, cnt));
       } else if (ch == 0 && !accumulate_dw) {
         RL_TRY((launch_gemm<rl::EPI_F32, true, true>(RL_K_DW_GEMM, t_dz_mn, t_h_mn, t_dw, V, H, rows,
                                                      group_m_for(RL_K_DW_GEMM, kGroupMBwd), e6, sms, st, 1, 0, cnt, 2)));
@@ -201,6 +222,18 @@ rl_status bwd_sparse_impl(const rl_lm_shape* s, const uint16_t* hidden, const ui
       rl::EpiParams e5 = {};
       e5.rows = rows;
       e5.cols = H;
+      if (dh_nvls) {
+        // the compact rows go straight to their own rows of the (zeroed) symmetric
+        // d_hidden_f32 and are reduced there: every rank holds the same compaction
+        // (S3 ran on identical inputs), so row_map is the same on all of them
+        RL_TRY(make_map(&t_dh, dh_c, true, H, rows, H, 32, 32));
+        set_nvls(e5, dh_nvls, dh32, 0, ch);
+        e5.row_map = idx + c0;
+        RL_TRY((launch_gemm<rl::EPI_F32_NVLS, false, true>(RL_K_DH_GEMM, t_dz_k, t_w_mn, t_dh, rows, H, V,
+                                                             group_m_for(RL_K_DH_GEMM, kGroupMBwd), e5, sms, st, 1, 0,
+                                                             cnt, 1)));
+        continue;
+      }
       if (dh) {
         RL_TRY(make_map(&t_dh, dh_c, false, H, rows, H, 64, 32));
         RL_TRY((launch_gemm<rl::EPI_BF16, false, true>(RL_K_DH_GEMM, t_dz_k, t_w_mn, t_dh, rows, H, V,
@@ -230,21 +263,30 @@ rl_status bwd_impl(const rl_lm_shape* s, const uint16_t* hidden, const uint16_t*
                    const rl_nvls_reduce* dw_nvls = nullptr, const rl_nvls_reduce* dh_nvls = nullptr) {
   const int64_t T = s->T, H = s->H, V = s->V_local;
   if (T == 0) {
+    if (dw && dw_nvls && (phases & RL_BWD_DW)) {
+      // no rows on this rank: K6 with an empty K range still joins the reduction
+      CUtensorMap t_any, t_dw;
+      RL_TRY(make_map(&t_any, dw, false, 64, 1, 64, 64, 1));  // never loaded from
+      RL_TRY(make_map(&t_dw, dw, true, H, V, H, 32, 32));
+      g_sync_ctr = nullptr;
+      return launch_dw_nvls(t_any, t_any, t_dw, V, H, 0, dw, dw_nvls, accumulate_dw != 0, sms, st);
+    }
     if (dw && !accumulate_dw) RL_CUDA(cudaMemsetAsync(dw, 0, static_cast<size_t>(V) * H * 4, st));
     return RL_OK;
   }
   uint16_t* dz = reinterpret_cast<uint16_t*>(ws + L.dz);
   const int64_t chunk = L.chunk;
   g_sync_ctr = reinterpret_cast<uint32_t*>(ws + L.sync);
-  if (!(phases & RL_BWD_DENSE) && !dh_nvls)
+  if (!(phases & RL_BWD_DENSE))
     return bwd_sparse_impl(s, hidden, w, targets, lse, coef, dh, dh32, dw, accumulate_dw, ws, L, sms, st, phases,
-                           dw_nvls);
+                           dw_nvls, dh_nvls);
   CUtensorMap t_h_k, t_w_k, t_dz_st, t_dz_k, t_w_mn, t_dh, t_dz_mn, t_h_mn, t_dw;
   RL_TRY(make_map(&t_w_k, w, false, H, V, H, 64, rl::BN / cta_group()));
   RL_TRY(make_map(&t_w_mn, w, false, H, V, H, 64, 64));
   if (dw) RL_TRY(make_map(&t_dw, dw, true, H, V, H, 32, 32));
-  for (int64_t c0 = 0; c0 < T; c0 += chunk) {
+  for (int64_t c0 = 0, ch = 0; c0 < T; c0 += chunk, ++ch) {
     const int64_t rows = (T - c0 < chunk) ? (T - c0) : chunk;
+    const bool last = c0 + rows >= T;
     const uint16_t* hc = hidden + c0 * H;
     RL_TRY(make_map(&t_h_k, hc, false, H, rows, H, 64, kARows));
     RL_TRY(make_map(&t_dz_st, dz, false, V, rows, L.ldz, 64, 32));
@@ -268,10 +310,8 @@ rl_status bwd_impl(const rl_lm_shape* s, const uint16_t* hidden, const uint16_t*
       rl::EpiParams e6 = {};
       e6.rows = V;
       e6.cols = H;
-      if (dw_nvls) {
-        set_nvls(e6, dw_nvls, dw);
-        RL_TRY((launch_gemm<rl::EPI_F32_NVLS, true, true>(RL_K_DW_GEMM, t_dz_mn, t_h_mn, t_dw, V, H, rows,
-                                                            group_m_for(RL_K_DW_GEMM, kGroupMBwd), e6, sms, st)));
+      if (dw_nvls && last) {
+        RL_TRY(launch_dw_nvls(t_dz_mn, t_h_mn, t_dw, V, H, rows, dw, dw_nvls, c0 > 0 || accumulate_dw, sms, st));
       } else if (c0 == 0 && !accumulate_dw) {
         RL_TRY((launch_gemm<rl::EPI_F32, true, true>(RL_K_DW_GEMM, t_dz_mn, t_h_mn, t_dw, V, H, rows, group_m_for(RL_K_DW_GEMM, kGroupMBwd), e6, sms, st)));
       } else {
@@ -290,7 +330,7 @@ rl_status bwd_impl(const rl_lm_shape* s, const uint16_t* hidden, const uint16_t*
       } else {
         RL_TRY(make_map(&t_dh, dh32 + c0 * H, true, H, rows, H, 32, 32));
         if (dh_nvls) {
-          set_nvls(e5, dh_nvls, dh32 + c0 * H);
+          set_nvls(e5, dh_nvls, dh32 + c0 * H, c0 * H, static_cast<int>(ch));
           RL_TRY((launch_gemm<rl::EPI_F32_NVLS, false, true>(RL_K_DH_GEMM, t_dz_k, t_w_mn, t_dh, rows, H, V,
                                                                group_m_for(RL_K_DH_GEMM, kGroupMBwd), e5, sms, st)));
         } else

@@ -93,13 +93,4 @@ rl_status check_params(const rl_loss_params* p) {
   return RL_OK;
 }
 
-#define RL_TRY(x)                  \
-  do {                             \
-    rl_status s_ = (x);            \
-    if (s_ != RL_OK) return s_;    \
-  } while (0)
-
-#define RL_NONNULL(p) \
-  if (!(p)) return fail(RL_ERR_INVALID_ARGUMENT, "%s is NULL", #p)
-
 }  // namespace

@@ -127,12 +127,12 @@ class LibrlPhases:
 
     def full_step(self, shape, params, hidden, w, targets, infer, adv, offsets, loss_mask, *, report, logprob,
                   entropy=None, lse=None, coef=None, keep=None, guarded=None, d_hidden=None, d_w_vocab=None,
-                  d_w_vocab_nvls=None, dz_chunk_rows=0, workspace=None):
+                  d_w_vocab_nvls=None, dz_chunk_rows=0, workspace=None, accumulate_dw=False):
         rl_policy_loss_fwd_bwd(shape, params, hidden, w, targets, infer, adv, offsets, loss_mask, report=report,
                                logprob=logprob, entropy=entropy, lse=lse, coef=coef, token_keep=keep,
                                rollout_guarded=guarded, d_hidden=d_hidden, d_w_vocab=d_w_vocab,
                                d_w_vocab_nvls=d_w_vocab_nvls, dz_chunk_rows=dz_chunk_rows,
-                               dense_backward=bool(self.dense), workspace=workspace)
+                               dense_backward=bool(self.dense), workspace=workspace, accumulate_dw=accumulate_dw)
         self._count()
 
 
@@ -176,11 +176,10 @@ class VocabParallelPolicyLoss:
         self.guarded = torch.empty(num_rollouts, dtype=torch.uint8, device=dev)
         self.adv = torch.empty(num_rollouts, **f32)
         self.report = torch.zeros(48, dtype=torch.uint8, device=dev)
-        # nvls: dH partials are all-reduced inside the K5 epilogue (NVLink multicast)
+        # nvls: dH partials are all-reduced inside the K5 epilogue (NVLink multicast),
+        # chunk by chunk, over all rows (dense) or the compacted rows (sparse backward)
         self.nvls = None
         if nvls:
-            if dz_chunk_rows and dz_chunk_rows < T:
-                raise ValueError("the NVLS dH reduction needs one dU chunk (dz_chunk_rows = 0)")
             self.nvls = NvlsReduction(T, H, rl_nvls_flag_count(self.shape, 1), group, dev)
             self.d_hidden = self.nvls.buf
         else:
@@ -213,7 +212,11 @@ class VocabParallelPolicyLoss:
         """step() with the per-step inputs in pinned HOST memory: the small inputs, then the
         hidden rows in slabs, go up on a copy stream, and the forward partials run slab by
         slab as the rows arrive (each row's partial is independent), so the upload hides
-        under K1. Returns d_hidden like step()."""
+        under K1. Returns d_hidden like step().
+
+        The copies are asynchronous: the host buffers must not be modified until
+        `self.upload_done` (a CUDA event recorded after the last copy) has completed,
+        e.g. `self.upload_done.synchronize()` before refilling them for the next step."""
         dev = w_shard.device
         if getattr(self, "_host_in", None) is None:
             self._host_in = {"hidden": torch.empty(self.T, self.H, dtype=torch.bfloat16, device=dev),
@@ -242,6 +245,7 @@ class VocabParallelPolicyLoss:
                 ev.record()
                 slab_evs.append((r0, r1, ev))
                 r0 = r1
+            self.upload_done = slab_evs[-1][2] if slab_evs else small_ev
         ph = self.ph
         main.wait_event(small_ev)
         ph.group_advantages(d["rewards"], self.G, self.adv)
@@ -320,7 +324,13 @@ class DataParallelPolicyLoss:
         dist.all_reduce(t, group=group)
         return float(t.item())
 
-    def step(self, hidden, w, targets, infer, rewards, offsets, loss_mask, d_w_vocab=None):
+    def step(self, hidden, w, targets, infer, rewards, offsets, loss_mask, d_w_vocab=None, *, accumulate=False,
+             reduce=True):
+        """One micro-batch. Gradient accumulation over micro-batches (the paper's FSDP
+        trainer): pass accumulate=True on all but the first and reduce=False on all
+        but the last; dW is summed locally and reduced once, on the last micro-batch
+        (fused into its dW GEMM with NVLS). Every micro-batch has this engine's T rows
+        and rollouts; D is the global count of loss tokens of the whole step (R5)."""
         ph = self.ph
         ph.group_advantages(rewards, self.G, self.adv)
         if self.nvls is not None:
@@ -328,19 +338,23 @@ class DataParallelPolicyLoss:
                          report=self.report, logprob=self.logprob, entropy=self.entropy, lse=self.lse,
                          coef=self.coef, keep=self.keep, guarded=self.guarded, d_hidden=self.d_hidden,
                          d_w_vocab=self.nvls.buf,
-                         d_w_vocab_nvls=self.nvls.descriptor(mode=1 if self.reduce_scatter else 0),
-                         workspace=self.ws)
+                         d_w_vocab_nvls=(self.nvls.descriptor(mode=1 if self.reduce_scatter else 0)
+                                         if reduce else None),
+                         workspace=self.ws, accumulate_dw=accumulate)
+            if not reduce:
+                return self.nvls.buf                              # this rank's partial sum so far
             self.nvls.barrier()                                   # the exchange, fused into K6's epilogue
             if self.reduce_scatter:
                 r = dist.get_rank(self.group)
                 return self.nvls.buf[r * self.shard_rows:(r + 1) * self.shard_rows]
             return self.nvls.buf
-        if not self.overlap:
+        if not self.overlap or accumulate or not reduce:
             ph.full_step(self.shape, self.params, hidden, w, targets, infer, self.adv, offsets, loss_mask,
                          report=self.report, logprob=self.logprob, entropy=self.entropy, lse=self.lse,
                          coef=self.coef, keep=self.keep, guarded=self.guarded, d_hidden=self.d_hidden,
-                         d_w_vocab=d_w_vocab, workspace=self.ws)
-            dist.all_reduce(d_w_vocab, group=self.group)                                  # the exchange
+                         d_w_vocab=d_w_vocab, workspace=self.ws, accumulate_dw=accumulate)
+            if reduce:
+                dist.all_reduce(d_w_vocab, group=self.group)                              # the exchange
             return d_w_vocab
         # S1..S3, then K4 (dU) and K6 (dW); the dW all-reduce runs on a side stream
         # while K5 (dH) uses the SMs NCCL leaves free.

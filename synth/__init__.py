@@ -23,9 +23,10 @@ import math
 import numpy as np
 
 # stream keys, one per drawn tensor
-_K_HIDDEN, _K_W, _K_TARGETS, _K_REWARDS, _K_DELTA, _K_LENGTHS, _K_SPIKES, _K_MASK = range(8)
+_K_HIDDEN, _K_W, _K_TARGETS, _K_REWARDS, _K_DELTA, _K_LENGTHS, _K_SPIKES, _K_MASK, _K_SAMPLE = range(9)
 
-GENERATOR_VERSION = 1
+# 2: adds `sample_u` (uniforms for sampling targets from the policy)
+GENERATOR_VERSION = 2
 
 
 @dataclasses.dataclass(frozen=True)
@@ -146,6 +147,9 @@ class Batch:
     loss_mask: np.ndarray        # [T] uint8
     delta_noise: np.ndarray      # [T] float64, trainer-minus-inference log-prob noise
     spikes: np.ndarray           # [T] bool, positions whose stored infer log-prob is 0
+    sample_u: np.ndarray         # [T] float64 uniforms in [0, 1): the draw that picks y_t when the
+                                 # targets are sampled from the policy (tests/harness.py); `targets`
+                                 # above is the uniform-id fallback
 
     @property
     def T(self) -> int:
@@ -191,7 +195,8 @@ def make_batch(wl: Workload, seed: int = 0, *, tokens: int | None = None,
             lm[a: a + int(math.floor(wl.prompt_frac * (b - a)))] = 0
     delta = _rng(seed, _K_DELTA).normal(0.0, wl.delta_sigma, size=T)
     spikes = _rng(seed, _K_SPIKES).random(T) < wl.spike_rate
-    return Batch(wl, seed, hid, W, targets, S, offsets.astype(np.int32), lm, delta, spikes)
+    u = _rng(seed, _K_SAMPLE).random(T)
+    return Batch(wl, seed, hid, W, targets, S, offsets.astype(np.int32), lm, delta, spikes, u)
 
 
 def compose_infer_logprobs(logp_ref: np.ndarray, delta_noise: np.ndarray,

@@ -38,7 +38,7 @@ def test_struct_layouts_match_header(lib):
     assert ctypes.sizeof(rl.rl_loss_report) == 48
     assert ctypes.sizeof(rl.rl_loss_outputs) == 104
     assert ctypes.sizeof(rl.rl_nvls_reduce) == 96
-    assert lib.rl_abi_version() == 2
+    assert lib.rl_abi_version() == 3
 
 
 def test_status_strings(lib):

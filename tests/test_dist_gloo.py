@@ -1,7 +1,8 @@
-"""Multi-process (world size 2, gloo, CPU) checks of the N > 1 host logic in
+"""Multi-process (world size 2 and 4, gloo, CPU) checks of the N > 1 host logic in
 paper_2512_16144_b200/parallel.py: vocab sharding, rank-ordered partial gather
-and merge, redundant S3, dH partial reduction, DP with a global denominator and
-the dW reduction. The arithmetic is supplied by `OraclePhases`, a test double
+and merge, redundant S3, dH partial reduction, DP with a global denominator, the
+dW reduction, and gradient accumulation over micro-batches with one deferred
+reduction. The arithmetic is supplied by `OraclePhases`, a test double
 built from the fp64 oracle, so the composition is checked on any machine; the
 GPU path runs the same classes with librl's phases (bench.py, N > 1)."""
 import os
@@ -19,6 +20,7 @@ import synth
 from paper_2512_16144_b200 import parallel
 
 WORLD = 2
+WORLDS = [2, 4]
 
 
 def _free_port():
@@ -76,7 +78,7 @@ class OraclePhases:
 
     def full_step(self, shape, params, hidden, w, targets, infer, adv, offsets, loss_mask, *, report, logprob,
                   entropy=None, lse=None, coef=None, keep=None, guarded=None, d_hidden=None, d_w_vocab=None,
-                  workspace=None):
+                  workspace=None, accumulate_dw=False):
         res = oracle.policy_loss_fwd_bwd(hidden.double().numpy(), w.double().numpy(), targets.long().numpy(),
                                          infer.double().numpy(), None, offsets.numpy(), loss_mask.numpy(),
                                          alpha=params.alpha, beta=params.beta,
@@ -88,7 +90,10 @@ class OraclePhases:
                                          kl_set={v: k for k, v in oracle.KL_SETS.items()}[params.kl_set])
         logprob.copy_(torch.from_numpy(res.logp))
         d_hidden.copy_(torch.from_numpy(res.d_hidden))
-        d_w_vocab.copy_(torch.from_numpy(res.d_w_vocab))
+        if accumulate_dw:
+            d_w_vocab.add_(torch.from_numpy(res.d_w_vocab))
+        else:
+            d_w_vocab.copy_(torch.from_numpy(res.d_w_vocab))
         self.loss = res.report.loss
 
 
@@ -109,7 +114,8 @@ class OraclePhases:
             out.copy_(torch.from_numpy(self.X))
 
 
-WL = synth.Workload("dist", 2, 4, 12, 32, 96, ragged=True, prompt_frac=0.2, delta_sigma=0.8, spike_rate=0.02)
+# 4 prompt groups, so 4 DP ranks each hold a whole group; V = 96 splits over 2 or 4 ranks
+WL = synth.Workload("dist", 4, 4, 12, 32, 96, ragged=True, prompt_frac=0.2, delta_sigma=0.8, spike_rate=0.02)
 
 
 def _batch():
@@ -127,9 +133,9 @@ def _bf16(bits):
 LOSS_KW = [{}, {"variant": "cispo", "kl_tau": 0.375, "kl_set": "all"}]   # 0.375: exact in the fp32 ABI field
 
 
-def _vocab_worker(rank, port, out_dir, kw_i=0):
+def _vocab_worker(rank, port, out_dir, kw_i=0, world=WORLD):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
-    dist.init_process_group("gloo", rank=rank, world_size=WORLD)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
     b, h64, w64, infer = _batch()
     vp = parallel.VocabParallelPolicyLoss(OraclePhases(), T=b.T, H=b.H, V_global=b.V, num_rollouts=len(b.rewards.reshape(-1)),
                                           group_size=WL.group_size, loss_denominator=b.loss_denominator,
@@ -146,17 +152,18 @@ def _vocab_worker(rank, port, out_dir, kw_i=0):
     dist.destroy_process_group()
 
 
-def _dp_worker(rank, port, out_dir, kw_i=0):
+def _dp_worker(rank, port, out_dir, kw_i=0, world=WORLD):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
-    dist.init_process_group("gloo", rank=rank, world_size=WORLD)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
     b, h64, w64, infer = _batch()
-    # rank r takes prompt group r (whole rollouts, so the guard stays local)
+    # rank r takes WL.num_prompts / world whole prompt groups (the guard stays local)
     G = WL.group_size
-    r0, r1 = rank * G, (rank + 1) * G
+    per = WL.num_prompts // world
+    r0, r1 = rank * per * G, (rank + 1) * per * G
     t0, t1 = int(b.rollout_offsets[r0]), int(b.rollout_offsets[r1])
     lm = torch.from_numpy(b.loss_mask[t0:t1].copy())
     D = parallel.DataParallelPolicyLoss.global_denominator(lm)
-    dp = parallel.DataParallelPolicyLoss(OraclePhases(), T=t1 - t0, H=b.H, V=b.V, num_rollouts=G, group_size=G,
+    dp = parallel.DataParallelPolicyLoss(OraclePhases(), T=t1 - t0, H=b.H, V=b.V, num_rollouts=r1 - r0, group_size=G,
                                          loss_denominator=D, device="cpu", d_hidden_dtype=torch.float64,
                                          workspace=False, **LOSS_KW[kw_i])
     for name in ("logprob", "entropy", "lse", "coef", "adv"):
@@ -164,7 +171,8 @@ def _dp_worker(rank, port, out_dir, kw_i=0):
     dw = torch.empty(b.V, b.H, dtype=torch.float64)
     offs = torch.from_numpy((b.rollout_offsets[r0:r1 + 1] - t0).astype(np.int32))
     dp.step(_bf16(b.hidden[t0:t1]), _bf16(b.w_vocab), torch.from_numpy(b.targets[t0:t1].copy()),
-            torch.from_numpy(infer[t0:t1].copy()), torch.from_numpy(b.rewards[rank].copy()), offs, lm, dw)
+            torch.from_numpy(infer[t0:t1].copy()), torch.from_numpy(b.rewards[rank * per:(rank + 1) * per].reshape(-1).copy()),
+            offs, lm, dw)
     loss = torch.tensor([dp.ph.loss], dtype=torch.float64)
     dist.all_reduce(loss)
     np.savez(os.path.join(out_dir, f"dp{rank}.npz"), dh=dp.d_hidden.numpy(), dw=dw.numpy(), t0=t0, t1=t1,
@@ -178,28 +186,82 @@ def _reference(kw_i=0):
                                          b.rollout_offsets, b.loss_mask, **LOSS_KW[kw_i])
 
 
+@pytest.mark.parametrize("world", WORLDS)
 @pytest.mark.parametrize("kw_i", range(len(LOSS_KW)))
-def test_vocab_parallel_composition(tmp_path, kw_i):
-    mp.start_processes(_vocab_worker, args=(_free_port(), str(tmp_path), kw_i), nprocs=WORLD, start_method="spawn")
+def test_vocab_parallel_composition(tmp_path, kw_i, world):
+    mp.start_processes(_vocab_worker, args=(_free_port(), str(tmp_path), kw_i, world), nprocs=world,
+                       start_method="spawn")
     b, ref = _reference(kw_i)
-    outs = [np.load(tmp_path / f"vp{r}.npz") for r in range(WORLD)]
+    outs = [np.load(tmp_path / f"vp{r}.npz") for r in range(world)]
     for o in outs:   # S2/S3 are identical on every rank; dH is the reduced sum
         np.testing.assert_allclose(o["logprob"], ref.logp, atol=1e-6)
         np.testing.assert_allclose(o["coef"], ref.report.coef, atol=1e-9)
         np.testing.assert_allclose(o["dh"], ref.d_hidden, atol=1e-9)
     dw = np.concatenate([o["dw"] for o in outs])
     np.testing.assert_allclose(dw, ref.d_w_vocab, atol=1e-9)
-    assert [int(o["lo"]) for o in outs] == [0, b.V // 2]
+    assert [int(o["lo"]) for o in outs] == [r * (b.V // world) for r in range(world)]
 
 
+@pytest.mark.parametrize("world", WORLDS)
 @pytest.mark.parametrize("kw_i", range(len(LOSS_KW)))
-def test_data_parallel_composition(tmp_path, kw_i):
-    mp.start_processes(_dp_worker, args=(_free_port(), str(tmp_path), kw_i), nprocs=WORLD, start_method="spawn")
+def test_data_parallel_composition(tmp_path, kw_i, world):
+    mp.start_processes(_dp_worker, args=(_free_port(), str(tmp_path), kw_i, world), nprocs=world,
+                       start_method="spawn")
     b, ref = _reference(kw_i)
-    outs = [np.load(tmp_path / f"dp{r}.npz") for r in range(WORLD)]
+    outs = [np.load(tmp_path / f"dp{r}.npz") for r in range(world)]
     for o in outs:
         assert float(o["D"]) == b.loss_denominator            # global D, reading R5
         np.testing.assert_allclose(o["dw"], ref.d_w_vocab, atol=1e-12)   # all-reduced dW
+        np.testing.assert_allclose(o["dh"], ref.d_hidden[int(o["t0"]):int(o["t1"])], atol=1e-12)
+        assert float(o["loss"][0]) == pytest.approx(ref.report.loss, abs=1e-12)
+
+
+def _dp_micro_worker(rank, port, out_dir):
+    """Rank r holds prompt groups 2r and 2r+1 and runs them as two micro-batches
+    (one engine per micro-batch shape): dW accumulates locally (accumulate=True on
+    the second) and is reduced once, on the last (reduce=False on the first)."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=WORLD)
+    b, h64, w64, infer = _batch()
+    G = WL.group_size
+    per = WL.num_prompts // WORLD
+    off = b.rollout_offsets
+    mine = off[rank * per * G], off[(rank + 1) * per * G]
+    D = parallel.DataParallelPolicyLoss.global_denominator(torch.from_numpy(b.loss_mask[mine[0]:mine[1]].copy()))
+    dw = torch.full((b.V, b.H), float("nan"), dtype=torch.float64)   # overwritten by the first micro-batch
+    dh, losses = [], 0.0
+    for j in range(per):
+        g = rank * per + j
+        t0, t1 = int(off[g * G]), int(off[(g + 1) * G])
+        dp = parallel.DataParallelPolicyLoss(OraclePhases(), T=t1 - t0, H=b.H, V=b.V, num_rollouts=G, group_size=G,
+                                             loss_denominator=D, device="cpu", d_hidden_dtype=torch.float64,
+                                             workspace=False)
+        for name in ("logprob", "entropy", "lse", "coef", "adv"):
+            setattr(dp, name, getattr(dp, name).double())
+        offs = torch.from_numpy((off[g * G:(g + 1) * G + 1] - t0).astype(np.int32))
+        dp.step(_bf16(b.hidden[t0:t1]), _bf16(b.w_vocab), torch.from_numpy(b.targets[t0:t1].copy()),
+                torch.from_numpy(infer[t0:t1].copy()), torch.from_numpy(b.rewards[g].copy()), offs,
+                torch.from_numpy(b.loss_mask[t0:t1].copy()), dw, accumulate=j > 0, reduce=j == per - 1)
+        if j < per - 1:   # nothing reduced yet: the buffer holds this rank's own partial sum
+            assert np.isfinite(dw.numpy()).all()
+        dh.append(dp.d_hidden.numpy().copy())
+        losses += dp.ph.loss
+    loss = torch.tensor([losses], dtype=torch.float64)
+    dist.all_reduce(loss)
+    np.savez(os.path.join(out_dir, f"mb{rank}.npz"), dh=np.concatenate(dh), dw=dw.numpy(), t0=mine[0], t1=mine[1],
+             loss=loss.numpy())
+    dist.destroy_process_group()
+
+
+def test_data_parallel_microbatch_accumulation(tmp_path):
+    """Two micro-batches per rank with the reduction deferred to the last equal the
+    oracle's gradient of the whole batch (the gradient is linear in the rows, and D
+    is the global loss-token count of the step, reading R5)."""
+    mp.start_processes(_dp_micro_worker, args=(_free_port(), str(tmp_path)), nprocs=WORLD, start_method="spawn")
+    b, ref = _reference(0)
+    for r in range(WORLD):
+        o = np.load(tmp_path / f"mb{r}.npz")
+        np.testing.assert_allclose(o["dw"], ref.d_w_vocab, atol=1e-12)
         np.testing.assert_allclose(o["dh"], ref.d_hidden[int(o["t0"]):int(o["t1"])], atol=1e-12)
         assert float(o["loss"][0]) == pytest.approx(ref.report.loss, abs=1e-12)
 

@@ -353,3 +353,31 @@ def test_cuda_graph_capture_replays_the_step():
     torch.cuda.synchronize()
     for a, e in zip(got, (out["logprob"], dh, dw, report)):
         assert torch.equal(a, e)
+
+
+# ---------------------------------------------- realistic rollouts
+MID = synth.Workload("mid", 2, 8, 80, 512, 4184, ragged=True, prompt_frac=0.1, delta_sigma=0.5, spike_rate=2e-3)
+# sigma_z = 32: 60% of the sampled targets at p_y > 0.99, a third at 1 - p_y < 1e-4
+PEAKED = synth.Workload("peaked", 2, 8, 80, 512, 4184, sigma_z=32.0, ragged=True, delta_sigma=0.3, spike_rate=2e-3)
+FLAT = synth.Workload("flat", 2, 8, 80, 512, 4184, sigma_z=1.0, ragged=True, delta_sigma=0.3, spike_rate=2e-3)
+
+
+@pytest.mark.parametrize("wl", [MID, PEAKED, FLAT], ids=lambda w: w.name)
+@pytest.mark.parametrize("dense", [False, True], ids=["sparse", "dense"])
+def test_sampled_targets_and_band_plants(wl, dense):
+    """Targets sampled from the policy itself (y ~ pi), guard spikes
+    on the row's least likely token, and tokens planted at ln alpha, ln beta, ln tau_g
+    +- {1e-6, 2e-4, 1e-3} (Eq.2, guard P:L472): outside the 1e-4 band the gate
+    is exact. PEAKED (sigma_z = 32) puts most sampled targets at p_y > 0.99, where K4
+    forms p - 1 by cancellation; FLAT (sigma_z = 1) is the high-entropy end."""
+    c = harness.make_case(wl, 21, targets="sampled", plants=True)
+    ref = harness.run_oracle(c)
+    py = np.exp(ref.logp)
+    if wl is PEAKED:
+        assert np.mean(py > 0.99) > 0.5                       # the p_y -> 1 regime is exercised
+    assert len(c.plants) >= 12 and ref.report.guarded_rollouts >= 1
+    gpu = harness.run_gpu_step(c, dense_backward=dense)
+    err = harness.compare(c, ref, gpu)
+    print(wl.name, "dense" if dense else "sparse", {k: v for k, v in err.items()},
+          "mean p_y", float(py.mean()), "plants", len(c.plants))
+    assert err["plants_outside_band"] >= 8
