@@ -305,6 +305,43 @@ def _setup(args):
     return r
 
 
+def _sample_targets(r, seed=77, chunk=1024):
+    """Rollout targets sampled from the policy itself (y ~ pi; SURVEY
+    §8(d)): Gumbel-max over the logits h W^T of each row, computed here with torch as
+    the inference engine's stand-in (input generation, outside the timed region; the
+    measured path never sees how the targets were made). Guard-spike rows get the row's
+    least likely token instead, so the guard trips although sampled targets are probable.
+    Vocab-parallel ranks take the max / min over their shard and agree on the global one
+    with one all-gather."""
+    import torch
+    import torch.distributed as dist
+
+    g = torch.Generator(device=r.dev)
+    g.manual_seed(seed * 1009 + r.rank)
+    h, w = r.b["hidden"], r.b["w"]
+    best = torch.empty(r.T, 4, dtype=torch.float32, device=r.dev)   # (max z+gumbel, its id, min z, its id)
+    for c0 in range(0, r.T, chunk):
+        c1 = min(r.T, c0 + chunk)
+        z = torch.matmul(h[c0:c1], w.t()).float()
+        u = torch.rand(z.shape, generator=g, device=r.dev).clamp_(1e-20, 1.0)
+        zg = z - torch.log(-torch.log(u))
+        mx, ix = zg.max(dim=1)
+        mn, jn = z.min(dim=1)
+        best[c0:c1] = torch.stack([mx, (ix + r.v_off).float(), mn, (jn + r.v_off).float()], dim=1)
+        del z, u, zg
+    if r.vocab_par:
+        allb = torch.empty(r.world, r.T, 4, dtype=torch.float32, device=r.dev)
+        dist.all_gather_into_tensor(allb, best)
+        k_mx = allb[:, :, 0].argmax(dim=0)
+        k_mn = allb[:, :, 2].argmin(dim=0)
+        rows = torch.arange(r.T, device=r.dev)
+        y, y_min = allb[k_mx, rows, 1], allb[k_mn, rows, 3]
+    else:
+        y, y_min = best[:, 1], best[:, 3]
+    y = torch.where(r.b["spikes"], y_min, y)
+    return y.round().to(torch.int32).contiguous()
+
+
 def _stored_infer_logprobs(r):
     """The stored inference log-probs: the trainer's own log-prob minus the drawn mismatch."""
     import torch
@@ -345,7 +382,7 @@ def _make_engine(r, args):
     if r.vocab_par:
         r.engine = parallel.VocabParallelPolicyLoss(r.phases, T=r.T, H=r.H, V_global=r.Vt, num_rollouts=r.R,
                                                     group_size=r.wl_rank.group_size, loss_denominator=r.D,
-                                                    dz_chunk_rows=0 if nv else r.chunk, device=r.dev, nvls=nv)
+                                                    dz_chunk_rows=r.chunk, device=r.dev, nvls=nv)
         r.ws, r.dh = r.engine.ws, r.engine.d_hidden
     elif r.world > 1:
         r.engine = parallel.DataParallelPolicyLoss(r.phases, T=r.T, H=r.H, V=r.Vt, num_rollouts=r.R,
@@ -422,13 +459,14 @@ def _kernel_report(r, args):
         c[0] += 1
         c[1] += m
     kern = {k: {"launches": v[0], "avg_ms": v[1] / v[0], "share": v[1] / (r.ms * args.steps)} for k, v in per.items()}
-    # the backward GEMMs run over the rows with coef != 0 (sparse backward) unless the
-    # vocab-parallel NVLS dH reduction forces the dense path; FLOPs per launch = the
-    # step's FLOPs of that kernel / its launches per step
+    # the backward GEMMs run over the rows with coef != 0 (sparse backward, also with
+    # the fused NVLS reductions) unless --dense-backward; FLOPs per launch = the step's
+    # FLOPs of that kernel / its launches per step
     T, H, V_local = r.T, r.H, r.V_local
     coef_t = r.engine.coef if r.engine is not None else r.coef
-    dense = args.dense_backward or (r.vocab_par and args.collective == "nvls")
-    bwd_rows = T if dense else int((coef_t != 0).sum().item())
+    dense = args.dense_backward
+    r.kept_rows = int((coef_t != 0).sum().item())
+    bwd_rows = T if dense else r.kept_rows
     step_kflops = {"K1_fwd_gemm_lse": 2.0 * T * V_local * H, "K4_bwd_dz_gemm": 2.0 * bwd_rows * V_local * H,
                    "K5_dh_gemm": 2.0 * bwd_rows * V_local * H, "K6_dw_gemm": 2.0 * bwd_rows * V_local * H}
     flops = {k: f / (per[k][0] / args.steps) for k, f in step_kflops.items() if k in per}
@@ -569,7 +607,11 @@ def _config(r, args):
            "group_size": r.wl_rank.group_size, "parallelism": f"{r.mode}{world}",
            "l2": "inputs exceed L2 (W %.2f GB, hidden %.0f MB > 126 MB); no flush needed" % (
                V_local * H * 2 / 1e9, T * H * 2 / 1e6),
-           "dz_chunk_rows": (T if (r.vocab_par and nv) else (r.chunk or T)),
+           "dz_chunk_rows": r.chunk or T,
+           "targets": args.targets + (" from the policy (Gumbel-max), guard spikes on the least likely token"
+                                      if args.targets == "sampled" else " ids"),
+           "kept_row_frac": r.kept_rows / T if T else 0.0,
+           "backward": "dense" if args.dense_backward else "sparse (rows with coef != 0)",
            "collectives": ([] if world == 1 else
                            (["all_gather partials (NCCL)", "dH fp32 all-reduce " +
                              ("fused in K5 epilogue (NVLS multimem)" if nv else "(NCCL)")]
@@ -592,6 +634,8 @@ def main_ours(args):
     import torch.distributed as dist
 
     r = _setup(args)
+    if args.targets == "sampled":
+        r.targets = r.b["targets"] = _sample_targets(r)
     r.infer = _stored_infer_logprobs(r)
     step = _make_engine(r, args)
     _time_steps(r, args, step)
@@ -636,6 +680,9 @@ def main():
                     help="nvls: the dW (DP) / dH (vocab-parallel) all-reduce is fused into the GEMM epilogue "
                          "over NVLink multicast; auto = nvls when the GPUs support multicast, else NCCL")
     ap.add_argument("--comm-sms", type=int, default=24, help="DP overlap: SMs left to NCCL while K5 runs")
+    ap.add_argument("--targets", default="sampled", choices=["sampled", "uniform"],
+                    help="sampled: y ~ the policy itself (Gumbel-max, guard spikes on the least likely token); "
+                         "uniform: uniform ids (round-1 workload)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -43,6 +43,23 @@ def _stale():
     return any(os.path.getmtime(d) > t for d in deps)
 
 
+def build_ab(tag: str, defines: list, verbose: bool = False) -> str:
+    """An A/B variant with extra -D flags, written to ab_libs/librl_<tag>.so (select it
+    with RL_LIBRARY); the product librl.so is left alone."""
+    out = os.path.join(ROOT, "ab_libs", f"librl_{tag}.so")
+    os.makedirs(os.path.dirname(out), exist_ok=True)
+    nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+    cmd = [nvcc, *NVCC_FLAGS, *defines, "-I", os.path.join(ROOT, "include"),
+           *[os.path.join(CSRC, s) for s in SOURCES], "-o", out]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        sys.stderr.write(r.stdout + r.stderr)
+        raise RuntimeError("nvcc failed building " + out)
+    if verbose:
+        sys.stderr.write(r.stderr)
+    return out
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
         return LIB
@@ -62,4 +79,10 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
 
 if __name__ == "__main__":
-    print(build(force="-f" in sys.argv, verbose=True))
+    # python _build.py [-f]                     product build
+    # python _build.py --ab TAG -DFOO=1 ...     A/B variant in ab_libs/
+    if "--ab" in sys.argv:
+        i = sys.argv.index("--ab")
+        print(build_ab(sys.argv[i + 1], sys.argv[i + 2:], verbose=False))
+    else:
+        print(build(force="-f" in sys.argv, verbose=True))

@@ -32,7 +32,8 @@
 namespace rl {
 
 constexpr int BN = 256, BK = 64;
-constexpr int GEMM_THREADS = 192;
+constexpr int GEMM_THREADS = 192;                        // 4 epilogue warps
+constexpr int gemm_threads(int epi_warps) { return 64 + 32 * epi_warps; }
 constexpr int EPI_BUF_BYTES = 32 * 128;  // one warp's 32-row x 128-byte store chunk
 constexpr int EPI_BYTES = 4 * 2 * EPI_BUF_BYTES;
 constexpr int BAR_BYTES = 256;
@@ -234,13 +235,19 @@ __device__ __noinline__ void nvls_reduce_slab_impl(const EpiParams& ep, const Ge
   }
 }
 
-template <int MODE, bool A_MN, bool B_MN, int CG, int STAGES, int NB = 1, int SKEW = 0>
-__global__ void __launch_bounds__(GEMM_THREADS, 1)
+// EW = epilogue warps: 4 (one per TMEM lane quarter), or 8 for EPI_LSE (two per lane
+// quarter, each taking half of a TMEM half's 256 columns; the pair merges its online
+// softmax states through shared memory): the drain of a TMEM half is bound by TMEM reads
+// (64 B/clk per SM) and the exponentials, and a second warp per SM sub-partition keeps a
+// load in flight while the other computes.
+template <int MODE, bool A_MN, bool B_MN, int CG, int STAGES, int NB = 1, int SKEW = 0, int EW = 4>
+__global__ void __launch_bounds__(gemm_threads(EW), 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const __grid_constant__ CUtensorMap tmC, const GemmShape sh_in, const EpiParams ep) {
   using TL = Tiling<CG>;
   static_assert(NB == 1 || (NB == 2 && CG == 2 && MODE != EPI_BF16_GROUPED), "wide tiles: CTA pairs, not grouped");
   static_assert(SKEW < STAGES, "the skewed head/tail holds SKEW stages");
+  static_assert(EW == 4 || (EW == 8 && MODE == EPI_LSE), "8 epilogue warps: LSE epilogue only");
   constexpr int TN = BN * NB;                 // tile columns
   constexpr int NACC = NB == 1 ? 2 : 1;       // TMEM accumulators (512 columns in total)
   constexpr int B_STAGE_ALL = NB * TL::B_STAGE;
@@ -284,7 +291,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 4 * CG);
+      mbar_init(&tempty[a], EW * CG);
     }
     fence_mbar_init();
     tma_prefetch(&tmA);
@@ -559,12 +566,14 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   } else {
     // ------------------------------------------------------------ epilogue
     const int q = warp & 3;  // TMEM lane quarter this warp may access
+    const int cgrp = (warp - 2) / 4;  // EW = 8: which 128 of a TMEM half's 256 columns
     const int r_in_tile = rank * 128 + q * 32 + lane;
     const uint32_t buf0 = smem_u32(sEpi + (warp - 2) * 2 * EPI_BUF_BYTES);
     const uint32_t tempty_leader0 = (CG == 2) ? mapa_shared(smem_u32(&tempty[0]), 0) : 0u;
     int acc = 0;
     uint32_t aph = 0;
     int chunk_ctr = 0;
+    int merge_ctr = 0;  // EW = 8 LSE merges done
     int it = 0;  // tile iteration of this CTA
     auto nvls_reduce_slab = [&](const EpiParams& e, const GemmShape& g, int t, uint32_t r, int qq, int l) {
       nvls_reduce_slab_impl<TL::TILE_M, TN>(e, g, t, r, qq, l, rows_valid);
@@ -615,12 +624,15 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           float mrun = -1e30f, srun = 0.f, trun = 0.f, zt = -INFINITY;
           const float it = (ep.invt_rows != nullptr && row_ok) ? ep.invt_rows[row] : ep.inv_temperature;
           const float sl2 = ep.invt_rows != nullptr ? it * 1.4426950408889634f : ep.scale_log2;
+          constexpr int CPW = (BN / 32) / (EW / 4);  // 32-column chunks per warp
+          const int cbeg = cgrp * CPW;
   #pragma unroll 1
-          for (int c = 0; c < BN / 32; ++c) {
+          for (int c = cbeg; c < cbeg + CPW; ++c) {
             uint32_t r[32];
             tmem_ld32(taddr + c * 32, r);
             tmem_wait_ld();
-            if (c == BN / 32 - 1) release_tmem(bi);
+            if (c == cbeg + CPW - 1) release_tmem(bi);
+            if (c * 32 >= nvalid) continue;  // columns past V (ragged last tile)
             float u[32];
   #pragma unroll
             for (int j = 0; j < 32; ++j) u[j] = __uint_as_float(r[j]) * sl2;
@@ -651,6 +663,22 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
               srun += e;
               trun = fmaf(e, d, trun);
             }
+          }
+          if constexpr (EW == 8) {
+            // merge the two column halves' states: (m, s, u) in log2 units, zt by max
+            // two slot sets used alternately: a set is rewritten only after the barrier of
+            // the following merge, which the reading warp reaches after reading it
+            float4* slot = reinterpret_cast<float4*>(sEpi) + ((merge_ctr++ & 1) * 4 + q) * 32 + lane;
+            if (cgrp == 1) *slot = make_float4(mrun, srun, trun, zt);
+            named_bar_sync(1 + q, 64);
+            if (cgrp == 1) continue;
+            const float4 o = *slot;
+            const float mn = fmaxf(mrun, o.x);
+            const float a1 = ex2f(mrun - mn), a2 = ex2f(o.x - mn);
+            trun = a1 * fmaf(srun, mrun - mn, trun) + a2 * fmaf(o.y, o.x - mn, o.z);
+            srun = a1 * srun + a2 * o.y;
+            mrun = mn;
+            zt = fmaxf(zt, o.w);
           }
           if (row_ok && n0 < ep.cols) {  // one partial per 256-column block
             constexpr float LN2 = 0.69314718055994530942f;
@@ -769,6 +797,14 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             stage_row(buf, lane, w);
             fence_async_smem();
             __syncwarp();
+#ifdef RL_AB_K4_NOSTORE
+            // A/B measurement only (never in the product build): K4 without its dU write,
+            // the math and the staging kept (the store is skipped behind a runtime test)
+            if (MODE == EPI_DZ && ep.rows >= 0) {
+              ++chunk_ctr;
+              continue;
+            }
+#endif
             if (lane == 0) {
               const int c0 = n0 + c * COLS;
               const int c1 = GROUPED ? tile_row0 + rank * 128 + q * 32

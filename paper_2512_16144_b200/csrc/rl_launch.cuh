@@ -141,6 +141,13 @@ int skew() {
   }();
   return v;
 }
+// Epilogue warps of the LSE GEMM (K1): RL_EPI_WARPS[_FWD] = 4 or 8 (default 8, two
+// warps per TMEM lane quarter; see rl_gemm.cuh).
+int epi_warps_for(int kid) {
+  static const std::array<int, kKnobKids> env = env_table("RL_EPI_WARPS", -1);
+  if (kid < 0 || kid >= kKnobKids) return 4;
+  return env[kid] == 4 ? 4 : 8;
+}
 int sync_slack_for(int kid) {
   static const std::array<int, kKnobKids> env = env_table("RL_SYNC_SLACK", -1);
   if (kid < 0 || kid >= kKnobKids) return 2;
@@ -168,12 +175,12 @@ constexpr int stages_for() {
   return CG == 2 ? (NB == 2 ? 4 : 6) : 4;
 }
 
-template <int MODE, bool A_MN, bool B_MN, int CG, int NB = 1, int SKEW = 0>
+template <int MODE, bool A_MN, bool B_MN, int CG, int NB = 1, int SKEW = 0, int EW = 4>
 rl_status launch_gemm_cg(int kid, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c, int64_t M,
                          int64_t N, int64_t K, int group_m, const rl::EpiParams& ep, int sms, cudaStream_t st,
                          int k_splits = 1, int split_rows = 0, const int* dyn_count = nullptr, int dyn_mode = 0) {
   constexpr int S = stages_for<CG, NB>();
-  auto kern = rl::gemm_kernel<MODE, A_MN, B_MN, CG, S, NB, SKEW>;
+  auto kern = rl::gemm_kernel<MODE, A_MN, B_MN, CG, S, NB, SKEW, EW>;
   constexpr int smem = rl::gemm_smem_bytes<CG, S, false, NB>();
   static_assert(smem <= 232448, "dynamic shared memory over 227 KB");
   static std::atomic<uint64_t> attr_done{0};  // per instantiation, one bit per device
@@ -214,7 +221,7 @@ rl_status launch_gemm_cg(int kid, const CUtensorMap& a, const CUtensorMap& b, co
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(units * CG);
-  cfg.blockDim = dim3(rl::GEMM_THREADS);
+  cfg.blockDim = dim3(rl::gemm_threads(EW));
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
@@ -232,29 +239,42 @@ rl_status launch_gemm_cg(int kid, const CUtensorMap& a, const CUtensorMap& b, co
   return RL_OK;
 }
 
+template <int MODE, bool A_MN, bool B_MN, int EW>
+rl_status launch_gemm_ew(int kid, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c, int64_t M,
+                         int64_t N, int64_t K, int group_m, const rl::EpiParams& ep, int sms, cudaStream_t st,
+                         int k_splits, int split_rows, const int* dyn_count, int dyn_mode) {
+  // wide tiles only where a tile covers at least two 256-column blocks
+  if (cta_group() == 2 && wide_for(kid) && N > rl::BN) {
+    switch (skew()) {
+      case 0:
+        return launch_gemm_cg<MODE, A_MN, B_MN, 2, 2, 0, EW>(kid, a, b, c, M, N, K, group_m, ep, sms, st, k_splits,
+                                                             split_rows, dyn_count, dyn_mode);
+      case 2:
+        return launch_gemm_cg<MODE, A_MN, B_MN, 2, 2, 2, EW>(kid, a, b, c, M, N, K, group_m, ep, sms, st, k_splits,
+                                                             split_rows, dyn_count, dyn_mode);
+      default:
+        return launch_gemm_cg<MODE, A_MN, B_MN, 2, 2, 3, EW>(kid, a, b, c, M, N, K, group_m, ep, sms, st, k_splits,
+                                                             split_rows, dyn_count, dyn_mode);
+    }
+  }
+  if (cta_group() == 2)
+    return launch_gemm_cg<MODE, A_MN, B_MN, 2, 1, 0, EW>(kid, a, b, c, M, N, K, group_m, ep, sms, st, k_splits,
+                                                         split_rows, dyn_count, dyn_mode);
+  return launch_gemm_cg<MODE, A_MN, B_MN, 1, 1, 0, EW>(kid, a, b, c, M, N, K, group_m, ep, sms, st, k_splits,
+                                                       split_rows, dyn_count, dyn_mode);
+}
+
 template <int MODE, bool A_MN, bool B_MN>
 rl_status launch_gemm(int kid, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c, int64_t M, int64_t N,
                       int64_t K, int group_m, const rl::EpiParams& ep, int sms, cudaStream_t st, int k_splits = 1,
                       int split_rows = 0, const int* dyn_count = nullptr, int dyn_mode = 0) {
   if (M <= 0 || N <= 0) return RL_OK;
-  // wide tiles only where a tile covers at least two 256-column blocks
-  if (cta_group() == 2 && wide_for(kid) && N > rl::BN) {
-    switch (skew()) {
-      case 0:
-        return launch_gemm_cg<MODE, A_MN, B_MN, 2, 2, 0>(kid, a, b, c, M, N, K, group_m, ep, sms, st, k_splits,
-                                                         split_rows, dyn_count, dyn_mode);
-      case 2:
-        return launch_gemm_cg<MODE, A_MN, B_MN, 2, 2, 2>(kid, a, b, c, M, N, K, group_m, ep, sms, st, k_splits,
-                                                         split_rows, dyn_count, dyn_mode);
-      default:
-        return launch_gemm_cg<MODE, A_MN, B_MN, 2, 2, 3>(kid, a, b, c, M, N, K, group_m, ep, sms, st, k_splits,
-                                                         split_rows, dyn_count, dyn_mode);
-    }
+  if constexpr (MODE == rl::EPI_LSE) {
+    if (epi_warps_for(kid) == 8)
+      return launch_gemm_ew<MODE, A_MN, B_MN, 8>(kid, a, b, c, M, N, K, group_m, ep, sms, st, k_splits, split_rows,
+                                                 dyn_count, dyn_mode);
   }
-  if (cta_group() == 2)
-    return launch_gemm_cg<MODE, A_MN, B_MN, 2>(kid, a, b, c, M, N, K, group_m, ep, sms, st, k_splits, split_rows,
-                                               dyn_count, dyn_mode);
-  return launch_gemm_cg<MODE, A_MN, B_MN, 1>(kid, a, b, c, M, N, K, group_m, ep, sms, st, k_splits, split_rows,
+  return launch_gemm_ew<MODE, A_MN, B_MN, 4>(kid, a, b, c, M, N, K, group_m, ep, sms, st, k_splits, split_rows,
                                              dyn_count, dyn_mode);
 }
 

@@ -279,8 +279,9 @@ class DataParallelPolicyLoss:
     def __init__(self, phases, *, T, H, V, num_rollouts, group_size, loss_denominator, group=None,
                  inv_temperature=1.0, alpha=0.5, beta=5.0, guard=1e-5, device=None, d_hidden_dtype=torch.bfloat16,
                  workspace=True, overlap=False, comm_sms=24, nvls=False, variant="icepop", kl_tau=0.0,
-                 kl_set="masked", inv_temperature_rows=None, reduce_scatter=False):
+                 kl_set="masked", inv_temperature_rows=None, reduce_scatter=False, dz_chunk_rows=0):
         self.ph = phases
+        self.chunk = dz_chunk_rows
         # overlap: the dW all-reduce (NCCL, side stream) runs concurrently with K5,
         # which then uses all but `comm_sms` SMs (NCCL's NVLS channels need SMs).
         self.overlap = overlap
@@ -305,7 +306,8 @@ class DataParallelPolicyLoss:
         self.adv = torch.empty(num_rollouts, **f32)
         self.report = torch.zeros(48, dtype=torch.uint8, device=dev)
         self.d_hidden = torch.empty(T, H, dtype=d_hidden_dtype, device=dev)
-        self.ws = alloc_workspace(rl_workspace_bytes(self.shape, num_rollouts), dev) if workspace else None
+        self.ws = (alloc_workspace(rl_workspace_bytes(self.shape, num_rollouts, dz_chunk_rows), dev) if workspace
+                   else None)
         self.loss_ws = alloc_workspace(48 * max(1, num_rollouts), dev) if workspace else None
         # nvls: dW is all-reduced inside the K6 epilogue (NVLink multicast); the
         # step then returns the symmetric buffer that holds the sum.
@@ -340,7 +342,7 @@ class DataParallelPolicyLoss:
                          d_w_vocab=self.nvls.buf,
                          d_w_vocab_nvls=(self.nvls.descriptor(mode=1 if self.reduce_scatter else 0)
                                          if reduce else None),
-                         workspace=self.ws, accumulate_dw=accumulate)
+                         dz_chunk_rows=self.chunk, workspace=self.ws, accumulate_dw=accumulate)
             if not reduce:
                 return self.nvls.buf                              # this rank's partial sum so far
             self.nvls.barrier()                                   # the exchange, fused into K6's epilogue
@@ -352,7 +354,7 @@ class DataParallelPolicyLoss:
             ph.full_step(self.shape, self.params, hidden, w, targets, infer, self.adv, offsets, loss_mask,
                          report=self.report, logprob=self.logprob, entropy=self.entropy, lse=self.lse,
                          coef=self.coef, keep=self.keep, guarded=self.guarded, d_hidden=self.d_hidden,
-                         d_w_vocab=d_w_vocab, workspace=self.ws, accumulate_dw=accumulate)
+                         d_w_vocab=d_w_vocab, dz_chunk_rows=self.chunk, workspace=self.ws, accumulate_dw=accumulate)
             if reduce:
                 dist.all_reduce(d_w_vocab, group=self.group)                              # the exchange
             return d_w_vocab

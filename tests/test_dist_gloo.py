@@ -78,7 +78,7 @@ class OraclePhases:
 
     def full_step(self, shape, params, hidden, w, targets, infer, adv, offsets, loss_mask, *, report, logprob,
                   entropy=None, lse=None, coef=None, keep=None, guarded=None, d_hidden=None, d_w_vocab=None,
-                  workspace=None, accumulate_dw=False):
+                  workspace=None, accumulate_dw=False, dz_chunk_rows=0):
         res = oracle.policy_loss_fwd_bwd(hidden.double().numpy(), w.double().numpy(), targets.long().numpy(),
                                          infer.double().numpy(), None, offsets.numpy(), loss_mask.numpy(),
                                          alpha=params.alpha, beta=params.beta,
