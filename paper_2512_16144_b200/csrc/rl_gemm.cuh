@@ -385,7 +385,14 @@ __global__ void __launch_bounds__(gemm_threads(EW), 1)
         mbar_wait_sleep(&empty[s], ph ^ 1);
         if (elect_one()) {
           if (leader) mbar_expect_tx(&full[s], CG * (TL::A_STAGE + B_STAGE_ALL));
-          const int k0 = kb * BK;
+          int k0 = kb * BK;
+#ifdef RL_AB_DU_L2
+          // A/B measurement only (never in the product build): K5 / K6 read their dU
+          // operand from a 256-row window (77 MB at V = 151552) that stays in L2, i.e. a
+          // backward whose dU never reaches DRAM; the outputs are garbage
+          if (MODE == EPI_BF16 && !A_MN && B_MN) a_row &= 255;
+          if (MODE == EPI_F32 && A_MN && B_MN) k0 &= 255;
+#endif
           uint8_t* a = sA + s * TL::A_STAGE;
           uint8_t* b = sB + s * B_STAGE_ALL;
           if constexpr (CG == 2) {

@@ -19,3 +19,46 @@ def test_batch_is_reproducible():
     a, b = synth.make_batch(wl, 5), synth.make_batch(wl, 5)
     for k in ("hidden", "w_vocab", "targets", "rewards", "rollout_offsets", "loss_mask", "delta_noise", "spikes"):
         assert np.array_equal(getattr(a, k), getattr(b, k)), k
+
+
+# ------------------------------------------------ input artifacts
+def _tiny_case_files(tmp_path):
+    from synth import artifact
+    wl = synth.CONFIGS["tiny"]
+    b = synth.make_batch(wl, 0)
+    infer = np.full(b.T, -1.5, np.float32)
+    return artifact, b, infer, artifact.write(str(tmp_path / "a"), b, infer, alpha=0.5, beta=5.0, guard=1e-5)
+
+
+def test_artifact_round_trip_and_digest_check(tmp_path):
+    artifact, b, infer, meta = _tiny_case_files(tmp_path)
+    m2, arr = artifact.read(str(tmp_path / "a"))
+    assert m2 == meta and m2["loss_denominator"] == float(b.T)
+    assert np.array_equal(arr["hidden.bf16"], b.hidden) and np.array_equal(arr["w_vocab.bf16"], b.w_vocab)
+    assert np.array_equal(arr["rollout_offsets.i32"], b.rollout_offsets)
+    assert np.array_equal(arr["infer_logprobs.f32"], infer)
+    # a flipped byte must be caught by the sha256 in meta.json
+    p = tmp_path / "a" / "targets.i32"
+    raw = bytearray(p.read_bytes())
+    raw[5] ^= 1
+    p.write_bytes(bytes(raw))
+    import pytest
+    with pytest.raises(ValueError, match="sha256"):
+        artifact.read(str(tmp_path / "a"))
+
+
+def test_generator_bytes_match_the_committed_digests():
+    """The seeded draws are platform independent: the digests of the generator-only files
+    of tiny/seed 0 (written by tests/make_artifact.py into tests/golden/) must reproduce
+    here and on the GPU box. A change of stream keys, dtype, rounding (float32 -> bf16 RNE)
+    or packing fails this test."""
+    import json
+    import os
+    from synth import artifact
+    with open(os.path.join(os.path.dirname(__file__), "golden", "artifact_tiny_seed0.meta.json")) as f:
+        gold = json.load(f)
+    assert gold["generator_version"] == synth.GENERATOR_VERSION
+    b = synth.make_batch(synth.CONFIGS[gold["config"]], gold["seed"])
+    d = artifact.digests(artifact.batch_arrays(b, np.zeros(b.T, np.float32)))
+    for name in ("hidden.bf16", "w_vocab.bf16", "rewards.f32", "rollout_offsets.i32", "loss_mask.u8"):
+        assert d[name] == gold["sha256"][name], name
