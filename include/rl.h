@@ -365,6 +365,21 @@ rl_status rl_grouped_gemm(const uint16_t* a, const uint16_t* b, const int32_t* o
 /* out[r] = 1 / sqrt(mean_k x[r, k]^2 + eps) for bf16 x [rows, K] (the RMSNorm scale). */
 rl_status rl_rms_inv(const uint16_t* x, int64_t rows, int64_t K, float eps, float* out, void* stream);
 
+/* RMSNorm weight folded into the expert weights along K (the pre-MoE
+ * norm of PAPER.md §2.1.8): out[r, k] = bf16_rn(w[r, k] * gamma[k]) for bf16 w [rows, K]
+ * (all experts' weights stacked, rows = n_groups * N) and fp32 gamma [K]. Run once per
+ * optimizer step; then rl_grouped_gemm(a, out, offsets, row_scale = rl_rms_inv(a)) is the
+ * expert GEMM of RMSNorm(a). out may alias w. K % 8 == 0; w, gamma, out 16-byte aligned
+ * (RL_ERR_INVALID_ARGUMENT otherwise). HBM-bound: 4 B per element moved. */
+rl_status rl_fold_gamma(const uint16_t* w, const float* gamma, int64_t rows, int64_t K, uint16_t* out,
+                        void* stream);
+
+/* Expert load balance from the DEVICE group offsets of rl_grouped_gemm:
+ * out[0] = max_g load_g, out[1] = mean load, out[2] = MaxViolation = (max - mean) / mean
+ * (0 when no row is routed). load_g = the group's row count after the same clamping
+ * rl_grouped_gemm applies. out: 3 fp32 on the device. */
+rl_status rl_expert_load(const int32_t* offsets, int32_t n_groups, int64_t rows, float* out, void* stream);
+
 /* ------------------------------------------------------------ utilities */
 /* Workspace needed by rl_logprob_fwd / rl_policy_loss_fwd_bwd / the split
  * phases for this shape. dz_chunk_rows = rows of the bf16 dU buffer (0 = T). */

@@ -127,6 +127,8 @@ _SIGS = {
     "rl_grouped_gemm": (ctypes.c_int, [_P, _P, _P, ctypes.c_int32, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
                                        _P, _P, _P]),
     "rl_rms_inv": (ctypes.c_int, [_P, ctypes.c_int64, ctypes.c_int64, ctypes.c_float, _P, _P]),
+    "rl_fold_gamma": (ctypes.c_int, [_P, _P, ctypes.c_int64, ctypes.c_int64, _P, _P]),
+    "rl_expert_load": (ctypes.c_int, [_P, ctypes.c_int32, ctypes.c_int64, _P, _P]),
     "rl_workspace_bytes": (ctypes.c_size_t, [ctypes.POINTER(rl_lm_shape), ctypes.c_int32, ctypes.c_int64]),
     "rl_workspace_bytes_hostio": (ctypes.c_size_t, [ctypes.POINTER(rl_lm_shape), ctypes.c_int32, ctypes.c_int64]),
     "rl_default_dz_chunk_rows": (ctypes.c_int64, [ctypes.POINTER(rl_lm_shape)]),
@@ -437,6 +439,29 @@ def rl_rms_inv(x: torch.Tensor, eps: float = 1e-6, out: torch.Tensor | None = No
     if out is None:
         out = torch.empty(rows, dtype=torch.float32, device=x.device)
     _check(load_library().rl_rms_inv(_ptr(_bf16(x, "x")), rows, K, float(eps), _ptr(out), _stream(stream)))
+    return out
+
+
+def rl_fold_gamma(w: torch.Tensor, gamma: torch.Tensor, out: torch.Tensor | None = None,
+                  stream=None) -> torch.Tensor:
+    """bf16(w * gamma) along the last dim of a bf16 [..., K] weight (RMSNorm gamma folded in)."""
+    K = w.shape[-1]
+    if out is None:
+        out = torch.empty_like(w)
+    if gamma.dtype != torch.float32 or gamma.numel() != K:
+        raise RLError(1, "gamma must be fp32 [K]")
+    _check(load_library().rl_fold_gamma(_ptr(_bf16(w, "w")), _ptr(gamma), w.numel() // K, K, _ptr(out),
+                                        _stream(stream)))
+    return out
+
+
+def rl_expert_load(offsets: torch.Tensor, rows: int, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """[max load, mean load, MaxViolation] (fp32, device) from int32 group offsets [G + 1]."""
+    if offsets.dtype != torch.int32:
+        raise RLError(1, "offsets must be int32")
+    if out is None:
+        out = torch.empty(3, dtype=torch.float32, device=offsets.device)
+    _check(load_library().rl_expert_load(_ptr(offsets), offsets.numel() - 1, int(rows), _ptr(out), _stream(stream)))
     return out
 
 

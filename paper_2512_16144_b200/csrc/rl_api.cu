@@ -445,6 +445,43 @@ rl_status rl_rms_inv(const uint16_t* x, int64_t rows, int64_t K, float eps, floa
   return RL_OK;
 }
 
+rl_status rl_fold_gamma(const uint16_t* w, const float* gamma, int64_t rows, int64_t K, uint16_t* out,
+                        void* stream) {
+  g_launches = 0;
+  if (rows < 0 || K < 8 || K % 8) return fail(RL_ERR_SHAPE, "need rows >= 0 and K a positive multiple of 8");
+  if (rows == 0) return RL_OK;
+  RL_NONNULL(w);
+  RL_NONNULL(gamma);
+  RL_NONNULL(out);
+  if ((reinterpret_cast<uintptr_t>(w) | reinterpret_cast<uintptr_t>(out)) & 15 ||
+      reinterpret_cast<uintptr_t>(gamma) & 15)
+    return fail(RL_ERR_INVALID_ARGUMENT, "w, gamma and out must be 16-byte aligned");
+  DevInfo d;
+  RL_TRY(device_info(d));
+  const int64_t n8 = rows * K / 8;
+  const int64_t blocks = std::min<int64_t>((n8 + 255) / 256, static_cast<int64_t>(d.sms) * 8);
+  {
+    ProfScope ps(RL_K_NS_AUX, static_cast<cudaStream_t>(stream));
+    rl::fold_gamma_kernel<<<static_cast<unsigned>(blocks), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+        w, gamma, rows, K, out);
+  }
+  RL_CHECK_LAUNCH();
+  return RL_OK;
+}
+
+rl_status rl_expert_load(const int32_t* offsets, int32_t n_groups, int64_t rows, float* out, void* stream) {
+  g_launches = 0;
+  if (n_groups < 1 || rows < 0) return fail(RL_ERR_SHAPE, "need n_groups >= 1 and rows >= 0");
+  RL_NONNULL(offsets);
+  RL_NONNULL(out);
+  {
+    ProfScope ps(RL_K_NS_AUX, static_cast<cudaStream_t>(stream));
+    rl::expert_load_kernel<<<1, 256, 0, static_cast<cudaStream_t>(stream)>>>(offsets, n_groups, rows, out);
+  }
+  RL_CHECK_LAUNCH();
+  return RL_OK;
+}
+
 size_t rl_newton_schulz_workspace_bytes(int64_t M, int64_t N) {
   if (check_ns_shape(M, N, 1) != RL_OK) return 0;
   return ns_layout(M, N, false).end;

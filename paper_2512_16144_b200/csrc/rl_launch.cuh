@@ -133,6 +133,20 @@ bool wide_for(int kid) {
   if (env[kid] >= 0) return env[kid] != 0;
   return kid == RL_K_FWD_GEMM || kid == RL_K_DH_GEMM || kid == RL_K_DW_GEMM || kid == RL_K_NS_GEMM;
 }
+// Serpentine K order (EpiParams::k_serpentine): a CTA's odd-numbered tiles walk their
+// k-blocks backwards. All CTAs are at the same tile number at the same time (the soft
+// k-barrier), so a wave starts on the operand rows the previous wave read last, which are
+// still in L2: the dW GEMM re-reads hidden [T, H] once per wave (~64 waves at GLM-16k).
+// RL_SERPENTINE[_<K>] = 0/1; default on for K6 (DW) and the Newton-Schulz GEMMs (the Gram
+// re-reads X). Off for K5 (DH): its accumulation order per dH row would then depend on the
+// wave the row lands in, and the sparse backward's dH is bitwise the dense one only while
+// every tile sums in the same order; off for K1 / K4 (K = H, nothing to reuse).
+bool serpentine_for(int kid) {
+  static const std::array<int, kKnobKids> env = env_table("RL_SERPENTINE", -1);
+  if (kid < 0 || kid >= kKnobKids) return false;
+  if (env[kid] >= 0) return env[kid] != 0;
+  return kid == RL_K_DW_GEMM || kid == RL_K_NS_GEMM;
+}
 int skew() {
   static const int v = [] {
     const char* e = getenv("RL_SKEW");
@@ -206,6 +220,7 @@ rl_status launch_gemm_cg(int kid, const CUtensorMap& a, const CUtensorMap& b, co
   const int64_t tiles = static_cast<int64_t>(sh.m_blocks) * sh.n_blocks * sh.k_splits;
   const int units = static_cast<int>(tiles < sms / CG ? tiles : sms / CG);
   rl::EpiParams ep2 = ep;
+  ep2.k_serpentine = serpentine_for(kid) ? 1 : 0;
   ep2.sync_every = 0;
   if (g_sync_ctr && sync_every_for(kid) > 0) {
     const int64_t max_tiles = (tiles + units - 1) / units;

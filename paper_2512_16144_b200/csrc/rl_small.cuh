@@ -581,4 +581,71 @@ __global__ void rms_inv_kernel(const uint16_t* __restrict__ x, int64_t rows, int
   if (lane == 0) out[r] = rsqrtf(acc / static_cast<float>(K) + eps);
 }
 
+
+// out[r, k] = bf16(w[r, k] * gamma[k]): the RMSNorm weight folded into the expert weights
+// along K (once per optimizer step), so the expert GEMM of RMSNorm(x) needs only the
+// 1/rms row scale in its epilogue. 8 bf16 (16 B) per thread and iteration, grid-stride.
+__global__ void fold_gamma_kernel(const uint16_t* __restrict__ w, const float* __restrict__ gamma, int64_t rows,
+                                  int64_t K, uint16_t* __restrict__ out) {
+  const int64_t n8 = rows * K / 8;  // K % 8 == 0
+  const int64_t k8 = K / 8;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n8;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const uint4 v = reinterpret_cast<const uint4*>(w)[i];
+    const int64_t k0 = (i % k8) * 8;
+    const float4 g0 = *reinterpret_cast<const float4*>(gamma + k0);
+    const float4 g1 = *reinterpret_cast<const float4*>(gamma + k0 + 4);
+    const float gs[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+    const uint32_t in[4] = {v.x, v.y, v.z, v.w};
+    uint32_t o[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float lo = __uint_as_float(in[j] << 16) * gs[2 * j];
+      const float hi = __uint_as_float(in[j] & 0xffff0000u) * gs[2 * j + 1];
+      o[j] = pack_bf16x2(lo, hi);
+    }
+    reinterpret_cast<uint4*>(out)[i] = make_uint4(o[0], o[1], o[2], o[3]);
+  }
+}
+
+// Expert-load statistics from the device group offsets: out[0] = max_g load,
+// out[1] = mean load, out[2] = MaxViolation = (max - mean) / mean (0 when there are no
+// rows). One block; a group's load is its row count as the grouped GEMM sees it (offsets
+// clamped to [0, rows], an end below its begin counts as empty).
+__device__ __forceinline__ int64_t group_load(const int32_t* offsets, int g, int64_t rows) {
+  const int64_t b = min(max(static_cast<int64_t>(offsets[g]), int64_t(0)), rows);
+  const int64_t e = min(max(static_cast<int64_t>(offsets[g + 1]), int64_t(0)), rows);
+  return e > b ? e - b : 0;
+}
+
+__global__ void expert_load_kernel(const int32_t* __restrict__ offsets, int n_groups, int64_t rows,
+                                   float* __restrict__ out) {
+  __shared__ long long smax[32], ssum[32];
+  long long mx = 0, sum = 0;
+  for (int g = threadIdx.x; g < n_groups; g += blockDim.x) {
+    const long long l = group_load(offsets, g, rows);
+    mx = max(mx, l);
+    sum += l;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    sum += __shfl_xor_sync(0xffffffffu, sum, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    smax[threadIdx.x >> 5] = mx;
+    ssum[threadIdx.x >> 5] = sum;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < static_cast<int>(blockDim.x + 31) / 32; ++w) {
+      mx = max(mx, smax[w]);
+      sum += ssum[w];
+    }
+    const double mean = static_cast<double>(sum) / n_groups;
+    out[0] = static_cast<float>(mx);
+    out[1] = static_cast<float>(mean);
+    out[2] = mean > 0 ? static_cast<float>((static_cast<double>(mx) - mean) / mean) : 0.f;
+  }
+}
+
 }  // namespace rl

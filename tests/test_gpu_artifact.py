@@ -7,6 +7,7 @@ import json
 import os
 import subprocess
 import sys
+import types
 
 import numpy as np
 import pytest
@@ -51,34 +52,26 @@ def test_artifact_gpu_vs_oracle_outputs(tmp_path, args):
     meta, c, ref = _load(out)
     gpu = harness.run_gpu_step(c)
     b = c.batch
-    err = {k: float(np.max(np.abs(gpu[k] - ref[k]))) for k in ("logprob", "entropy", "lse")}
-    assert max(err.values()) <= harness.LOGP_TOL, err
-    k = ref["ratio"]
-    band = ref["valid"] & ((np.abs(k - c.alpha) <= harness.BAND) | (np.abs(k - c.beta) <= harness.BAND)
-                           | (np.abs(k / c.guard - 1.0) <= harness.BAND))
-    flips = np.nonzero(gpu["keep"].astype(bool) != ref["keep"].astype(bool))[0]
-    assert np.all(band[flips]), flips
-    assert np.array_equal(gpu["guarded"].astype(bool), ref["guarded"].astype(bool))
-    plants = np.array(sorted(int(r) for r in ref["report"]["plants"]), dtype=np.int64)
-    if len(plants):
-        outside = plants[~band[plants]]
-        assert np.array_equal(gpu["keep"][outside].astype(bool), ref["keep"][outside].astype(bool))
-    slack = float((np.abs(gpu["coef"][flips]) + np.abs(ref["coef"][flips])).sum())
-    err["loss"] = abs(gpu["report"]["loss"] - ref["report"]["loss"])
-    assert err["loss"] <= harness.LOSS_TOL + slack, err
-    for key in ("nonfinite_inputs", "bad_targets", "bad_offsets", "guarded_rollouts"):
-        assert gpu["report"][key] == ref["report"][key], key
+    r = ref["report"]
+    rep = types.SimpleNamespace(keep=ref["keep"].astype(bool), guarded=ref["guarded"].astype(bool),
+                                ratio=ref["ratio"], valid=ref["valid"].astype(bool), coef=ref["coef"],
+                                **{k: v for k, v in r.items() if k != "plants"})
+    oref = types.SimpleNamespace(logp=ref["logprob"], entropy=ref["entropy"], lse=ref["lse"], report=rep)
+    c.plants = {int(k): tuple(v) for k, v in r["plants"].items()}
+    # forward, gate (bit-exact outside the 1e-4 bands, incl. the guard band's rollouts),
+    # counters, loss: the same contract as every other parity test
+    err = harness.compare(c, oref, gpu, check_grads=False)
+    flips = np.nonzero(gpu["keep"].astype(bool) != rep.keep)[0]
     same = np.ones(b.T, bool)
     same[flips] = False
-    # dH_t depends on row t only: compare every row whose gate agrees, per row
-    dh = harness.dh_row_error(gpu["d_hidden"][same], ref["d_hidden"][same], ref["coef"][same],
-                              artifact_w64(c), b.targets[same])
-    err["d_hidden_row"] = dh
-    assert dh <= 1.0, err
+    # dH_t depends on row t only: every row whose gate agrees, per row
+    err["d_hidden_row"] = harness.dh_row_error(gpu["d_hidden"][same], ref["d_hidden"][same], ref["coef"][same],
+                                               artifact_w64(c), b.targets[same])
+    assert err["d_hidden_row"] <= 1.0, err
     if not len(flips):
         err["d_w_vocab"] = harness.rel_fro(gpu["d_w_vocab"], ref["d_w_vocab"])
         assert err["d_w_vocab"] <= harness.GRAD_RTOL, err
-    print(meta["config"], meta["T"], "x", meta["H"], "x", meta["V"], err, "flips", len(flips), "plants", len(plants))
+    print(meta["config"], meta["T"], "x", meta["H"], "x", meta["V"], err, "flips", len(flips))
 
 
 def artifact_w64(c):

@@ -68,12 +68,48 @@ def test_grouped_gemm_fused_rmsnorm():
     gamma = rng.uniform(0.5, 1.5, K)
     w = rng.standard_normal((G, N, K)) / np.sqrt(K)
     ref = moe.grouped_mm_rmsnorm(x.float().numpy(), gamma, w, off, eps=1e-6)
-    b = _bf(w * gamma[None, None, :])
+    # gamma folded into the expert weights on the device (once per optimizer step)
+    b = rl.rl_fold_gamma(_bf(w).cuda(), torch.from_numpy(gamma.astype(np.float32)).cuda())
     xs = x.cuda()
     scale = rl.rl_rms_inv(xs, 1e-6)
-    out = rl.rl_grouped_gemm(xs, b.cuda(), torch.from_numpy(off).cuda(), row_scale=scale)
+    out = rl.rl_grouped_gemm(xs, b, torch.from_numpy(off).cuda(), row_scale=scale)
     torch.cuda.synchronize()
     got = out.float().cpu().numpy().astype(np.float64)
     err = np.linalg.norm(got - ref) / np.linalg.norm(ref)
     print("rmsnorm-fused", err)
     assert err <= 5e-3
+
+
+def test_fold_gamma_vs_oracle_rounding():
+    """out = bf16_rn(w * gamma): the fp32 product rounded once more to bf16 may differ
+    from the exact product's rounding only on a double-rounding tie (<= 1 bf16 ulp)."""
+    rng = np.random.default_rng(5)
+    G, N, K = 3, 200, 1408
+    w = _bf(rng.standard_normal((G, N, K)))
+    gamma = rng.uniform(0.25, 2.0, K).astype(np.float32)
+    got = rl.rl_fold_gamma(w.cuda(), torch.from_numpy(gamma).cuda())
+    torch.cuda.synchronize()
+    exact = w.double().numpy() * gamma.astype(np.float64)
+    ref = torch.from_numpy(exact).to(torch.bfloat16).double().numpy()   # RN of the exact product
+    g = got.double().cpu().numpy()
+    diff = g != ref
+    assert diff.mean() < 1e-3, diff.mean()
+    assert np.all(np.abs(g - exact) <= np.abs(exact) * 2.0 ** -8 + 1e-30)
+    inplace = w.cuda()
+    rl.rl_fold_gamma(inplace, torch.from_numpy(gamma).cuda(), out=inplace)   # out may alias w
+    assert torch.equal(inplace.cpu(), got.cpu())
+
+
+@pytest.mark.parametrize("offs", [[0, 300, 300, 700], [0, 0, 0, 0], [0, 50, 40, 90, 90], [0, 7, 7, 7, 7, 7, 7, 8]])
+def test_expert_load_vs_oracle(offs):
+    """MaxViolation of the loads the grouped GEMM sees (offsets clamped,
+    a decreasing pair counts as an empty group) vs oracle.moe.max_violation."""
+    o = np.array(offs, np.int64)
+    rows = int(o[-1])
+    b = np.clip(o[:-1], 0, rows)
+    e = np.maximum(np.clip(o[1:], 0, rows), b)
+    load = (e - b).astype(np.float64)
+    got = rl.rl_expert_load(torch.tensor(offs, dtype=torch.int32).cuda(), rows).cpu().numpy()
+    assert got[0] == load.max() and got[1] == pytest.approx(load.mean(), rel=1e-7)
+    want = moe.max_violation(load) if load.sum() > 0 else 0.0
+    assert got[2] == pytest.approx(want, rel=1e-6, abs=1e-7)

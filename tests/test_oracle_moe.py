@@ -33,6 +33,9 @@ def test_max_violation():
     """Balanced load -> 0; one expert with twice the mean... (PAPER.md L204 definition)."""
     assert moe.max_violation(np.full(8, 5.0)) == 0.0
     assert moe.max_violation(np.array([1.0, 1.0, 1.0, 5.0])) == pytest.approx(1.5)
+    # every token on one of G experts: max = G * mean -> G - 1 (catches a max/mean swap or a
+    # missing "- mean")
+    assert moe.max_violation(np.array([0.0, 0.0, 12.0, 0.0, 0.0, 0.0])) == pytest.approx(5.0)
 
 
 def test_rmsnorm_unit_mean_square_and_scale_invariance():

@@ -5,7 +5,7 @@
 # alternated with the product library, 3 rounds; then per-GEMM DRAM bytes of each.
 set -x
 mkdir -p gpurun_out/r02/f1
-python -c "import paper_2512_16144_b200 as rl; rl.load_library()"
+timeout 900 python -m pytest tests/test_gpu_artifact.py -q -s -p no:cacheprovider > gpurun_out/r02/f1/artifact_test.log 2>&1
 for i in 1 2 3; do
   timeout 300 python bench.py --steps 20 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/r02/f1/prod_$i.jsonl 2>/dev/null
   RL_LIBRARY=ab_libs/librl_dufree.so timeout 300 python bench.py --steps 20 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/r02/f1/dufree_$i.jsonl 2>/dev/null
