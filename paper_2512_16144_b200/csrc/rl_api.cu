@@ -661,3 +661,15 @@ extern "C" int32_t rl_debug_max_active_clusters(int32_t cluster) {
   if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess) return -2;
   return n;
 }
+
+#ifdef RL_AB_STATS
+// A/B build only (not in include/rl.h): copy the per-CTA cycle counters of the last launch
+// of epilogue mode `mode` (rl_gemm.cuh, g_ab_stats) to host memory `out` [512][8].
+extern "C" int32_t rl_ab_stats_read(int32_t mode, unsigned long long* out) {
+  if (mode < 0 || mode >= 8) return -1;
+  if (cudaMemcpyFromSymbol(out, rl::g_ab_stats, sizeof(unsigned long long) * 512 * 8,
+                           sizeof(unsigned long long) * 512 * 8 * mode) != cudaSuccess)
+    return -2;
+  return 0;
+}
+#endif

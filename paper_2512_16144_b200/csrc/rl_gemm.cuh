@@ -54,6 +54,18 @@ constexpr int NVLS_MAX_RANKS = 8;
 #ifdef RL_AB_K4_NOSTORE
 __device__ unsigned g_ab_k4_launches = 0;  // A/B build only: K4 launches so far
 #endif
+#ifdef RL_AB_STATS
+// A/B build only: per-CTA cycle counters of the last launch of each epilogue mode
+// [mode][cta][slot]: 0 MMA waits on tempty, 1 MMA waits on full, 2 MMA loop total,
+// 3 producer waits on empty, 4 producer k-barrier waits, 5 epilogue (warp 2) waits on
+// tfull, 6 epilogue (warp 2) drain cycles, 7 tiles
+__device__ unsigned long long g_ab_stats[8][512][8];
+#define RL_AB_CLK(v) const long long v = clock64()
+#define RL_AB_ADD(slot, t0) g_ab_stats[MODE][blockIdx.x][slot] += static_cast<unsigned long long>(clock64() - (t0))
+#else
+#define RL_AB_CLK(v)
+#define RL_AB_ADD(slot, t0)
+#endif
 
 template <int CG>
 struct Tiling {
@@ -293,6 +305,9 @@ __global__ void __launch_bounds__(gemm_threads(EW), 1)
   const int n_units = gridDim.x / CG;
 
   if (threadIdx.x == 0) {
+#ifdef RL_AB_STATS
+    for (int k = 0; k < 8; ++k) g_ab_stats[MODE][blockIdx.x][k] = 0;
+#endif
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
@@ -388,12 +403,17 @@ __global__ void __launch_bounds__(gemm_threads(EW), 1)
               const uint32_t* c = ep.sync_ctr + (p - ep.sync_slack);
               const long long t0 = clock64();
               while (ld_acquire(c) < gridDim.x && clock64() - t0 < (1ll << 17)) __nanosleep(64);
+              RL_AB_ADD(4, t0);
             }
           }
           __syncwarp();
           last_sync = p;
         }
-        mbar_wait_sleep(&empty[s], ph ^ 1);
+        {
+          RL_AB_CLK(tw);
+          mbar_wait_sleep(&empty[s], ph ^ 1);
+          if (lane == 0) RL_AB_ADD(3, tw);
+        }
         if (elect_one()) {
           if (leader) mbar_expect_tx(&full[s], CG * (TL::A_STAGE + B_STAGE_ALL));
           int k0 = kb * BK;
@@ -466,6 +486,7 @@ __global__ void __launch_bounds__(gemm_threads(EW), 1)
       //   ops [L, L+D)          tail, block 0      (wait full), then tfull[0]
       //   ops [L+D, L+2D)       tail, block 1      (release stage), then tfull[1]
       if (leader) {
+        RL_AB_CLK(t_mma0);
         constexpr uint32_t idesc = umma_idesc_bf16(TL::TILE_M, BN, A_MN, B_MN);
         uint32_t aph = 0;
         int g0 = 0;  // k-blocks consumed before this tile (stage = g % STAGES)
@@ -475,8 +496,12 @@ __global__ void __launch_bounds__(gemm_threads(EW), 1)
           tile_k_range(tile, sh, kb0, kb1);
           const int L = kb1 > kb0 ? kb1 - kb0 : 0;
           const int D = SKEW < L / 2 ? SKEW : L / 2;
-          mbar_wait(&tempty[0], aph ^ 1);
-          if (D == 0) mbar_wait(&tempty[1], aph ^ 1);
+          {
+            RL_AB_CLK(tw);
+            mbar_wait(&tempty[0], aph ^ 1);
+            if (D == 0) mbar_wait(&tempty[1], aph ^ 1);
+            if (lane == 0) RL_AB_ADD(0, tw);
+          }
           tc_fence_after();
 #pragma unroll 1
           for (int op = 0; op < L + 2 * D; ++op) {
@@ -488,13 +513,17 @@ __global__ void __launch_bounds__(gemm_threads(EW), 1)
             else if (op < L + D) { j = op - D; nb_lo = 0; nb_hi = 0; wait_full = true; release = false; }
             else { j = op - 2 * D; nb_lo = 1; nb_hi = 1; wait_full = false; release = true; }
             if (op == D && D > 0) {
+              RL_AB_CLK(tw);
               mbar_wait(&tempty[1], aph ^ 1);
+              if (lane == 0) RL_AB_ADD(0, tw);
               tc_fence_after();
             }
             const int g = g0 + j;
             const int st = g % STAGES;
             if (wait_full) {
+              RL_AB_CLK(tw);
               mbar_wait(&full[st], (g / STAGES) & 1);
+              if (lane == 0) RL_AB_ADD(1, tw);
               tc_fence_after();
             }
             if (elect_one()) {
@@ -524,7 +553,11 @@ __global__ void __launch_bounds__(gemm_threads(EW), 1)
           __syncwarp();
           g0 += L;
           aph ^= 1;
+#ifdef RL_AB_STATS
+          if (lane == 0) g_ab_stats[MODE][blockIdx.x][7] += 1;
+#endif
         }
+        if (lane == 0) RL_AB_ADD(2, t_mma0);
       }
     } else if (leader) {
       constexpr uint32_t idesc = umma_idesc_bf16(TL::TILE_M, BN, A_MN, B_MN);
@@ -533,14 +566,23 @@ __global__ void __launch_bounds__(gemm_threads(EW), 1)
       int acc = 0;
       uint32_t aph = 0;
       const uint32_t a_base = smem_u32(sA), b_base = smem_u32(sB);
+      RL_AB_CLK(t_mma0);
       for (int tile = unit; tile < total; tile += n_units) {
-        mbar_wait(&tempty[acc], aph ^ 1);
+        {
+          RL_AB_CLK(tw);
+          mbar_wait(&tempty[acc], aph ^ 1);
+          if (lane == 0) RL_AB_ADD(0, tw);
+        }
         tc_fence_after();
         const uint32_t d = tmem_base + acc * TN;
         int kb0 = 0, kb1 = sh.k_blocks;
         if constexpr (!GROUPED) tile_k_range(tile, sh, kb0, kb1);
         for (int kb = kb0; kb < kb1; ++kb) {
-          mbar_wait(&full[s], ph);
+          {
+            RL_AB_CLK(tw);
+            mbar_wait(&full[s], ph);
+            if (lane == 0) RL_AB_ADD(1, tw);
+          }
           tc_fence_after();
           if (elect_one()) {
             const uint32_t a0 = a_base + s * TL::A_STAGE;
@@ -579,7 +621,11 @@ __global__ void __launch_bounds__(gemm_threads(EW), 1)
         __syncwarp();
         if (NACC == 2) acc ^= 1;
         if (acc == 0) aph ^= 1;
+#ifdef RL_AB_STATS
+        if (lane == 0) g_ab_stats[MODE][blockIdx.x][7] += 1;
+#endif
       }
+      if (lane == 0) RL_AB_ADD(2, t_mma0);
     }
   } else {
     // ------------------------------------------------------------ epilogue
@@ -596,9 +642,15 @@ __global__ void __launch_bounds__(gemm_threads(EW), 1)
     auto nvls_reduce_slab = [&](const EpiParams& e, const GemmShape& g, int t, uint32_t r, int qq, int l) {
       nvls_reduce_slab_impl<TL::TILE_M, TN>(e, g, t, r, qq, l, rows_valid);
     };
+#ifdef RL_AB_STATS
+    long long t_drain0_shared = 0;
+#endif
     auto release_tmem = [&](int a) {
       tc_fence_before();
       __syncwarp();
+#ifdef RL_AB_STATS
+      if (warp == 2 && lane == 0) RL_AB_ADD(6, t_drain0_shared);
+#endif
       if (lane == 0) {
         if constexpr (CG == 2)
           mbar_arrive_cluster(tempty_leader0 + a * 8);
@@ -628,7 +680,14 @@ __global__ void __launch_bounds__(gemm_threads(EW), 1)
       for (int h = 0; h < NB; ++h) {
         const int bi = NB == 2 ? h : acc;  // TMEM half (wide tiles) or accumulator
         const int n0 = n * TN + h * BN;
-        mbar_wait_sleep(&tfull[bi], aph);
+        {
+          RL_AB_CLK(tw);
+          mbar_wait_sleep(&tfull[bi], aph);
+          if (warp == 2 && lane == 0) RL_AB_ADD(5, tw);
+        }
+#ifdef RL_AB_STATS
+        t_drain0_shared = clock64();
+#endif
         tc_fence_after();
         const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + bi * BN;
 
