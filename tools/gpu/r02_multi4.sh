@@ -17,3 +17,5 @@ timeout 900 $T --nproc-per-node 4 bench.py --gpus 4 --config glm64k --steps 10 -
 timeout 900 $T --nproc-per-node 2 bench.py --gpus 2 --config glm64k --steps 10 --warmup 3 > gpurun_out/r02/multi4/vp_glm64k_n2.jsonl 2> gpurun_out/r02/multi4/vp_glm64k_n2.err
 timeout 900 $T --nproc-per-node 4 bench.py --gpus 4 --config stress --steps 20 --warmup 3 > gpurun_out/r02/multi4/stress_n4.jsonl 2> gpurun_out/r02/multi4/stress_n4.err
 python tools/bench_summary.py gpurun_out/r02/multi4/*.jsonl
+RL_LIBRARY=ab_libs/librl_stats.so timeout 300 python tools/gemm_stats.py > gpurun_out/r02/multi4/gemm_stats.log 2>&1
+cat gpurun_out/r02/multi4/gemm_stats.log | tail -5
