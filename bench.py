@@ -255,6 +255,11 @@ def _setup(args):
     if r.world > 1:
         dist.init_process_group("nccl", device_id=dev)
     r.name, r.wl = workload_for(args, r.world)
+    if args.delta_sigma is not None:
+        # A/B knob: the trainer-inference mismatch of the stress config on another shape
+        # (e.g. vocab-parallel glm64k with ~43% of rows masked, for the sparse backward)
+        import dataclasses
+        r.wl = dataclasses.replace(r.wl, delta_sigma=float(args.delta_sigma))
     if args.collective == "auto":
         args.collective = "nccl"
         if r.world > 1:
@@ -611,6 +616,7 @@ def _config(r, args):
            "targets": args.targets + (" from the policy (Gumbel-max), guard spikes on the least likely token"
                                       if args.targets == "sampled" else " ids"),
            "kept_row_frac": r.kept_rows / T if T else 0.0,
+           "delta_sigma": r.wl_rank.delta_sigma,
            "backward": "dense" if args.dense_backward else "sparse (rows with coef != 0)",
            "collectives": ([] if world == 1 else
                            (["all_gather partials (NCCL)", "dH fp32 all-reduce " +
@@ -680,6 +686,8 @@ def main():
                     help="nvls: the dW (DP) / dH (vocab-parallel) all-reduce is fused into the GEMM epilogue "
                          "over NVLink multicast; auto = nvls when the GPUs support multicast, else NCCL")
     ap.add_argument("--comm-sms", type=int, default=24, help="DP overlap: SMs left to NCCL while K5 runs")
+    ap.add_argument("--delta-sigma", type=float, default=None,
+                    help="override the workload's log-prob mismatch sigma (A/B: 1.0 = the stress config's)")
     ap.add_argument("--targets", default="sampled", choices=["sampled", "uniform"],
                     help="sampled: y ~ the policy itself (Gumbel-max, guard spikes on the least likely token); "
                          "uniform: uniform ids (round-1 workload)")
