@@ -61,8 +61,11 @@ __device__ unsigned g_ab_k4_launches = 0;  // A/B build only: K4 launches so far
 // tfull, 6 epilogue (warp 2) drain cycles, 7 tiles
 __device__ unsigned long long g_ab_stats[8][512][8];
 #define RL_AB_CLK(v) const long long v = clock64()
-#define RL_AB_ADD(slot, t0) g_ab_stats[MODE][blockIdx.x][slot] += static_cast<unsigned long long>(clock64() - (t0))
+// accumulate in registers (ab_acc[], per thread); RL_AB_FLUSH writes them out once
+#define RL_AB_ADD(slot, t0) ab_acc[slot] += static_cast<unsigned long long>(clock64() - (t0))
+#define RL_AB_FLUSH(slot) g_ab_stats[MODE][blockIdx.x][slot] = ab_acc[slot]
 #else
+#define RL_AB_FLUSH(slot)
 #define RL_AB_CLK(v)
 #define RL_AB_ADD(slot, t0)
 #endif
@@ -121,6 +124,7 @@ struct EpiParams {
   int sync_slack;
   int max_sync;            // highest sync point any CTA reaches
   int k_serpentine;        // odd tiles of a CTA walk their k-blocks backwards (L2 reuse across waves)
+  int k_rotate;            // > 1: pair u starts its k loop at phase u % k_rotate of k_rotate (L2 hot spots)
   // EPI_F32_NVLS: D is also reduced over the ranks of an NVLink multicast group.
   // Every warp stores its 32-row slab locally (TMA), then publishes flag[slab] =
   // epoch; the rank owning the tile (tile % world) later sums the slab over all
@@ -281,6 +285,9 @@ __global__ void __launch_bounds__(gemm_threads(EW), 1)
       sh.k_splits = 1;
     }
   }
+#ifdef RL_AB_STATS
+  unsigned long long ab_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#endif
 #ifdef RL_AB_K4_NOSTORE
   const bool ab_k4_skip = MODE == EPI_DZ && *(volatile unsigned*)&g_ab_k4_launches > 0;
 #endif
@@ -391,8 +398,13 @@ __global__ void __launch_bounds__(gemm_threads(EW), 1)
       if constexpr (!GROUPED) tile_k_range(tile, sh, kb0, kb1);
       // serpentine: the MMA accumulates in issue order, so only the loads are reordered
       const bool k_rev = ep.k_serpentine && (((tile - unit) / n_units) & 1);
+      // rotated K start (EpiParams::k_rotate phases): CTA pairs that share an operand block
+      // read different k-slices of it at the same moment instead of the same L2 lines
+      const int k_len = kb1 - kb0;
+      const int k_rot = (ep.k_rotate > 1 && k_len > 0) ? ((unit % ep.k_rotate) * k_len) / ep.k_rotate : 0;
       for (int kb_i = kb0; kb_i < kb1; ++kb_i, ++gk) {
-        const int kb = k_rev ? kb0 + kb1 - 1 - kb_i : kb_i;
+        int kb = k_rev ? kb0 + kb1 - 1 - kb_i : kb_i;
+        if (k_rot) kb = kb0 + (kb - kb0 + k_rot) % k_len;
         if (ep.sync_every > 0 && gk > 0 && gk % ep.sync_every == 0) {
           const int p = gk / ep.sync_every;
           if (lane == 0) {
@@ -472,6 +484,10 @@ __global__ void __launch_bounds__(gemm_threads(EW), 1)
     // arrive on the sync points this CTA never reaches (it had fewer tiles)
     if (ep.sync_every > 0 && lane == 0)
       for (int p = last_sync + 1; p <= ep.max_sync; ++p) red_release_add(ep.sync_ctr + p, 1u);
+    if (lane == 0) {
+      RL_AB_FLUSH(3);
+      RL_AB_FLUSH(4);
+    }
   } else if (warp == 1) {
     // ----------------------------------------------------------- MMA issuer
     if constexpr (NB == 2) {
@@ -554,10 +570,13 @@ __global__ void __launch_bounds__(gemm_threads(EW), 1)
           g0 += L;
           aph ^= 1;
 #ifdef RL_AB_STATS
-          if (lane == 0) g_ab_stats[MODE][blockIdx.x][7] += 1;
+          ab_acc[7] += 1;
 #endif
         }
-        if (lane == 0) RL_AB_ADD(2, t_mma0);
+        if (lane == 0) {
+          RL_AB_ADD(2, t_mma0);
+          RL_AB_FLUSH(0); RL_AB_FLUSH(1); RL_AB_FLUSH(2); RL_AB_FLUSH(7);
+        }
       }
     } else if (leader) {
       constexpr uint32_t idesc = umma_idesc_bf16(TL::TILE_M, BN, A_MN, B_MN);
@@ -622,10 +641,13 @@ __global__ void __launch_bounds__(gemm_threads(EW), 1)
         if (NACC == 2) acc ^= 1;
         if (acc == 0) aph ^= 1;
 #ifdef RL_AB_STATS
-        if (lane == 0) g_ab_stats[MODE][blockIdx.x][7] += 1;
+        ab_acc[7] += 1;
 #endif
       }
-      if (lane == 0) RL_AB_ADD(2, t_mma0);
+      if (lane == 0) {
+        RL_AB_ADD(2, t_mma0);
+        RL_AB_FLUSH(0); RL_AB_FLUSH(1); RL_AB_FLUSH(2); RL_AB_FLUSH(7);
+      }
     }
   } else {
     // ------------------------------------------------------------ epilogue
@@ -922,6 +944,10 @@ __global__ void __launch_bounds__(gemm_threads(EW), 1)
       fence_sys();
     }
     if (lane == 0) bulk_wait_all();
+    if (warp == 2 && lane == 0) {
+      RL_AB_FLUSH(5);
+      RL_AB_FLUSH(6);
+    }
   }
   tc_fence_before();
   if constexpr (CG == 2)
