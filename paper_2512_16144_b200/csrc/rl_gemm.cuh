@@ -124,7 +124,6 @@ struct EpiParams {
   int sync_slack;
   int max_sync;            // highest sync point any CTA reaches
   int k_serpentine;        // odd tiles of a CTA walk their k-blocks backwards (L2 reuse across waves)
-  int k_rotate;            // > 1: pair u starts its k loop at phase u % k_rotate of k_rotate (L2 hot spots)
   // EPI_F32_NVLS: D is also reduced over the ranks of an NVLink multicast group.
   // Every warp stores its 32-row slab locally (TMA), then publishes flag[slab] =
   // epoch; the rank owning the tile (tile % world) later sums the slab over all
@@ -398,13 +397,8 @@ __global__ void __launch_bounds__(gemm_threads(EW), 1)
       if constexpr (!GROUPED) tile_k_range(tile, sh, kb0, kb1);
       // serpentine: the MMA accumulates in issue order, so only the loads are reordered
       const bool k_rev = ep.k_serpentine && (((tile - unit) / n_units) & 1);
-      // rotated K start (EpiParams::k_rotate phases): CTA pairs that share an operand block
-      // read different k-slices of it at the same moment instead of the same L2 lines
-      const int k_len = kb1 - kb0;
-      const int k_rot = (ep.k_rotate > 1 && k_len > 0) ? ((unit % ep.k_rotate) * k_len) / ep.k_rotate : 0;
       for (int kb_i = kb0; kb_i < kb1; ++kb_i, ++gk) {
-        int kb = k_rev ? kb0 + kb1 - 1 - kb_i : kb_i;
-        if (k_rot) kb = kb0 + (kb - kb0 + k_rot) % k_len;
+        const int kb = k_rev ? kb0 + kb1 - 1 - kb_i : kb_i;
         if (ep.sync_every > 0 && gk > 0 && gk % ep.sync_every == 0) {
           const int p = gk / ep.sync_every;
           if (lane == 0) {

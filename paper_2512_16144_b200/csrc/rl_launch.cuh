@@ -147,12 +147,6 @@ bool serpentine_for(int kid) {
   if (env[kid] >= 0) return env[kid] != 0;
   return kid == RL_K_DW_GEMM || kid == RL_K_NS_GEMM;
 }
-// Rotated K start (EpiParams::k_rotate): RL_KROT[_<K>] = number of phases (0/1 = off).
-int k_rotate_for(int kid) {
-  static const std::array<int, kKnobKids> env = env_table("RL_KROT", -1);
-  if (kid < 0 || kid >= kKnobKids) return 0;
-  return env[kid] > 1 ? env[kid] : 0;
-}
 int skew() {
   static const int v = [] {
     const char* e = getenv("RL_SKEW");
@@ -227,7 +221,6 @@ rl_status launch_gemm_cg(int kid, const CUtensorMap& a, const CUtensorMap& b, co
   const int units = static_cast<int>(tiles < sms / CG ? tiles : sms / CG);
   rl::EpiParams ep2 = ep;
   ep2.k_serpentine = serpentine_for(kid) ? 1 : 0;
-  ep2.k_rotate = k_rotate_for(kid);
   ep2.sync_every = 0;
   if (g_sync_ctr && sync_every_for(kid) > 0) {
     const int64_t max_tiles = (tiles + units - 1) / units;
