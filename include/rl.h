@@ -153,7 +153,9 @@ typedef struct rl_nvls_reduce {
   int32_t rank;                       /* this rank in the multicast group                  */
   int32_t world;                      /* ranks in the group, 2..RL_NVLS_MAX_RANKS          */
   uint32_t epoch;                     /* > every epoch used before with these flags        */
-  int32_t lag;                        /* tiles between a slab's store and its reduction; 0 = 2 */
+  int32_t lag;                        /* 0: dedicated warps reduce each slab as soon as every
+                                         rank published it (default); > 0: the epilogue warps
+                                         reduce the slab stored `lag` tiles earlier (A/B)     */
   int32_t mode;                       /* rl_nvls_mode                                      */
   int32_t _pad;
 } rl_nvls_reduce;

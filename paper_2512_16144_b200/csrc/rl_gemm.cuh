@@ -34,6 +34,10 @@ namespace rl {
 constexpr int BN = 256, BK = 64;
 constexpr int GEMM_THREADS = 192;                        // 4 epilogue warps
 constexpr int gemm_threads(int epi_warps) { return 64 + 32 * epi_warps; }
+// EPI_F32_NVLS adds 4 communication warps (one per TMEM lane quarter's slabs) that run the
+// cross-rank reductions, so the epilogue warps only drain TMEM, store and publish
+constexpr int comm_warps(int mode);
+constexpr int kernel_threads(int mode, int epi_warps) { return gemm_threads(epi_warps) + 32 * comm_warps(mode); }
 constexpr int EPI_BUF_BYTES = 32 * 128;  // one warp's 32-row x 128-byte store chunk
 constexpr int EPI_BYTES = 4 * 2 * EPI_BUF_BYTES;
 constexpr int BAR_BYTES = 256;
@@ -48,6 +52,7 @@ enum EpiMode {
   EPI_BF16_GROUPED = 6  // grouped GEMM (MoE experts): row groups from device offsets, masked bf16 stores
 };
 constexpr int MAX_GROUPS = 1024;
+constexpr int comm_warps(int mode) { return mode == EPI_F32_NVLS ? 4 : 0; }
 
 constexpr int NVLS_MAX_RANKS = 8;
 
@@ -138,7 +143,9 @@ struct EpiParams {
   uint32_t* nvls_flags[NVLS_MAX_RANKS];    // every rank's flag array ([rank] is local)
   int nvls_rank, nvls_world;
   uint32_t nvls_epoch;
-  int nvls_lag;                            // reduce the slab finished this many tiles ago
+  int nvls_lag;                            // 0: the communication warps reduce each slab once every
+                                           // rank published it; > 0: the epilogue warps reduce the
+                                           // slab finished this many tiles ago (round-1 schedule)
   int nvls_mode;                           // 0 all-reduce (owner tile % world), 1 reduce-scatter by rows
   int64_t nvls_shard;                      // mode 1: rows per rank (a multiple of 32)
   float* nvls_local;                       // mode 1 / row_map: this rank's replica (plain stores)
@@ -261,7 +268,7 @@ __device__ __noinline__ void nvls_reduce_slab_impl(const EpiParams& ep, const Ge
 // (64 B/clk per SM) and the exponentials, and a second warp per SM sub-partition keeps a
 // load in flight while the other computes.
 template <int MODE, bool A_MN, bool B_MN, int CG, int STAGES, int NB = 1, int SKEW = 0, int EW = 4>
-__global__ void __launch_bounds__(gemm_threads(EW), 1)
+__global__ void __launch_bounds__(kernel_threads(MODE, EW), 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const __grid_constant__ CUtensorMap tmC, const GemmShape sh_in, const EpiParams ep) {
   using TL = Tiling<CG>;
@@ -269,6 +276,7 @@ __global__ void __launch_bounds__(gemm_threads(EW), 1)
   static_assert(SKEW < STAGES, "the skewed head/tail holds SKEW stages");
   static_assert(EW == 4 || (EW == 8 && MODE == EPI_LSE), "8 epilogue warps: LSE epilogue only");
   constexpr int TN = BN * NB;                 // tile columns
+  constexpr int kStoreGroups = NB * (BN / 32);  // fp32 store epilogues: bulk groups per tile and warp
   constexpr int NACC = NB == 1 ? 2 : 1;       // TMEM accumulators (512 columns in total)
   constexpr int B_STAGE_ALL = NB * TL::B_STAGE;
   GemmShape sh = sh_in;
@@ -643,6 +651,19 @@ __global__ void __launch_bounds__(gemm_threads(EW), 1)
         RL_AB_FLUSH(0); RL_AB_FLUSH(1); RL_AB_FLUSH(2); RL_AB_FLUSH(7);
       }
     }
+  } else if (warp >= 2 + EW) {
+    // ------------------------------------------------ communication (EPI_F32_NVLS)
+    // Warp 2 + EW + q owns lane quarter q's slabs: for every tile of this CTA, wait until
+    // every rank published the slab, and (if this rank owns it) sum it over the replicas
+    // through the switch. Nothing here touches TMEM, so the MMA never waits for it.
+    if constexpr (MODE == EPI_F32_NVLS) {
+      if (ep.nvls_lag == 0) {
+        const int cq = (warp - 2 - EW) & 3;
+        for (int tile = unit; tile < total; tile += n_units)
+          nvls_reduce_slab_impl<TL::TILE_M, TN>(ep, sh, tile, rank, cq, lane, rows_valid);
+        fence_sys();
+      }
+    }
   } else {
     // ------------------------------------------------------------ epilogue
     const int q = warp & 3;  // TMEM lane quarter this warp may access
@@ -917,24 +938,45 @@ __global__ void __launch_bounds__(gemm_threads(EW), 1)
       }
       if constexpr (MODE == EPI_F32_NVLS) {
         // publish this warp's slab once its stores are globally visible
-        if (ep.row_map != nullptr) fence_sys();  // every lane's plain row stores
-        __syncwarp();
-        if (lane == 0) {
-          bulk_wait_all();
-          fence_async_global();
-          fence_sys();
-          st_release_sys(ep.nvls_flags[ep.nvls_rank] + nvls_slab(tile, rank, q), ep.nvls_epoch);
+        if (ep.row_map != nullptr || ep.nvls_lag > 0) {
+          if (ep.row_map != nullptr) fence_sys();  // every lane's plain row stores
+          __syncwarp();
+          if (lane == 0) {
+            bulk_wait_all();
+            fence_async_global();
+            fence_sys();
+            st_release_sys(ep.nvls_flags[ep.nvls_rank] + nvls_slab(tile, rank, q), ep.nvls_epoch);
+          }
+          __syncwarp();
+          if (ep.nvls_lag > 0 && it >= ep.nvls_lag)
+            nvls_reduce_slab(ep, sh, unit + (it - ep.nvls_lag) * n_units, rank, q, lane);
+        } else if (it > 0) {
+          // TMA stores with communication warps: publish the PREVIOUS tile's slab once
+          // its bulk groups completed (all but this tile's kStoreGroups newest), so the
+          // warp never blocks on the stores it just issued
+          if (lane == 0) {
+            bulk_wait<kStoreGroups>();
+            fence_async_global();
+            fence_sys();
+            st_release_sys(ep.nvls_flags[ep.nvls_rank] + nvls_slab(tile - n_units, rank, q), ep.nvls_epoch);
+          }
+          __syncwarp();
         }
-        __syncwarp();
-        if (it >= ep.nvls_lag) nvls_reduce_slab(ep, sh, unit + (it - ep.nvls_lag) * n_units, rank, q, lane);
       }
       ++it;
       if (NACC == 2) acc ^= 1;
       if (acc == 0) aph ^= 1;
     }
     if constexpr (MODE == EPI_F32_NVLS) {
-      for (int j = it - ep.nvls_lag < 0 ? 0 : it - ep.nvls_lag; j < it; ++j)
-        nvls_reduce_slab(ep, sh, unit + j * n_units, rank, q, lane);
+      if (ep.nvls_lag > 0) {
+        for (int j = it - ep.nvls_lag < 0 ? 0 : it - ep.nvls_lag; j < it; ++j)
+          nvls_reduce_slab(ep, sh, unit + j * n_units, rank, q, lane);
+      } else if (ep.row_map == nullptr && it > 0 && lane == 0) {
+        bulk_wait_all();  // the last tile's slab
+        fence_async_global();
+        fence_sys();
+        st_release_sys(ep.nvls_flags[ep.nvls_rank] + nvls_slab(unit + (it - 1) * n_units, rank, q), ep.nvls_epoch);
+      }
       fence_sys();
     }
     if (lane == 0) bulk_wait_all();

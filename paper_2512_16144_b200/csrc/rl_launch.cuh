@@ -236,7 +236,7 @@ rl_status launch_gemm_cg(int kid, const CUtensorMap& a, const CUtensorMap& b, co
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(units * CG);
-  cfg.blockDim = dim3(rl::gemm_threads(EW));
+  cfg.blockDim = dim3(rl::kernel_threads(MODE, EW));
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];

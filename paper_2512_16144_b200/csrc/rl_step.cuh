@@ -97,7 +97,7 @@ void set_nvls(rl::EpiParams& e, const rl_nvls_reduce* n, float* local, int64_t m
   e.nvls_rank = n->rank;
   e.nvls_world = n->world;
   e.nvls_epoch = n->epoch * kNvlsChunkEpochs + static_cast<uint32_t>(chunk);
-  e.nvls_lag = n->lag > 0 ? n->lag : 2;
+  e.nvls_lag = n->lag > 0 ? n->lag : 0;  // 0: communication warps (default)
 }
 
 rl_status check_nvls(const rl_nvls_reduce* n, const char* what) {

@@ -49,10 +49,11 @@ class NvlsReduction:
         self.handle.barrier(channel=0)
 
     def descriptor(self, lag=None, mode=0) -> rl_nvls_reduce:
-        """lag: the owner reduces a slab this many tiles after its own store of it
-        (more lag = more slack for slower ranks; RL_NVLS_LAG, default 2)."""
+        """lag: 0 (default, RL_NVLS_LAG) = the GEMM's communication warps reduce each
+        slab as soon as every rank published it; > 0 = the epilogue warps reduce the
+        slab stored `lag` tiles earlier (the round-1 schedule, for A/B runs)."""
         if lag is None:
-            lag = int(os.environ.get("RL_NVLS_LAG", "2"))
+            lag = int(os.environ.get("RL_NVLS_LAG", "0"))
         self.epoch += 1
         d = rl_nvls_reduce()
         d.multicast = self.handle.multicast_ptr

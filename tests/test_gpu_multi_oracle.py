@@ -14,7 +14,8 @@ NVLS.
 Data parallel: rank r holds prompt groups 2r, 2r+1 (whole groups: guard and
 advantages stay local) with the global denominator D (R5); modes: NCCL, NVLS
 all-reduce, NVLS reduce-scatter, NVLS with two micro-batches and three dU chunks
-(accumulate, one deferred reduction), NVLS with an empty last rank (T = 0).
+(accumulate, one deferred reduction), NVLS with an empty last rank (T = 0), NVLS
+reduced by the epilogue warps (lag 2) instead of the communication warps.
 Vocab parallel: W row-sharded; modes: NCCL, NVLS dense, NVLS sparse, NVLS sparse
 with dU chunks.
 """
@@ -39,7 +40,7 @@ import torch.multiprocessing as mp  # noqa: E402
 WORLD = min(4, torch.cuda.device_count())
 G = 4
 WL = synth.Workload("multi", 2 * WORLD, G, 96, 512, 3008, delta_sigma=0.5, spike_rate=3e-3)   # equal lengths
-DP_MODES = ["nccl", "nvls", "nvls_rs", "nvls_micro", "nvls_empty"]
+DP_MODES = ["nccl", "nvls", "nvls_rs", "nvls_micro", "nvls_empty", "nvls_lag2"]
 VP_MODES = ["nccl", "nvls_dense", "nvls_sparse", "nvls_sparse_chunked"]
 
 
@@ -87,6 +88,9 @@ def _dp_worker(rank, port, d):
     off = z["offsets"]
     res = {}
     for mode in DP_MODES:
+        # nvls_lag2: the epilogue warps reduce (rl_nvls_reduce.lag = 2, the round-1 schedule)
+        # instead of the dedicated communication warps
+        os.environ["RL_NVLS_LAG"] = "2" if mode == "nvls_lag2" else "0"
         micro = mode == "nvls_micro"
         empty = mode == "nvls_empty" and rank == WORLD - 1
         groups = [2 * rank, 2 * rank + 1]
