@@ -381,3 +381,17 @@ def test_sampled_targets_and_band_plants(wl, dense):
     print(wl.name, "dense" if dense else "sparse", {k: v for k, v in err.items()},
           "mean p_y", float(py.mean()), "plants", len(c.plants))
     assert err["plants_outside_band"] >= 8
+
+
+# H = 8192 (a larger model's hidden size: 128 k-blocks per tile, twice GLM-4.5-Air's), a
+# vocabulary that ends mid-tile (3001 = 11 * 256 + 185), sampled targets and band plants
+WIDE_H = synth.Workload("wide-h", 2, 6, 50, 8192, 3001, ragged=True, delta_sigma=0.5, spike_rate=5e-3)
+
+
+def test_hidden_8192_vs_oracle():
+    c = harness.make_case(WIDE_H, 22, targets="sampled", plants=True)
+    ref = harness.run_oracle(c)
+    for dense in (False, True):
+        gpu = harness.run_gpu_step(c, dense_backward=dense)
+        err = harness.compare(c, ref, gpu)
+        print("H=8192", "dense" if dense else "sparse", err)
