@@ -34,7 +34,8 @@ def test_example_compiles_and_links(tmp_path):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("cfg", [("tiny", 0, [], 2, 4), ("small", 1, ["--tokens", "2048"], 8, 8)])
+# tiny without band plants (so the whole dW is compared), the small shape with them (dH per row)
+@pytest.mark.parametrize("cfg", [("tiny", 0, [], 2, 4), ("small", 1, ["--tokens", "2048", "--plants"], 8, 8)])
 def test_example_step_vs_oracle(tmp_path, cfg):
     torch = pytest.importorskip("torch")
     if not torch.cuda.is_available():
@@ -43,7 +44,7 @@ def test_example_step_vs_oracle(tmp_path, cfg):
     exe = _compile(str(tmp_path / "c_abi_step"))
     art = str(tmp_path / "art")
     subprocess.run([sys.executable, os.path.join(ROOT, "tests", "make_artifact.py"), "--config", name, "--seed",
-                    str(seed), "--out", art, "--plants", *extra], check=True, timeout=600)
+                    str(seed), "--out", art, *extra], check=True, timeout=600)
     r = subprocess.run([exe, art, str(num_prompts), str(group)], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stderr
     print(r.stdout.strip())
@@ -83,7 +84,8 @@ def test_example_step_vs_oracle(tmp_path, cfg):
     sure = ~unsure
     err = harness.dh_row_error(dh[sure], dh_ref[sure], coef[sure], w64, targets[sure])
     assert err <= 1.0, err
-    if not unsure.any():
+    if name == "tiny":
+        assert not unsure.any()
         dw = np.fromfile(os.path.join(art, "c_d_w_vocab.f32"), dtype=np.float32).reshape(w64.shape)
         assert harness.rel_fro(dw, np.load(os.path.join(art, "oracle_d_w_vocab.npy"))) <= harness.GRAD_RTOL
     print(name, "d_hidden_row", err, "unsure rows", int(unsure.sum()))
