@@ -228,6 +228,13 @@ def test_full_size_all_rows_vs_oracle(name):
     wl = FULL[name]
     b = synth.make_batch(wl, 3)
     T, H, V = b.T, b.H, b.V
+    if name == "glm16k":   # the bytes are the committed ones (tests/golden/generator_glm16k_seed3.json)
+        import json
+        import os
+        from synth import artifact
+        gold = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "generator_glm16k_seed3.json")))
+        d = artifact.digests(artifact.batch_arrays(b, np.zeros(T, np.float32)))
+        assert {k: d[k] for k in gold["sha256"]} == gold["sha256"]
     rng = np.random.default_rng(1234)
     dh_rows = np.sort(rng.choice(T, size=4096, replace=False))
     blocks = np.arange(0, V, 256)

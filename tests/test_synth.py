@@ -62,3 +62,18 @@ def test_generator_bytes_match_the_committed_digests():
     d = artifact.digests(artifact.batch_arrays(b, np.zeros(b.T, np.float32)))
     for name in ("hidden.bf16", "w_vocab.bf16", "rewards.f32", "rollout_offsets.i32", "loss_mask.u8"):
         assert d[name] == gold["sha256"][name], name
+
+
+def test_full_size_batch_bytes_match_the_committed_digests():
+    """The glm16k batch the full-size parity test holds to the oracle (seed 3, 134 MB of
+    hidden and 1.24 GB of W_vocab) is regenerated on every machine, not shipped: its
+    generator-only digests are committed (tests/golden/generator_glm16k_seed3.json) and
+    checked here on the CPU and again on the GPU box before the parity run."""
+    import json
+    import os
+    from synth import artifact
+    with open(os.path.join(os.path.dirname(__file__), "golden", "generator_glm16k_seed3.json")) as f:
+        gold = json.load(f)
+    b = synth.make_batch(synth.CONFIGS[gold["config"]], gold["seed"])
+    d = artifact.digests(artifact.batch_arrays(b, np.zeros(b.T, np.float32)))
+    assert {k: d[k] for k in gold["sha256"]} == gold["sha256"]
