@@ -11,13 +11,18 @@
 // BK = 64 (one 128-byte swizzle atom of bf16), a STAGES-deep TMA ring, two TMEM
 // accumulators (2 x 256 columns) so the epilogue of tile i overlaps the MMAs of
 // tile i+1.
-// NB = 2 (wide tiles, CG = 2 store epilogues only): the pair computes 256 x 512
-//         with two N = 256 MMAs per k-step that share the A stage, so each SM moves
-//         48 instead of 64 bytes from L2 per 1024 MMA cycles (3/4). The one
-//         accumulator then fills all 512 TMEM columns and the epilogue is not
-//         overlapped: worth it only where a tile's main loop is long (K5, K6).
-// Warp roles: warp 0 = TMA producer, warp 1 = TMEM owner + MMA issuer
-// (leader CTA), warps 2..5 = epilogue (thread = accumulator row).
+// NB = 2 (wide tiles, CG = 2): the pair computes 256 x 512 with two N = 256 MMAs
+//         per k-step that share the A stage, so each SM moves 48 instead of 64 bytes
+//         from L2 per 1024 MMA cycles (3/4). The one accumulator then fills all 512
+//         TMEM columns; the first / last SKEW k-blocks of a tile run block 0 before
+//         block 1, so each TMEM half drains under the other half's MMAs (K1, K5, K6).
+// Warp roles: warp 0 = TMA producer, warp 1 = TMEM owner + MMA issuer (leader
+// CTA), warps 2 .. 2+EW-1 = epilogue (thread = accumulator row; EW = 8 for K1:
+// two warps per TMEM lane quarter), and for EPI_F32_NVLS 4 more communication
+// warps that run the cross-rank slab reductions (comm_warps()).
+// Order of k-blocks: ascending, or serpentine (odd tiles of a CTA backwards,
+// EpiParams::k_serpentine) for K6 / Newton-Schulz. A soft k-barrier between the
+// producers keeps the CTAs sharing operands inside one L2 window (sync_*).
 //
 // Epilogues:
 //   EPI_LSE  (K1): per row of the tile, online (m, s, u, z_target) over the
@@ -26,6 +31,9 @@
 //   EPI_DZ   (K4): dU = coef*invT*(exp(z - lse) - [v == y]) -> bf16 -> TMA store.
 //   EPI_BF16 (K5): plain bf16 store.   EPI_F32 / EPI_F32_ADD (K5/K6): fp32 store
 //                  or TMA reduce-add into the destination.
+//   EPI_F32_NVLS (K5/K6 multi-GPU): fp32 store into this rank's replica of a
+//                  symmetric buffer + the NVLink-multicast reduction.
+//   EPI_BF16_GROUPED (MoE): masked bf16 stores per expert group, optional row scale.
 #pragma once
 #include "rl_ptx.cuh"
 
