@@ -77,3 +77,18 @@ def test_fault_counters_raise_on_check():
         bad = rl.rl_loss_report(**{key: 2})
         with pytest.raises(rl.RLDataFault, match=key):
             rl.check_faults(bad)
+
+
+def test_moe_helpers_validate_on_the_host(lib):
+    """rl_fold_gamma / rl_expert_load reject bad sizes and misaligned pointers before any
+    device work (include/rl.h), so these run without a GPU."""
+    P = ctypes.c_void_p
+    assert lib.rl_fold_gamma(P(16), P(16), 4, 12, P(16), None) == 2          # K % 8 != 0
+    assert b"multiple of 8" in lib.rl_last_error_message()
+    assert lib.rl_fold_gamma(P(16), P(16), -1, 64, P(16), None) == 2         # rows < 0
+    assert lib.rl_fold_gamma(P(18), P(16), 4, 64, P(16), None) == 1          # w not 16-byte aligned
+    assert b"aligned" in lib.rl_last_error_message()
+    assert lib.rl_fold_gamma(None, P(16), 4, 64, P(16), None) != 0           # null pointer
+    assert lib.rl_fold_gamma(P(16), P(16), 0, 64, P(16), None) == 0          # nothing to do
+    assert lib.rl_expert_load(P(16), 0, 10, P(16), None) == 2                # no groups
+    assert lib.rl_expert_load(None, 4, 10, P(16), None) != 0
