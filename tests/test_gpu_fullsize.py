@@ -329,3 +329,105 @@ def test_hostio_full_size_bitwise_equals_device_path():
     assert outs[0][0]["kept_tokens"] > T // 2 and outs[0][0]["masked_low"] > 0   # a real backward ran
     assert torch.equal(outs[0][1], outs[1][1]) and torch.equal(outs[0][2], outs[1][2])
     print("\n[hostio glm16k] report", outs[1][0])
+
+
+# ------------------------------------------- loss variants at full size (sampled rows)
+VARIANTS_FULL = [
+    dict(variant="cispo", alpha=0.8, beta=1.25, kl_tau=0.0, invt="scalar"),
+    dict(variant="gspo", alpha=0.9, beta=1.1, kl_tau=0.0, invt="rows"),
+    dict(variant="icepop", alpha=0.5, beta=5.0, kl_tau=0.375, kl_set="all", invt="rows"),
+]
+
+
+@pytest.mark.parametrize("cfg", VARIANTS_FULL, ids=lambda c: f"{c['variant']}-kl{c['kl_tau']}-{c['invt']}")
+def test_full_size_variants_sampled_rows(cfg):
+    """SURVEY §8 f2 at the glm16k size in the bench's launch configuration: CISPO (R16),
+    GSPO (R17), the KL term (R19) and per-token temperature (R20) change only S3 (and the
+    scale of z), so the GPU runs all 16384 rows and the loss sits on 512 sampled rows the
+    oracle evaluates one by one: log-probs, gate, coef, loss, dH per row, dW per tile."""
+    wl = synth.CONFIGS["glm16k"]
+    b = synth.make_batch(wl, 21)
+    T, H, V, R = b.T, b.H, b.V, wl.num_rollouts
+    rng = np.random.default_rng(21)
+    rows = np.sort(rng.choice(T, size=512, replace=False))
+    invt_rows = rng.uniform(0.7, 1.5, T).astype(np.float32) if cfg["invt"] == "rows" else None
+    invt_scalar = 1.0 / 0.7
+    invt = invt_rows[rows].astype(np.float64) if invt_rows is not None else invt_scalar
+    h64, w64 = oracle.bf16_to_f64(b.hidden[rows]), oracle.bf16_to_f64(b.w_vocab)
+    Z = oracle.lm_logits(h64, w64, invt)
+    _, _, lse0 = oracle.log_softmax_stats(Z, np.zeros(len(rows), np.int64))
+    y = harness.sample_from_policy(Z, lse0, b.sample_u[rows])
+    targets = b.targets.copy()
+    targets[rows] = y
+    logp0 = Z[np.arange(len(rows)), y] - lse0
+    infer = np.full(T, -5.0, np.float32)
+    infer[rows] = synth.compose_infer_logprobs(logp0, b.delta_noise[rows], np.zeros(len(rows), bool))
+    lm = np.zeros(T, np.uint8)
+    lm[rows] = 1
+    rollout_of = np.repeat(np.arange(R), np.diff(b.rollout_offsets))
+    sub_off = np.concatenate([[0], np.cumsum(np.bincount(rollout_of[rows], minlength=R))]).astype(np.int64)
+    adv = oracle.group_advantages(b.rewards).reshape(-1)
+    D = float(R) if cfg["variant"] == "gspo" else float(len(rows))
+    kw = dict(alpha=cfg["alpha"], beta=cfg["beta"], guard_threshold=synth.GUARD, loss_denominator=D,
+              inv_temperature=invt, backward=False, rollout_adv=adv, variant=cfg["variant"], kl_tau=cfg["kl_tau"],
+              kl_set=cfg.get("kl_set", "masked"))
+    ref = oracle.policy_loss_fwd_bwd(h64, w64, y, infer[rows].astype(np.float64), None, sub_off, None, **kw)
+    # GPU: the whole batch through the C ABI (sparse backward, one 16384-row dU chunk)
+    dev = "cuda"
+    bf = lambda x: torch.from_numpy(x.view(np.int16).copy()).view(torch.bfloat16).to(dev)  # noqa: E731
+    invt_dev = torch.from_numpy(invt_rows).to(dev) if invt_rows is not None else None
+    shape = rl.make_shape(T, H, V, 0, V, invt_scalar if invt_rows is None else 1.0, inv_temperature_rows=invt_dev)
+    params = rl.make_params(R, D, cfg["alpha"], cfg["beta"], synth.GUARD, cfg["variant"], kl_tau=cfg["kl_tau"],
+                            kl_set=cfg.get("kl_set", "masked"))
+    f32 = dict(dtype=torch.float32, device=dev)
+    lp, ent, lse, coef = (torch.empty(T, **f32) for _ in range(4))
+    keep = torch.empty(T, dtype=torch.uint8, device=dev)
+    report = rl.new_report(dev)
+    dh = torch.empty(T, H, dtype=torch.bfloat16, device=dev)
+    dw = torch.empty(V, H, **f32)
+    rl.rl_policy_loss_fwd_bwd(shape, params, bf(b.hidden), bf(b.w_vocab), torch.from_numpy(targets).to(dev),
+                              torch.from_numpy(infer).to(dev), torch.from_numpy(adv.astype(np.float32)).to(dev),
+                              torch.from_numpy(b.rollout_offsets).to(dev), torch.from_numpy(lm).to(dev),
+                              report=report, logprob=lp, entropy=ent, lse=lse, coef=coef, token_keep=keep,
+                              d_hidden=dh, d_w_vocab=dw, dz_chunk_rows=T)
+    torch.cuda.synchronize()
+    rt = torch.from_numpy(rows).to(dev)
+    g_lp, g_ent, g_coef = lp[rt].cpu().numpy(), ent[rt].cpu().numpy(), coef[rt].cpu().numpy()
+    assert np.max(np.abs(g_lp - ref.logp)) <= harness.LOGP_TOL
+    assert np.max(np.abs(g_ent - ref.entropy)) <= harness.LOGP_TOL
+    rep = rl.read_report(report).as_dict()
+    # the gate is exact outside the 1e-4 band (GSPO: of the rollout's sequence ratio)
+    if cfg["variant"] == "gspo":
+        v = ref.report.valid
+        lr = np.where(v, ref.logp - infer[rows].astype(np.float64), 0.0)
+        rsub = np.repeat(np.arange(R), np.diff(sub_off))
+        n = np.bincount(rsub, weights=v.astype(float), minlength=R)
+        s = np.exp(np.bincount(rsub, weights=lr, minlength=R) / np.maximum(n, 1))
+        near = ((np.abs(s - cfg["alpha"]) <= harness.BAND) | (np.abs(s - cfg["beta"]) <= harness.BAND))[rsub]
+    else:
+        k = ref.report.ratio
+        near = (np.abs(k - cfg["alpha"]) <= harness.BAND) | (np.abs(k - cfg["beta"]) <= harness.BAND) | (
+            np.abs(k / synth.GUARD - 1.0) <= harness.BAND)
+    differ = np.nonzero(np.abs(g_coef - ref.report.coef) > 1e-2 * np.abs(ref.report.coef) + 1e-9)[0]
+    assert np.all(near[differ]), differ
+    c_ref = ref.report.coef.copy()
+    c_ref[differ] = g_coef[differ]
+    slack = float(np.abs(g_coef[differ] - ref.report.coef[differ]).sum() * max(1.0, np.abs(ref.logp).max()))
+    assert abs(rep["loss"] - ref.report.loss) <= harness.LOSS_TOL + slack, (rep["loss"], ref.report.loss)
+    # gradients given the gate: dZ_t = invT_t coef_t (p_t - onehot)
+    it = np.broadcast_to(np.asarray(invt, np.float64), (len(rows),))
+    P = np.exp(Z - ref.lse[:, None])
+    dh_ref = (it * c_ref)[:, None] * (P @ w64 - w64[y])
+    err_h = harness.dh_row_error(dh[rt].float().cpu().numpy().astype(np.float64), dh_ref, c_ref, w64, y, it)
+    blocks = np.arange(0, V, 256)
+    ids = np.unique(np.concatenate([blocks + rng.integers(0, 256, len(blocks)), blocks + rng.integers(0, 256, len(blocks))]))
+    ids = ids[ids < V]
+    onehot = (y[:, None] == ids[None, :]).astype(np.float64)
+    dw_ref = ((it * c_ref)[:, None] * (P[:, ids] - onehot)).T @ h64
+    got = dw[torch.from_numpy(ids).to(dev)].cpu().numpy().astype(np.float64)
+    err_w = harness.dw_tile_error(got, dw_ref, c_ref, h64, y, it, row_ids=ids)
+    zero = ~np.isin(np.arange(T), rows)
+    assert not dh.float()[torch.from_numpy(np.nonzero(zero)[0]).to(dev)].any().item()   # coef = 0 rows
+    print(f"\n[{cfg['variant']} kl {cfg['kl_tau']} invT {cfg['invt']}] logp {np.max(np.abs(g_lp - ref.logp)):.3g} "
+          f"coef differ {len(differ)} loss {rep['loss']:.6g} vs {ref.report.loss:.6g} dH row {err_h:.3g} dW tile {err_w:.3g}")
+    assert err_h <= 1.0 and err_w <= 1.0
