@@ -267,6 +267,33 @@ rl_status rl_loss_coef(const rl_loss_params* params, int64_t T, int64_t V_global
                        uint8_t* rollout_guarded, rl_loss_report* report, void* workspace,
                        size_t workspace_bytes, void* stream);
 
+/* Rollouts split across ranks (packed rows sharded by sequence, so a
+ * rollout's tokens may sit on several ranks). The guard of PAPER.md L472 (min over the
+ * rollout's tokens) and GSPO's sequence ratio (R17) then need the whole rollout:
+ *   1. rl_rollout_stats: per local rollout i (rows [offsets[i], offsets[i+1]) of this
+ *      rank), over its valid loss tokens: rollout_kmin[i] = min k
+ *      (+inf if none), rollout_logratio_sum[i] = sum log k (fp64), rollout_n_valid[i].
+ *   2. the caller reduces them over the ranks that hold parts of the same rollout:
+ *      all-reduce MIN of kmin, SUM of logratio_sum and n_valid (R floats each).
+ *   3. rl_loss_coef_ex: rl_loss_coef with those reduced statistics in place of the local
+ *      ones (logratio_sum / n_valid may be NULL except for GSPO). A GSPO rollout adds
+ *      n_local / n_valid of its sequence term to this rank's loss, so the ranks' losses
+ *      sum to the whole batch's. report.guarded_rollouts counts the guarded rollouts with
+ *      rows on this rank (a split rollout is counted by every rank that holds part of it);
+ *      every token counter is exact per rank.
+ * rollout_adv holds the advantages of the local rollouts (from the whole groups' rewards);
+ * rollout_offsets are local (0 .. T). Arrays are DEVICE [num_rollouts]. */
+rl_status rl_rollout_stats(const rl_loss_params* params, int64_t T, int64_t V_global, const float* logprob,
+                           const float* infer_logprobs, const int32_t* targets, const int32_t* rollout_offsets,
+                           const uint8_t* loss_mask, float* rollout_kmin, double* rollout_logratio_sum,
+                           int32_t* rollout_n_valid, void* stream);
+rl_status rl_loss_coef_ex(const rl_loss_params* params, int64_t T, int64_t V_global, const float* logprob,
+                          const float* infer_logprobs, const int32_t* targets, const float* rollout_adv,
+                          const int32_t* rollout_offsets, const uint8_t* loss_mask, const float* rollout_kmin,
+                          const double* rollout_logratio_sum, const int32_t* rollout_n_valid, float* coef,
+                          uint8_t* token_keep, uint8_t* rollout_guarded, rl_loss_report* report, void* workspace,
+                          size_t workspace_bytes, void* stream);
+
 /* S4-S6 on the local shard, given lse and coef for every row:
  * dU = coef invT (softmax - onehot) recomputed chunk by chunk (dz_chunk_rows
  * rows at a time, 0 = all T), d_hidden(_f32) = dU W_shard (a partial sum over

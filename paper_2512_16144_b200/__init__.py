@@ -106,6 +106,10 @@ _SIGS = {
     "rl_merge_partials": (ctypes.c_int, [_P, ctypes.c_int32, ctypes.c_int64, _P, _P, _P, _P]),
     "rl_loss_coef": (ctypes.c_int, [ctypes.POINTER(rl_loss_params), ctypes.c_int64, ctypes.c_int64, _P, _P, _P, _P,
                                     _P, _P, _P, _P, _P, _P, _P, ctypes.c_size_t, _P]),
+    "rl_rollout_stats": (ctypes.c_int, [ctypes.POINTER(rl_loss_params), ctypes.c_int64, ctypes.c_int64, _P, _P, _P,
+                                        _P, _P, _P, _P, _P, _P]),
+    "rl_loss_coef_ex": (ctypes.c_int, [ctypes.POINTER(rl_loss_params), ctypes.c_int64, ctypes.c_int64, _P, _P, _P,
+                                       _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, ctypes.c_size_t, _P]),
     "rl_bwd": (ctypes.c_int, [ctypes.POINTER(rl_lm_shape), _P, _P, _P, _P, _P, _P, _P, _P, ctypes.c_int32,
                               ctypes.c_int64, _P, ctypes.c_size_t, _P]),
     "rl_bwd_ex": (ctypes.c_int, [ctypes.POINTER(rl_lm_shape), _P, _P, _P, _P, _P, _P, _P, _P, ctypes.c_int32,
@@ -323,6 +327,35 @@ def rl_loss_coef(params: rl_loss_params, T: int, V_global: int, logprob, infer_l
                                        _ptr(infer_logprobs), _ptr(targets), _ptr(rollout_adv),
                                        _ptr(rollout_offsets), _ptr(loss_mask), _ptr(coef), _ptr(token_keep),
                                        _ptr(rollout_guarded), _ptr(report), _ptr(ws), ws.numel(), _stream(stream)))
+
+
+def rl_rollout_stats(params: rl_loss_params, T: int, V_global: int, logprob, infer_logprobs, targets,
+                     rollout_offsets, loss_mask, kmin=None, logratio_sum=None, n_valid=None, stream=None):
+    """Per local rollout (min k, sum log k, valid tokens) for rollouts split across ranks;
+    reduce them over the ranks (MIN, SUM, SUM), then call rl_loss_coef_ex."""
+    R = params.num_rollouts
+    dev = rollout_offsets.device
+    kmin = kmin if kmin is not None else torch.empty(R, dtype=torch.float32, device=dev)
+    logratio_sum = logratio_sum if logratio_sum is not None else torch.empty(R, dtype=torch.float64, device=dev)
+    n_valid = n_valid if n_valid is not None else torch.empty(R, dtype=torch.int32, device=dev)
+    _check(load_library().rl_rollout_stats(ctypes.byref(params), int(T), int(V_global), _ptr(logprob),
+                                           _ptr(infer_logprobs), _ptr(targets), _ptr(rollout_offsets),
+                                           _ptr(loss_mask), _ptr(kmin), _ptr(logratio_sum), _ptr(n_valid),
+                                           _stream(stream)))
+    return kmin, logratio_sum, n_valid
+
+
+def rl_loss_coef_ex(params: rl_loss_params, T: int, V_global: int, logprob, infer_logprobs, targets, rollout_adv,
+                    rollout_offsets, loss_mask, rollout_kmin, rollout_logratio_sum, rollout_n_valid, coef,
+                    token_keep=None, rollout_guarded=None, *, report, workspace=None, stream=None):
+    """S3 with rollout statistics reduced over the ranks that share split rollouts."""
+    ws = workspace if workspace is not None else alloc_workspace(48 * max(1, params.num_rollouts), coef.device)
+    _check(load_library().rl_loss_coef_ex(ctypes.byref(params), int(T), int(V_global), _ptr(logprob),
+                                          _ptr(infer_logprobs), _ptr(targets), _ptr(rollout_adv),
+                                          _ptr(rollout_offsets), _ptr(loss_mask), _ptr(rollout_kmin),
+                                          _ptr(rollout_logratio_sum), _ptr(rollout_n_valid), _ptr(coef),
+                                          _ptr(token_keep), _ptr(rollout_guarded), _ptr(report), _ptr(ws),
+                                          ws.numel(), _stream(stream)))
 
 
 def rl_bwd(shape: rl_lm_shape, hidden, w_vocab, targets, lse, coef, d_hidden=None, d_hidden_f32=None,

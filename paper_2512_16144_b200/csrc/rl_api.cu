@@ -209,6 +209,64 @@ rl_status rl_loss_coef(const rl_loss_params* params, int64_t T, int64_t V_global
                    static_cast<cudaStream_t>(stream));
 }
 
+rl_status rl_rollout_stats(const rl_loss_params* params, int64_t T, int64_t V_global, const float* logprob,
+                           const float* infer_logprobs, const int32_t* targets, const int32_t* rollout_offsets,
+                           const uint8_t* loss_mask, float* rollout_kmin, double* rollout_logratio_sum,
+                           int32_t* rollout_n_valid, void* stream) {
+  g_launches = 0;
+  RL_TRY(check_params(params));
+  if (T < 0) return fail(RL_ERR_SHAPE, "T < 0");
+  RL_NONNULL(rollout_offsets);
+  RL_NONNULL(rollout_kmin);
+  RL_NONNULL(rollout_logratio_sum);
+  RL_NONNULL(rollout_n_valid);
+  if (T > 0) {
+    RL_NONNULL(logprob);
+    RL_NONNULL(infer_logprobs);
+  }
+  DevInfo d;
+  RL_TRY(device_info(d));
+  const rl::LossArgs a = loss_args(params, T, V_global, logprob, infer_logprobs, targets, nullptr, rollout_offsets,
+                                   loss_mask);
+  {
+    ProfScope ps(RL_K_LOSS, static_cast<cudaStream_t>(stream));
+    rl::rollout_stats_kernel<<<params->num_rollouts, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+        a, rollout_kmin, rollout_logratio_sum, rollout_n_valid);
+  }
+  RL_CHECK_LAUNCH();
+  return RL_OK;
+}
+
+rl_status rl_loss_coef_ex(const rl_loss_params* params, int64_t T, int64_t V_global, const float* logprob,
+                          const float* infer_logprobs, const int32_t* targets, const float* rollout_adv,
+                          const int32_t* rollout_offsets, const uint8_t* loss_mask, const float* rollout_kmin,
+                          const double* rollout_logratio_sum, const int32_t* rollout_n_valid, float* coef,
+                          uint8_t* token_keep, uint8_t* rollout_guarded, rl_loss_report* report, void* workspace,
+                          size_t workspace_bytes, void* stream) {
+  g_launches = 0;
+  RL_TRY(check_params(params));
+  if (T < 0) return fail(RL_ERR_SHAPE, "T < 0");
+  RL_NONNULL(rollout_adv);
+  RL_NONNULL(rollout_offsets);
+  RL_NONNULL(report);
+  RL_NONNULL(rollout_kmin);
+  if (params->variant == RL_LOSS_GSPO && (!rollout_logratio_sum || !rollout_n_valid))
+    return fail(RL_ERR_INVALID_ARGUMENT, "GSPO over split rollouts needs rollout_logratio_sum and rollout_n_valid");
+  if (T > 0) {
+    RL_NONNULL(logprob);
+    RL_NONNULL(infer_logprobs);
+    RL_NONNULL(coef);
+  }
+  const size_t need = static_cast<size_t>(params->num_rollouts) * sizeof(rl::RolloutPartial);
+  if (!workspace || workspace_bytes < need)
+    return fail(RL_ERR_WORKSPACE, "workspace needs %zu bytes, got %zu", need, workspace_bytes);
+  DevInfo d;
+  RL_TRY(device_info(d));
+  return loss_impl(params, T, V_global, logprob, infer_logprobs, targets, rollout_adv, rollout_offsets, loss_mask,
+                   coef, token_keep, rollout_guarded, report, static_cast<rl::RolloutPartial*>(workspace),
+                   static_cast<cudaStream_t>(stream), rollout_kmin, rollout_logratio_sum, rollout_n_valid);
+}
+
 rl_status rl_bwd(const rl_lm_shape* shape, const uint16_t* hidden, const uint16_t* w_vocab, const int32_t* targets,
                  const float* lse, const float* coef, uint16_t* d_hidden, float* d_hidden_f32, float* d_w_vocab,
                  int32_t accumulate_dw, int64_t dz_chunk_rows, void* workspace, size_t workspace_bytes,

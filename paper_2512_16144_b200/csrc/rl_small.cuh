@@ -133,7 +133,63 @@ struct LossArgs {
   uint8_t* keep;
   uint8_t* guarded;
   RolloutPartial* rp;
+  // rollouts split across ranks: the rollout statistics reduced over every
+  // rank holding part of rollout i (rl_rollout_stats, then all-reduce MIN / SUM / SUM);
+  // NULL = this call holds whole rollouts and computes them itself
+  const float* ext_kmin;     // [R] min over valid tokens of k = exp(logprob - infer), +inf if none
+  const double* ext_lr_sum;  // [R] sum over valid tokens of log k (GSPO)
+  const int32_t* ext_n;      // [R] number of valid tokens (GSPO)
 };
+
+// A loss token that takes part in the loss and the guard: loss_mask, a finite stored
+// log-prob <= 0 and (when targets are given) a target in [0, V_global).
+__device__ __forceinline__ bool token_valid(const LossArgs& a, int64_t t) {
+  const bool lm = a.loss_mask ? (a.loss_mask[t] != 0) : true;
+  const float inf = a.infer[t];
+  const bool fin = isfinite(inf) && inf <= 0.f;
+  bool tg = true;
+  if (a.targets) {
+    const int32_t y = a.targets[t];
+    tg = y >= 0 && static_cast<int64_t>(y) < a.V_global;
+  }
+  return lm && fin && tg;
+}
+
+// Per-rollout statistics of this rank's rows for rollouts split across ranks: one block
+// per rollout, the same validity rule and fixed-order reductions as loss_coef_kernel.
+__global__ void __launch_bounds__(256) rollout_stats_kernel(const LossArgs a, float* __restrict__ kmin_out,
+                                                             double* __restrict__ lr_out, int32_t* __restrict__ n_out) {
+  __shared__ double shd[256];
+  __shared__ uint32_t shu[256];
+  __shared__ float shf[256];
+  const int i = blockIdx.x;
+  int64_t t0 = a.offsets[i], t1 = a.offsets[i + 1];
+  if (t0 < 0 || t1 > a.T || t1 < t0) t0 = t1 = 0;  // malformed offsets: counted by the loss call
+  float kmin = INFINITY;
+  double lr = 0.0;
+  uint32_t n = 0;
+  for (int64_t t = t0 + threadIdx.x; t < t1; t += blockDim.x) {
+    if (token_valid(a, t)) {
+      const float d = a.logprob[t] - a.infer[t];
+      kmin = fminf(kmin, expf(d));
+      lr += static_cast<double>(d);
+      ++n;
+    }
+  }
+  shf[threadIdx.x] = kmin;
+  __syncthreads();
+  for (int s2 = blockDim.x / 2; s2 > 0; s2 >>= 1) {
+    if (threadIdx.x < s2) shf[threadIdx.x] = fminf(shf[threadIdx.x], shf[threadIdx.x + s2]);
+    __syncthreads();
+  }
+  const double lr_all = block_reduce_sum(lr, shd);
+  const uint32_t n_all = block_reduce_sum(n, shu);
+  if (threadIdx.x == 0) {
+    kmin_out[i] = shf[0];
+    lr_out[i] = lr_all;
+    n_out[i] = static_cast<int32_t>(n_all);
+  }
+}
 
 // One block per rollout (256 threads). Pass 1: guard min over valid tokens.
 // Pass 2: Eq.2 gate, coef, counters. Offsets are validated by every block so all
@@ -171,16 +227,8 @@ __global__ void __launch_bounds__(256) loss_coef_kernel(const LossArgs a) {
   double lr_sum = 0.0;
   uint32_t n_valid = 0;
   for (int64_t t = t0 + threadIdx.x; t < t1; t += blockDim.x) {
-    const bool lm = a.loss_mask ? (a.loss_mask[t] != 0) : true;
-    const float inf = a.infer[t];
-    const bool fin = isfinite(inf) && inf <= 0.f;
-    bool tg = true;
-    if (a.targets) {
-      const int32_t y = a.targets[t];
-      tg = y >= 0 && static_cast<int64_t>(y) < a.V_global;
-    }
-    if (lm && fin && tg) {
-      const float d = a.logprob[t] - inf;
+    if (token_valid(a, t)) {
+      const float d = a.logprob[t] - a.infer[t];
       kmin = fminf(kmin, expf(d));
       lr_sum += static_cast<double>(d);
       ++n_valid;
@@ -193,15 +241,19 @@ __global__ void __launch_bounds__(256) loss_coef_kernel(const LossArgs a) {
     if (threadIdx.x < s) shf[threadIdx.x] = fminf(shf[threadIdx.x], shf[threadIdx.x + s]);
     __syncthreads();
   }
-  const bool g = shf[0] < a.guard;
+  const bool g = (a.ext_kmin ? a.ext_kmin[i] : shf[0]) < a.guard;
   __syncthreads();
   // GSPO: s_i, the liveness and clip gate of the rollout (identical in every thread)
   float s_seq = 1.f, gspo_w = 0.f;
   bool gspo_live = false, gspo_clip_lo = false, gspo_clip_hi = false, gspo_u = false;
   double gspo_J = 0.0;
   if (a.variant == RL_LOSS_GSPO) {
-    const double lr = block_reduce_sum(lr_sum, shd);
-    const uint32_t n = block_reduce_sum(n_valid, shu);
+    const double lr_local = block_reduce_sum(lr_sum, shd);
+    const uint32_t n_local = block_reduce_sum(n_valid, shu);
+    // split rollouts: s_i from the whole rollout; this rank adds its share n_local / n of J_i
+    const double lr = a.ext_lr_sum ? a.ext_lr_sum[i] : lr_local;
+    const uint32_t n = a.ext_n ? static_cast<uint32_t>(a.ext_n[i] > 0 ? a.ext_n[i] : 0) : n_local;
+    const double share = (a.ext_n && n > 0) ? static_cast<double>(n_local) / n : 1.0;
     gspo_live = n > 0 && !g;
     s_seq = n > 0 ? static_cast<float>(exp(lr / n)) : 1.f;
     gspo_clip_hi = gspo_live && A > 0.0 && s_seq > a.beta;
@@ -211,7 +263,7 @@ __global__ void __launch_bounds__(256) loss_coef_kernel(const LossArgs a) {
     if (gspo_live) {
       const double sc = fmin(fmax(static_cast<double>(s_seq), static_cast<double>(a.alpha)),
                              static_cast<double>(a.beta));
-      gspo_J = fmin(static_cast<double>(s_seq) * A, sc * A) * a.inv_D;
+      gspo_J = fmin(static_cast<double>(s_seq) * A, sc * A) * a.inv_D * share;
     }
   }
 

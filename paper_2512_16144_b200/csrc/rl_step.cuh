@@ -37,11 +37,10 @@ rl_status forward_impl(const rl_lm_shape* s, const uint16_t* hidden, const uint1
   return RL_OK;
 }
 
-rl_status loss_impl(const rl_loss_params* p, int64_t T, int64_t V_global, const float* logprob, const float* infer,
-                    const int32_t* targets, const float* adv, const int32_t* offsets, const uint8_t* loss_mask,
-                    float* coef, uint8_t* keep, uint8_t* guarded, rl_loss_report* rep, rl::RolloutPartial* rp,
-                    cudaStream_t st) {
-  rl::LossArgs a;
+rl::LossArgs loss_args(const rl_loss_params* p, int64_t T, int64_t V_global, const float* logprob,
+                       const float* infer, const int32_t* targets, const float* adv, const int32_t* offsets,
+                       const uint8_t* loss_mask) {
+  rl::LossArgs a = {};
   a.variant = p->variant;
   a.kl_set = p->kl_set;
   a.kl_w = static_cast<double>(p->kl_tau) / p->loss_denominator;
@@ -58,10 +57,22 @@ rl_status loss_impl(const rl_loss_params* p, int64_t T, int64_t V_global, const 
   a.adv = adv;
   a.offsets = offsets;
   a.loss_mask = loss_mask;
+  return a;
+}
+
+rl_status loss_impl(const rl_loss_params* p, int64_t T, int64_t V_global, const float* logprob, const float* infer,
+                    const int32_t* targets, const float* adv, const int32_t* offsets, const uint8_t* loss_mask,
+                    float* coef, uint8_t* keep, uint8_t* guarded, rl_loss_report* rep, rl::RolloutPartial* rp,
+                    cudaStream_t st, const float* ext_kmin = nullptr, const double* ext_lr_sum = nullptr,
+                    const int32_t* ext_n = nullptr) {
+  rl::LossArgs a = loss_args(p, T, V_global, logprob, infer, targets, adv, offsets, loss_mask);
   a.coef = coef;
   a.keep = keep;
   a.guarded = guarded;
   a.rp = rp;
+  a.ext_kmin = ext_kmin;
+  a.ext_lr_sum = ext_lr_sum;
+  a.ext_n = ext_n;
   {
     ProfScope ps(RL_K_LOSS, st);
     rl::loss_coef_kernel<<<p->num_rollouts, 256, 0, st>>>(a);

@@ -8,6 +8,10 @@ split-phase C calls for all arithmetic.
 * VocabParallelPolicyLoss — W row-sharded; K1 partials (16 B/token) are
   all-gathered and merged in rank order; S3 runs redundantly; the dH partials
   are all-reduced; each rank keeps its complete dW shard.
+* SplitRolloutPolicyLoss — data parallel over ANY split of the packed rows, so a
+  rollout may straddle ranks (CP-style): the guard's per-rollout min
+  ratio is all-reduced (MIN), GSPO's log-ratio sums and counts (SUM); advantages
+  come from the whole groups' rewards; dW is all-reduced.
 
 The arithmetic goes through a `phases` object with librl's split-phase
 signatures. `LibrlPhases` (the C ABI) is the only implementation in the
@@ -22,6 +26,7 @@ import torch.distributed as dist
 
 from . import (RL_BWD_ALL, RL_BWD_DENSE, RL_BWD_DH, RL_BWD_DU, RL_BWD_DW, alloc_workspace, make_params,
                make_shape, rl_bwd_ex, rl_fwd_partials, rl_group_advantages, rl_last_launch_count, rl_logprob_fwd, rl_loss_coef,
+               rl_loss_coef_ex, rl_rollout_stats,
                rl_merge_partials, rl_ns_shard_apply, rl_ns_shard_gram, rl_ns_shard_sumsq,
                rl_nvls_flag_count, rl_nvls_reduce, rl_nvls_shard_rows, rl_policy_loss_fwd_bwd, rl_workspace_bytes)
 
@@ -107,6 +112,18 @@ class LibrlPhases:
                   report, workspace=None):
         rl_loss_coef(params, T, V_global, logprob, infer, targets, adv, offsets, loss_mask, coef, keep, guarded,
                      report=report, workspace=workspace)
+        self._count()
+
+    def rollout_stats(self, params, T, V_global, logprob, infer, targets, offsets, loss_mask, kmin, logratio_sum,
+                      n_valid):
+        rl_rollout_stats(params, T, V_global, logprob, infer, targets, offsets, loss_mask, kmin, logratio_sum,
+                         n_valid)
+        self._count()
+
+    def loss_coef_ex(self, params, T, V_global, logprob, infer, targets, adv, offsets, loss_mask, kmin, logratio_sum,
+                     n_valid, coef, keep, guarded, report, workspace=None):
+        rl_loss_coef_ex(params, T, V_global, logprob, infer, targets, adv, offsets, loss_mask, kmin, logratio_sum,
+                        n_valid, coef, keep, guarded, report=report, workspace=workspace)
         self._count()
 
     def bwd(self, shape, hidden, w_shard, targets, lse, coef, d_hidden_f32, d_w_vocab, dz_chunk_rows=0,
@@ -373,6 +390,99 @@ class DataParallelPolicyLoss:
         ph.bwd_phases(self.shape, hidden, w, targets, self.lse, self.coef, self.d_hidden, d_w_vocab, RL_BWD_DH,
                       max_sms=self.dh_sms, workspace=self.ws)
         main.wait_stream(self.comm)
+        return d_w_vocab
+
+
+class SplitRolloutPolicyLoss:
+    """Data parallel over an arbitrary split of the packed rows (sequence
+    sharding): rank r holds rows [row_start, row_start + T) of the global batch whose
+    rollouts are `global_offsets` ([R_global + 1], host), so the first and last rollouts
+    of a rank may continue on its neighbours. What couples the ranks, besides the dW
+    all-reduce:
+      * the guard is a min over the WHOLE rollout: per-rollout min ratios of
+        every rank are all-reduced (MIN) over [R_global] floats before S3;
+      * GSPO's sequence ratio (R17) needs the whole rollout's log-ratio sum and token
+        count (SUM over [R_global]);
+      * advantages use whole groups: every rank computes them from all
+        R_global rewards (a few hundred floats) and keeps its rollouts' slice;
+      * D (R5) is the global count of loss tokens.
+    Loss values add up over ranks (a split GSPO rollout contributes n_local / n of its
+    term on each rank); report.guarded_rollouts is per rank (split rollouts count on
+    every rank that holds part of them) — `guarded_global` is the exact count."""
+
+    def __init__(self, phases, *, T, H, V, global_offsets, row_start, group_size, loss_denominator, group=None,
+                 inv_temperature=1.0, alpha=0.5, beta=5.0, guard=1e-5, variant="icepop", kl_tau=0.0,
+                 kl_set="masked", device=None, d_hidden_dtype=torch.bfloat16, workspace=True, dz_chunk_rows=0):
+        import numpy as np
+        self.ph = phases
+        self.group = group
+        self.T, self.H, self.V, self.G = T, H, V, group_size
+        off = np.asarray(global_offsets, dtype=np.int64)
+        self.R_global = len(off) - 1
+        lo, hi = int(row_start), int(row_start) + T
+        # the global rollouts with at least one row in [lo, hi) (empty rollouts at the
+        # boundary are kept by the rank whose range contains their position)
+        ids = [i for i in range(self.R_global) if off[i] < hi and off[i + 1] > lo or (off[i] == off[i + 1] and lo <= off[i] < hi)]
+        self.r_lo = ids[0] if ids else 0
+        self.r_hi = ids[-1] + 1 if ids else 0
+        self.R = self.r_hi - self.r_lo
+        loc = np.clip(off[self.r_lo:self.r_hi + 1] - lo, 0, T) if self.R else np.zeros(1, np.int64)
+        self.offsets = torch.from_numpy(loc.astype(np.int32)).to(device)
+        self.chunk = dz_chunk_rows
+        self.shape = make_shape(T, H, V, 0, V, inv_temperature)
+        self.params = make_params(max(1, self.R), loss_denominator, alpha, beta, guard, variant, kl_tau, kl_set)
+        f32 = dict(dtype=torch.float32, device=device)
+        self.logprob, self.entropy, self.lse, self.coef = (torch.empty(T, **f32) for _ in range(4))
+        self.keep = torch.empty(T, dtype=torch.uint8, device=device)
+        self.guarded = torch.empty(max(1, self.R), dtype=torch.uint8, device=device)
+        self.adv_global = torch.empty(self.R_global, **f32)
+        self.kmin = torch.empty(max(1, self.R), **f32)
+        self.lr = torch.empty(max(1, self.R), dtype=torch.float64, device=device)
+        self.n = torch.empty(max(1, self.R), dtype=torch.int32, device=device)
+        self.kmin_g = torch.empty(self.R_global, **f32)
+        self.lr_g = torch.empty(self.R_global, dtype=torch.float64, device=device)
+        self.n_g = torch.empty(self.R_global, dtype=torch.int32, device=device)
+        self.report = torch.zeros(48, dtype=torch.uint8, device=device)
+        self.d_hidden = torch.empty(T, H, dtype=d_hidden_dtype, device=device)
+        self.ws = (alloc_workspace(rl_workspace_bytes(self.shape, max(1, self.R), dz_chunk_rows), device)
+                   if workspace else None)
+        self.loss_ws = alloc_workspace(48 * max(1, self.R), device) if workspace else None
+        self.guarded_global = 0
+
+    def step(self, hidden, w, targets, infer, rewards_global, loss_mask, d_w_vocab):
+        """rewards_global: [R_global] rewards of every rollout of the step (group-major).
+        Returns d_w_vocab, all-reduced over the group."""
+        ph, R, a, b = self.ph, self.R, self.r_lo, self.r_hi
+        ph.group_advantages(rewards_global, self.G, self.adv_global)
+        ph.logprob_fwd(self.shape, hidden, w, targets, self.logprob, self.entropy, self.lse, workspace=self.ws)
+        if R:
+            ph.rollout_stats(self.params, self.T, self.V, self.logprob, infer, targets, self.offsets, loss_mask,
+                             self.kmin, self.lr, self.n)
+        # the rollouts' statistics over every rank that holds part of them
+        self.kmin_g.fill_(float("inf"))
+        self.lr_g.zero_()
+        self.n_g.zero_()
+        if R:
+            self.kmin_g[a:b] = self.kmin[:R]
+            self.lr_g[a:b] = self.lr[:R]
+            self.n_g[a:b] = self.n[:R]
+        dist.all_reduce(self.kmin_g, op=dist.ReduceOp.MIN, group=self.group)
+        dist.all_reduce(self.lr_g, group=self.group)
+        dist.all_reduce(self.n_g, group=self.group)
+        self.guarded_global = int((self.kmin_g < self.params.guard_threshold).sum().item())
+        if R:
+            self.kmin[:R] = self.kmin_g[a:b]
+            self.lr[:R] = self.lr_g[a:b]
+            self.n[:R] = self.n_g[a:b]
+            ph.loss_coef_ex(self.params, self.T, self.V, self.logprob, infer, targets, self.adv_global[a:b].contiguous(),
+                            self.offsets, loss_mask, self.kmin, self.lr, self.n, self.coef, self.keep, self.guarded,
+                            self.report, workspace=self.loss_ws)
+        else:
+            self.coef.zero_()
+            self.keep.zero_()
+        ph.bwd_phases(self.shape, hidden, w, targets, self.lse, self.coef, self.d_hidden, d_w_vocab, RL_BWD_ALL,
+                      workspace=self.ws)
+        dist.all_reduce(d_w_vocab, group=self.group)                                      # the exchange
         return d_w_vocab
 
 

@@ -136,7 +136,9 @@ def band_tokens(c: Case, ref) -> np.ndarray:
         n = np.bincount(rollout_of, weights=v.astype(float), minlength=R)
         s = np.exp(np.bincount(rollout_of, weights=lr, minlength=R) / np.maximum(n, 1))
         near = (np.abs(s - c.alpha) <= BAND) | (np.abs(s - c.beta) <= BAND)
-        return v & near[rollout_of]
+        # the rollout guard applies to GSPO too (R17): its band counts as well
+        gnear = np.abs(ref.report.ratio / c.guard - 1.0) <= BAND if c.guard > 0 else np.zeros(len(v), bool)
+        return v & (near[rollout_of] | gnear)
     k = ref.report.ratio
     v = ref.report.valid
     near = (np.abs(k - c.alpha) <= BAND) | (np.abs(k - c.beta) <= BAND)

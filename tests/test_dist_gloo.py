@@ -97,6 +97,48 @@ class OraclePhases:
         self.loss = res.report.loss
 
 
+    # split rollouts (SplitRolloutPolicyLoss); IcePop only in this double
+    def logprob_fwd(self, shape, hidden, w, targets, logprob, entropy, lse, workspace=None):
+        Z = oracle.lm_logits(hidden.double().numpy(), w.double().numpy(), shape.inv_temperature)
+        lp, ent, l = oracle.log_softmax_stats(Z, targets.long().numpy())
+        logprob.copy_(torch.from_numpy(lp))
+        entropy.copy_(torch.from_numpy(ent))
+        lse.copy_(torch.from_numpy(l))
+
+    @staticmethod
+    def _valid(V, infer, targets, loss_mask):
+        inf, y = infer.double().numpy(), targets.long().numpy()
+        return loss_mask.numpy().astype(bool) & np.isfinite(inf) & (inf <= 0) & (y >= 0) & (y < V)
+
+    def rollout_stats(self, params, T, V, logprob, infer, targets, offsets, loss_mask, kmin, logratio_sum, n_valid):
+        d = logprob.double().numpy() - infer.double().numpy()
+        v = self._valid(V, infer, targets, loss_mask)
+        off = offsets.numpy()
+        for i in range(len(off) - 1):
+            sel = v[off[i]:off[i + 1]]
+            di = d[off[i]:off[i + 1]][sel]
+            kmin[i] = float(np.exp(di).min()) if di.size else float("inf")
+            logratio_sum[i] = float(di.sum())
+            n_valid[i] = int(sel.sum())
+
+    def loss_coef_ex(self, params, T, V, logprob, infer, targets, adv, offsets, loss_mask, kmin, logratio_sum,
+                     n_valid, coef, keep, guarded, report, workspace=None):
+        assert params.variant == 0, "the double implements IcePop only"
+        v = self._valid(V, infer, targets, loss_mask)
+        k = np.exp(logprob.double().numpy() - infer.double().numpy())
+        g = kmin.double().numpy()[: len(offsets) - 1] < params.guard_threshold       # the reduced guard
+        rollout_of = np.repeat(np.arange(len(offsets) - 1), np.diff(offsets.numpy()))
+        kp = v & (oracle.masking_function(k, params.alpha, params.beta) > 0) & ~g[rollout_of]
+        c = np.where(kp, k * adv.double().numpy()[rollout_of] / params.loss_denominator, 0.0)
+        coef.copy_(torch.from_numpy(c))
+        keep.copy_(torch.from_numpy(kp.astype(np.uint8)))
+        guarded[: len(g)] = torch.from_numpy(g.astype(np.uint8))
+        self.loss = -float(c.sum())
+
+    def bwd_phases(self, shape, hidden, w, targets, lse, coef, d_hidden, d_w_vocab, phases, max_sms=0,
+                   workspace=None):
+        self.bwd(shape, hidden, w, targets, lse, coef, d_hidden, d_w_vocab)
+
     # row-sharded Newton-Schulz (fp64, the oracle's quintic)
     def ns_sumsq(self, g, sumsq, workspace):
         sumsq.fill_(float((g.double() ** 2).sum()))
@@ -288,3 +330,54 @@ def test_row_sharded_newton_schulz_composition(tmp_path):
     got = np.concatenate([np.load(tmp_path / f"ns{r}.npy") for r in range(WORLD)])
     G = np.random.default_rng(3).standard_normal((96, 16))
     np.testing.assert_allclose(got, oracle.muon.newton_schulz(G, 5), rtol=0, atol=1e-12)
+
+
+# ---------------------------------------------- rollouts split across ranks (§8(e))
+def _split_worker(rank, port, out_dir, bounds):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    world = len(bounds) - 1
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    b, h64, w64, infer = _batch()
+    lo, hi = bounds[rank], bounds[rank + 1]
+    eng = parallel.SplitRolloutPolicyLoss(OraclePhases(), T=hi - lo, H=b.H, V=b.V, global_offsets=b.rollout_offsets,
+                                          row_start=lo, group_size=WL.group_size,
+                                          loss_denominator=b.loss_denominator, device="cpu",
+                                          d_hidden_dtype=torch.float64, workspace=False)
+    for name in ("logprob", "entropy", "lse", "coef", "adv_global", "kmin", "kmin_g"):
+        setattr(eng, name, getattr(eng, name).double())
+    dw = torch.empty(b.V, b.H, dtype=torch.float64)
+    eng.step(_bf16(b.hidden[lo:hi]), _bf16(b.w_vocab), torch.from_numpy(b.targets[lo:hi].copy()),
+             torch.from_numpy(infer[lo:hi].copy()), torch.from_numpy(b.rewards.reshape(-1).copy()),
+             torch.from_numpy(b.loss_mask[lo:hi].copy()), dw)
+    loss = torch.tensor([getattr(eng.ph, "loss", 0.0)], dtype=torch.float64)
+    dist.all_reduce(loss)
+    np.savez(os.path.join(out_dir, f"sp{rank}.npz"), dh=eng.d_hidden.numpy(), dw=dw.numpy(), coef=eng.coef.numpy(),
+             loss=loss.numpy(), guarded=eng.guarded_global, R=eng.R)
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_split_rollout_composition(tmp_path, world):
+    """Packed rows split at arbitrary positions, cutting through rollouts (one boundary
+    inside a guarded rollout): the ranks' coefficients, dH rows, all-reduced dW and the
+    summed loss equal the oracle of the whole batch, and the guard decision of a split
+    rollout is the whole rollout's (the reduced min ratio)."""
+    b, ref = _reference(0)
+    T = b.T
+    g = np.nonzero(ref.report.guarded)[0]
+    assert len(g), "the batch needs a guarded rollout"
+    gi = int(g[len(g) // 2])
+    cut = int((b.rollout_offsets[gi] + b.rollout_offsets[gi + 1]) // 2)        # inside a guarded rollout
+    assert b.rollout_offsets[gi] < cut < b.rollout_offsets[gi + 1]
+    rng = np.random.default_rng(world)
+    others = sorted(rng.choice(np.setdiff1d(np.arange(1, T), [cut]), size=world - 2, replace=False).tolist())
+    bounds = [0] + sorted([cut] + others) + [T]
+    mp.start_processes(_split_worker, args=(_free_port(), str(tmp_path), bounds), nprocs=world, start_method="spawn")
+    outs = [np.load(tmp_path / f"sp{r}.npz") for r in range(world)]
+    np.testing.assert_allclose(np.concatenate([o["coef"] for o in outs]), ref.report.coef, atol=1e-12)
+    np.testing.assert_allclose(np.concatenate([o["dh"] for o in outs]), ref.d_hidden, atol=1e-12)
+    for o in outs:
+        np.testing.assert_allclose(o["dw"], ref.d_w_vocab, atol=1e-12)
+        assert float(o["loss"][0]) == pytest.approx(ref.report.loss, abs=1e-12)
+        assert int(o["guarded"]) == int(ref.report.guarded_rollouts)
+
