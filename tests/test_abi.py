@@ -92,3 +92,22 @@ def test_moe_helpers_validate_on_the_host(lib):
     assert lib.rl_fold_gamma(P(16), P(16), 0, 64, P(16), None) == 0          # nothing to do
     assert lib.rl_expert_load(P(16), 0, 10, P(16), None) == 2                # no groups
     assert lib.rl_expert_load(None, 4, 10, P(16), None) != 0
+
+
+def test_split_rollout_calls_validate_on_the_host(lib):
+    P = ctypes.c_void_p
+    p = rl.make_params(4, 10.0, variant="gspo")
+    args = [P(16)] * 6   # logprob, infer, targets, adv, offsets, loss_mask
+    # GSPO over split rollouts needs the log-ratio sums and counts
+    st = lib.rl_loss_coef_ex(ctypes.byref(p), 10, 100, *args, P(16), None, None, P(16), None, None, P(16), P(16),
+                             4096, None)
+    assert st == 1 and b"GSPO" in lib.rl_last_error_message()
+    p = rl.make_params(4, 10.0)
+    st = lib.rl_loss_coef_ex(ctypes.byref(p), 10, 100, *args, None, None, None, P(16), None, None, P(16), P(16),
+                             4096, None)
+    assert st != 0                                                     # rollout_kmin is required
+    st = lib.rl_rollout_stats(ctypes.byref(p), 10, 100, P(16), P(16), P(16), P(16), None, None, P(16), P(16), None)
+    assert st != 0                                                     # kmin output is required
+    p = rl.make_params(4, 0.0)
+    st = lib.rl_rollout_stats(ctypes.byref(p), 10, 100, P(16), P(16), P(16), P(16), None, P(16), P(16), P(16), None)
+    assert st == 1                                                     # D <= 0
