@@ -1,5 +1,5 @@
 """Small end-to-end cases (tiny config, ragged tails, split phases) for compute-sanitizer.
-usage: compute-sanitizer --tool memcheck python tools/sanitize_case.py"""
+usage: compute-sanitizer --tool memcheck python tests/sanitize_case.py"""
 import os
 import sys
 
