@@ -282,7 +282,7 @@ __global__ void __launch_bounds__(kernel_threads(MODE, EW), 1)
   using TL = Tiling<CG>;
   static_assert(NB == 1 || (NB == 2 && CG == 2 && MODE != EPI_BF16_GROUPED), "wide tiles: CTA pairs, not grouped");
   static_assert(SKEW < STAGES, "the skewed head/tail holds SKEW stages");
-  static_assert(EW == 4 || (EW == 8 && MODE == EPI_LSE), "8 epilogue warps: LSE epilogue only");
+  static_assert(EW == 4 || ((EW == 8 || EW == 16) && MODE == EPI_LSE), "8 / 16 epilogue warps: LSE epilogue only");
   constexpr int TN = BN * NB;                 // tile columns
   constexpr int kStoreGroups = NB * (BN / 32);  // fp32 store epilogues: bulk groups per tile and warp
   constexpr int NACC = NB == 1 ? 2 : 1;       // TMEM accumulators (512 columns in total)
@@ -786,21 +786,26 @@ __global__ void __launch_bounds__(kernel_threads(MODE, EW), 1)
               trun = fmaf(e, d, trun);
             }
           }
-          if constexpr (EW == 8) {
-            // merge the two column halves' states: (m, s, u) in log2 units, zt by max
-            // two slot sets used alternately: a set is rewritten only after the barrier of
-            // the following merge, which the reading warp reaches after reading it
-            float4* slot = reinterpret_cast<float4*>(sEpi) + ((merge_ctr++ & 1) * 4 + q) * 32 + lane;
-            if (cgrp == 1) *slot = make_float4(mrun, srun, trun, zt);
-            named_bar_sync(1 + q, 64);
-            if (cgrp == 1) continue;
-            const float4 o = *slot;
-            const float mn = fmaxf(mrun, o.x);
-            const float a1 = ex2f(mrun - mn), a2 = ex2f(o.x - mn);
-            trun = a1 * fmaf(srun, mrun - mn, trun) + a2 * fmaf(o.y, o.x - mn, o.z);
-            srun = a1 * srun + a2 * o.y;
-            mrun = mn;
-            zt = fmaxf(zt, o.w);
+          if constexpr (EW > 4) {
+            // merge the column groups' states into group 0: (m, s, u) in log2 units, zt by
+            // max, in group order (deterministic). Two slot sets used alternately: a set is
+            // rewritten only after the barrier of the following merge, which the reading
+            // warp reaches after reading it.
+            constexpr int NG = EW / 4;
+            float4* slots = reinterpret_cast<float4*>(sEpi) + ((merge_ctr++ & 1) * 4 + q) * (NG - 1) * 32 + lane;
+            if (cgrp > 0) slots[(cgrp - 1) * 32] = make_float4(mrun, srun, trun, zt);
+            named_bar_sync(1 + q, 32 * NG);
+            if (cgrp > 0) continue;
+  #pragma unroll
+            for (int gi = 0; gi < NG - 1; ++gi) {
+              const float4 o = slots[gi * 32];
+              const float mn = fmaxf(mrun, o.x);
+              const float a1 = ex2f(mrun - mn), a2 = ex2f(o.x - mn);
+              trun = a1 * fmaf(srun, mrun - mn, trun) + a2 * fmaf(o.y, o.x - mn, o.z);
+              srun = a1 * srun + a2 * o.y;
+              mrun = mn;
+              zt = fmaxf(zt, o.w);
+            }
           }
           if (row_ok && n0 < ep.cols) {  // one partial per 256-column block
             constexpr float LN2 = 0.69314718055994530942f;

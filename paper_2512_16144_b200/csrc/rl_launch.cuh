@@ -155,12 +155,12 @@ int skew() {
   }();
   return v;
 }
-// Epilogue warps of the LSE GEMM (K1): RL_EPI_WARPS[_FWD] = 4 or 8 (default 8, two
+// Epilogue warps of the LSE GEMM (K1): RL_EPI_WARPS[_FWD] = 4, 8 or 16 (default 8, two
 // warps per TMEM lane quarter; see rl_gemm.cuh).
 int epi_warps_for(int kid) {
   static const std::array<int, kKnobKids> env = env_table("RL_EPI_WARPS", -1);
   if (kid < 0 || kid >= kKnobKids) return 4;
-  return env[kid] == 4 ? 4 : 8;
+  return env[kid] == 4 ? 4 : (env[kid] == 16 ? 16 : 8);
 }
 int sync_slack_for(int kid) {
   static const std::array<int, kKnobKids> env = env_table("RL_SYNC_SLACK", -1);
@@ -288,6 +288,9 @@ rl_status launch_gemm(int kid, const CUtensorMap& a, const CUtensorMap& b, const
     if (epi_warps_for(kid) == 8)
       return launch_gemm_ew<MODE, A_MN, B_MN, 8>(kid, a, b, c, M, N, K, group_m, ep, sms, st, k_splits, split_rows,
                                                  dyn_count, dyn_mode);
+    if (epi_warps_for(kid) == 16)
+      return launch_gemm_ew<MODE, A_MN, B_MN, 16>(kid, a, b, c, M, N, K, group_m, ep, sms, st, k_splits, split_rows,
+                                                  dyn_count, dyn_mode);
   }
   return launch_gemm_ew<MODE, A_MN, B_MN, 4>(kid, a, b, c, M, N, K, group_m, ep, sms, st, k_splits, split_rows,
                                              dyn_count, dyn_mode);
