@@ -315,3 +315,55 @@ def test_oracle_deterministic():
     r2 = oracle.policy_loss_fwd_bwd(h, W, b.targets, infer, b.rewards, b.rollout_offsets)
     assert r1.report.loss == r2.report.loss
     assert np.array_equal(r1.d_w_vocab, r2.d_w_vocab)
+
+
+# ------------------------------------------------- direct pins of the remaining helpers
+def test_validate_offsets_hand_cases():
+    """CSR rollout offsets (SPEC 'misaligned lengths'): start at 0, end at T,
+    never decrease. Each rule broken once."""
+    from oracle.icepop import validate_offsets
+    assert validate_offsets([0, 3, 3, 7], 7)            # an empty rollout is fine
+    assert validate_offsets([0], 0)
+    assert not validate_offsets([1, 3, 7], 7)           # does not start at 0
+    assert not validate_offsets([0, 3, 6], 7)           # does not end at T
+    assert not validate_offsets([0, 5, 3, 7], 7)        # decreasing
+
+
+def test_icepop_backward_hand_example():
+    """dZ = coef invT (softmax - onehot), dH = dZ W, dW = dZ^T h on a 1-row, 2-word
+    vocabulary worked by hand: z = (0, ln 3) -> p = (1/4, 3/4); y = 1, coef = 2,
+    invT = 1/2 -> dZ = 2 * 1/2 * (1/4, 3/4 - 1) = (1/4, -1/4)."""
+    Z = np.array([[0.0, np.log(3.0)]])
+    lse = np.array([np.log(4.0)])
+    h = np.array([[2.0, -1.0]])
+    W = np.array([[1.0, 0.0], [0.0, 1.0]])
+    dZ, dH, dW = oracle.icepop_backward(Z, lse, np.array([1]), np.array([2.0]), h, W, 0.5)
+    np.testing.assert_allclose(dZ, [[0.25, -0.25]], atol=1e-15)
+    np.testing.assert_allclose(dH, [[0.25, -0.25]], atol=1e-15)          # dZ @ I
+    np.testing.assert_allclose(dW, [[0.5, -0.25], [-0.5, 0.25]], atol=1e-15)   # dZ^T h
+
+
+def test_variant_loss_dispatch():
+    """variant_loss is a name -> function table: each name reaches its own definition
+    (a swapped entry would compute another variant's coefficients)."""
+    from oracle import icepop as ic
+    rng = np.random.default_rng(4)
+    lp = -rng.uniform(0.1, 3.0, 12)
+    inf = lp + rng.normal(0, 0.5, 12)
+    inf = np.minimum(inf, 0.0)
+    args = (lp, inf, np.array([0.5, -0.5, 1.0]), np.array([0, 4, 8, 12]), None, 0.8, 1.2, 1e-5, 12.0)
+    for name, fn in (("icepop", ic.icepop_loss), ("cispo", ic.cispo_loss), ("gspo", ic.gspo_loss)):
+        a, b = ic.variant_loss(name, *args), fn(*args)
+        np.testing.assert_array_equal(a.coef, b.coef)
+        assert a.loss == b.loss
+    assert not np.array_equal(ic.variant_loss("icepop", *args).coef, ic.variant_loss("cispo", *args).coef)
+
+
+def test_grouped_mm_rmsnorm_hand_example():
+    """The expert projection of normalised tokens on a 1-token, 1-expert case by hand:
+    x = (3, 4) -> rms = sqrt(12.5), gamma = (1, 2), W = [[1, 1]] ->
+    y = (3 * 1 + 4 * 2) / sqrt(12.5) = 11 / sqrt(12.5)."""
+    from oracle import moe
+    y = moe.grouped_mm_rmsnorm(np.array([[3.0, 4.0]]), np.array([1.0, 2.0]), np.array([[[1.0, 1.0]]]),
+                               np.array([0, 1]), eps=0.0)
+    assert y[0, 0] == pytest.approx(11.0 / np.sqrt(12.5), rel=1e-14)
