@@ -40,8 +40,8 @@
 namespace rl {
 
 constexpr int BN = 256, BK = 64;
-constexpr int GEMM_THREADS = 192;                        // 4 epilogue warps
 constexpr int gemm_threads(int epi_warps) { return 64 + 32 * epi_warps; }
+constexpr int GEMM_THREADS = gemm_threads(4);  // the 4-epilogue-warp kernels (grouped GEMM, diagnostics)
 // EPI_F32_NVLS adds 4 communication warps (one per TMEM lane quarter's slabs) that run the
 // cross-rank reductions, so the epilogue warps only drain TMEM, store and publish
 constexpr int comm_warps(int mode);
