@@ -255,6 +255,10 @@ def _setup(args):
     if r.world > 1:
         dist.init_process_group("nccl", device_id=dev)
     r.name, r.wl = workload_for(args, r.world)
+    if args.tokens:
+        # A/B knob: the same shape with another micro-batch size (rollouts keep their count)
+        import dataclasses
+        r.wl = dataclasses.replace(r.wl, rollout_len=max(1, int(args.tokens) // r.wl.num_rollouts))
     if args.delta_sigma is not None:
         # A/B knob: the trainer-inference mismatch of the stress config on another shape
         # (e.g. vocab-parallel glm64k with ~43% of rows masked, for the sparse backward)
@@ -699,6 +703,8 @@ def main():
                     help="nvls: the dW (DP) / dH (vocab-parallel) all-reduce is fused into the GEMM epilogue "
                          "over NVLink multicast; auto = nvls when the GPUs support multicast, else NCCL")
     ap.add_argument("--comm-sms", type=int, default=24, help="DP overlap: SMs left to NCCL while K5 runs")
+    ap.add_argument("--tokens", type=int, default=0,
+                    help="override the workload's tokens per rank (A/B: micro-batch size sweep)")
     ap.add_argument("--delta-sigma", type=float, default=None,
                     help="override the workload's log-prob mismatch sigma (A/B: 1.0 = the stress config's)")
     ap.add_argument("--targets", default="sampled", choices=["sampled", "uniform"],
