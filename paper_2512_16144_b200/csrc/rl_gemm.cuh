@@ -736,6 +736,14 @@ __global__ void __launch_bounds__(kernel_threads(MODE, EW), 1)
         tc_fence_after();
         const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + bi * BN;
 
+#ifdef RL_AB_K1_NOEPI
+        // A/B measurement only: K1's epilogue releases the TMEM half without reading it
+        // (no partials are written): separates the MMA loop from the drain
+        if constexpr (MODE == EPI_LSE) {
+          release_tmem(bi);
+          continue;
+        }
+#endif
         if constexpr (MODE == EPI_LSE) {
           int64_t y = row_ok ? static_cast<int64_t>(ep.targets[row]) - ep.vocab_offset : -1;
           if (y >= ep.cols) y = -1;  // target lives in another vocab shard
@@ -755,6 +763,40 @@ __global__ void __launch_bounds__(kernel_threads(MODE, EW), 1)
             tmem_wait_ld();
             if (c == cbeg + CPW - 1) release_tmem(bi);
             if (c * 32 >= nvalid) continue;  // columns past V (ragged last tile)
+#ifdef RL_AB_K1_NOMATH
+            // A/B measurement only: read the accumulator, skip the softmax arithmetic
+            if (r[0] == 0x7fc00001u) srun += 1.f;
+            continue;
+#endif
+            if (tl >= c * 32 && tl < c * 32 + 32) {
+              const int jt = tl - c * 32;
+              float z = -INFINITY;
+  #pragma unroll
+              for (int j = 0; j < 32; ++j) z = fmaxf(z, (j == jt) ? __uint_as_float(r[j]) : -INFINITY);
+              zt = z * it;
+            }
+            if (c * 32 + 32 <= nvalid) {
+              // full chunk: max on the raw accumulator (sl2 > 0) and the scale folded into one
+              // FFMA per element; the drain is bound by the MUFU pipe (one ex2 per logit), not
+              // by TMEM reads (profiles/r02/k1_drain/)
+              float cr = __uint_as_float(r[0]);
+  #pragma unroll
+              for (int j = 1; j < 32; ++j) cr = fmaxf(cr, __uint_as_float(r[j]));
+              const float mn = fmaxf(mrun, cr * sl2);
+              const float sc = ex2f(mrun - mn);
+              trun = sc * fmaf(srun, mrun - mn, trun);
+              srun *= sc;
+              mrun = mn;
+  #pragma unroll
+              for (int j = 0; j < 32; ++j) {
+                const float d = fmaf(__uint_as_float(r[j]), sl2, -mn);
+                const float e = ex2f(d);
+                srun += e;
+                trun = fmaf(e, d, trun);
+              }
+              continue;
+            }
+            // the ragged last chunk of the vocabulary: columns past V are masked out
             float u[32];
   #pragma unroll
             for (int j = 0; j < 32; ++j) u[j] = __uint_as_float(r[j]) * sl2;
@@ -762,13 +804,6 @@ __global__ void __launch_bounds__(kernel_threads(MODE, EW), 1)
   #pragma unroll
               for (int j = 0; j < 32; ++j)
                 if (c * 32 + j >= nvalid) u[j] = -1e30f;
-            }
-            if (tl >= c * 32 && tl < c * 32 + 32) {
-              const int jt = tl - c * 32;
-              float z = -INFINITY;
-  #pragma unroll
-              for (int j = 0; j < 32; ++j) z = fmaxf(z, (j == jt) ? __uint_as_float(r[j]) : -INFINITY);
-              zt = z * it;
             }
             float cm = u[0];
   #pragma unroll
