@@ -282,7 +282,8 @@ __global__ void __launch_bounds__(kernel_threads(MODE, EW), 1)
   using TL = Tiling<CG>;
   static_assert(NB == 1 || (NB == 2 && CG == 2 && MODE != EPI_BF16_GROUPED), "wide tiles: CTA pairs, not grouped");
   static_assert(SKEW < STAGES, "the skewed head/tail holds SKEW stages");
-  static_assert(EW == 4 || ((EW == 8 || EW == 16) && MODE == EPI_LSE), "8 / 16 epilogue warps: LSE epilogue only");
+  static_assert(EW == 4 || ((EW == 8 || EW == 16) && MODE == EPI_LSE) || (EW == 8 && MODE == EPI_DZ),
+                "more epilogue warps: LSE (8 / 16) and dU (8) epilogues only");
   constexpr int TN = BN * NB;                 // tile columns
   constexpr int kStoreGroups = NB * (BN / 32);  // fp32 store epilogues: bulk groups per tile and warp
   constexpr int NACC = NB == 1 ? 2 : 1;       // TMEM accumulators (512 columns in total)
@@ -677,7 +678,11 @@ __global__ void __launch_bounds__(kernel_threads(MODE, EW), 1)
     const int q = warp & 3;  // TMEM lane quarter this warp may access
     const int cgrp = (warp - 2) / 4;  // EW = 8: which 128 of a TMEM half's 256 columns
     const int r_in_tile = rank * 128 + q * 32 + lane;
-    const uint32_t buf0 = smem_u32(sEpi + (warp - 2) * 2 * EPI_BUF_BYTES);
+    // store staging: two 4 KB buffers per warp with 4 epilogue warps, one with 8 (the same
+    // EPI_BYTES); EW > 4 store epilogues split each TMEM half's chunks between the warps
+    // of a lane quarter
+    constexpr int NBUF = EW == 4 ? 2 : 1;
+    const uint32_t buf0 = smem_u32(sEpi + (warp - 2) * NBUF * EPI_BUF_BYTES);
     const uint32_t tempty_leader0 = (CG == 2) ? mapa_shared(smem_u32(&tempty[0]), 0) : 0u;
     int acc = 0;
     uint32_t aph = 0;
@@ -895,14 +900,16 @@ __global__ void __launch_bounds__(kernel_threads(MODE, EW), 1)
             empty_k = kb1 <= kb0;
           }
   #pragma unroll 1
-          for (int c = 0; c < BN / COLS; ++c) {
+          constexpr int SCPW = (BN / COLS) / (EW / 4);  // store chunks per warp and TMEM half
+          const int sc0 = (MODE == EPI_LSE ? 0 : cgrp) * SCPW;
+          for (int c = sc0; c < sc0 + SCPW; ++c) {
             uint32_t w[32];
             if constexpr (COLS == 64) {
               uint32_t r0[32], r1[32];
               tmem_ld32(taddr + c * 64, r0);
               tmem_ld32(taddr + c * 64 + 32, r1);
               tmem_wait_ld();
-              if (c == BN / COLS - 1) release_tmem(bi);
+              if (c == sc0 + SCPW - 1) release_tmem(bi);
   #pragma unroll
               for (int j = 0; j < 16; ++j) {
                 float v0 = __uint_as_float(r0[2 * j]), v1 = __uint_as_float(r0[2 * j + 1]);
@@ -931,7 +938,7 @@ __global__ void __launch_bounds__(kernel_threads(MODE, EW), 1)
               uint32_t r0[32];
               tmem_ld32(taddr + c * 32, r0);
               tmem_wait_ld();
-              if (c == BN / COLS - 1) release_tmem(bi);
+              if (c == sc0 + SCPW - 1) release_tmem(bi);
   #pragma unroll
               for (int j = 0; j < 32; ++j) w[j] = empty_k ? 0u : r0[j];
             }
@@ -953,8 +960,8 @@ __global__ void __launch_bounds__(kernel_threads(MODE, EW), 1)
                 continue;
               }
             }
-            const uint32_t buf = buf0 + (chunk_ctr & 1) * EPI_BUF_BYTES;
-            if (lane == 0) bulk_wait_read<1>();
+            const uint32_t buf = buf0 + (chunk_ctr % NBUF) * EPI_BUF_BYTES;
+            if (lane == 0) bulk_wait_read<NBUF - 1>();
             __syncwarp();
             stage_row(buf, lane, w);
             fence_async_smem();
