@@ -282,8 +282,9 @@ __global__ void __launch_bounds__(kernel_threads(MODE, EW), 1)
   using TL = Tiling<CG>;
   static_assert(NB == 1 || (NB == 2 && CG == 2 && MODE != EPI_BF16_GROUPED), "wide tiles: CTA pairs, not grouped");
   static_assert(SKEW < STAGES, "the skewed head/tail holds SKEW stages");
-  static_assert(EW == 4 || ((EW == 8 || EW == 16) && MODE == EPI_LSE) || (EW == 8 && MODE == EPI_DZ),
-                "more epilogue warps: LSE (8 / 16) and dU (8) epilogues only");
+  static_assert(EW == 4 || ((EW == 8 || EW == 16) && MODE == EPI_LSE) ||
+                    (EW == 8 && (MODE == EPI_DZ || MODE == EPI_F32 || MODE == EPI_F32_ADD)),
+                "more epilogue warps: LSE (8 / 16), dU and fp32 store (8) epilogues only");
   constexpr int TN = BN * NB;                 // tile columns
   constexpr int kStoreGroups = NB * (BN / 32);  // fp32 store epilogues: bulk groups per tile and warp
   constexpr int NACC = NB == 1 ? 2 : 1;       // TMEM accumulators (512 columns in total)

@@ -162,14 +162,6 @@ int epi_warps_for(int kid) {
   if (kid < 0 || kid >= kKnobKids) return 4;
   return env[kid] == 4 ? 4 : (env[kid] == 16 ? 16 : 8);
 }
-// Epilogue warps of the dU GEMM (K4): RL_EPI_WARPS_DZ = 4 (default) or 8 (with RL_WIDE_DZ=1).
-int epi_warps_for_dz() {
-  static const int v = [] {
-    const char* e = getenv("RL_EPI_WARPS_DZ");
-    return (e && atoi(e) == 8) ? 8 : 4;
-  }();
-  return v;
-}
 int sync_slack_for(int kid) {
   static const std::array<int, kKnobKids> env = env_table("RL_SYNC_SLACK", -1);
   if (kid < 0 || kid >= kKnobKids) return 2;
@@ -292,12 +284,6 @@ rl_status launch_gemm(int kid, const CUtensorMap& a, const CUtensorMap& b, const
                       int64_t K, int group_m, const rl::EpiParams& ep, int sms, cudaStream_t st, int k_splits = 1,
                       int split_rows = 0, const int* dyn_count = nullptr, int dyn_mode = 0) {
   if (M <= 0 || N <= 0) return RL_OK;
-  if constexpr (MODE == rl::EPI_DZ) {
-    // 8 epilogue warps for K4 only with its wide tiles (RL_WIDE_DZ=1 RL_EPI_WARPS_DZ=8, A/B)
-    if (epi_warps_for_dz() == 8 && cta_group() == 2 && wide_for(kid) && N > rl::BN)
-      return launch_gemm_ew<MODE, A_MN, B_MN, 8>(kid, a, b, c, M, N, K, group_m, ep, sms, st, k_splits, split_rows,
-                                                 dyn_count, dyn_mode);
-  }
   if constexpr (MODE == rl::EPI_LSE) {
     if (epi_warps_for(kid) == 8)
       return launch_gemm_ew<MODE, A_MN, B_MN, 8>(kid, a, b, c, M, N, K, group_m, ep, sms, st, k_splits, split_rows,
