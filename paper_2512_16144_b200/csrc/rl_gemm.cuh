@@ -900,6 +900,40 @@ __global__ void __launch_bounds__(kernel_threads(MODE, EW), 1)
             tile_k_range(tile, sh, kb0, kb1);
             empty_k = kb1 <= kb0;
           }
+          if constexpr ((MODE == EPI_F32 || MODE == EPI_F32_ADD) && EW == 8) {
+            // 8 warps, fp32 stores: a warp loads its 4 chunks of the half at once and releases
+            // the TMEM half before storing any, so the next tile's MMAs never wait on stores
+            constexpr int K8 = (BN / 32) / 2;
+            const int sc0e = cgrp * K8;
+            uint32_t pre[K8][32];
+  #pragma unroll
+            for (int k = 0; k < K8; ++k) tmem_ld32(taddr + (sc0e + k) * 32, pre[k]);
+            tmem_wait_ld();
+            release_tmem(bi);
+  #pragma unroll
+            for (int k = 0; k < K8; ++k) {
+              if (empty_k) {
+  #pragma unroll
+                for (int j = 0; j < 32; ++j) pre[k][j] = 0u;
+              }
+              if (lane == 0) bulk_wait_read<0>();
+              __syncwarp();
+              stage_row(buf0, lane, pre[k]);
+              fence_async_smem();
+              __syncwarp();
+              if (lane == 0) {
+                const int c0 = n0 + (sc0e + k) * 32;
+                const int c1 = m * TL::TILE_M + rank * 128 + q * 32 + (tile / (sh.m_blocks * sh.n_blocks)) * sh.split_rows;
+                if (MODE == EPI_F32_ADD)
+                  tma_reduce_add_2d(&tmC, sEpi + (buf0 - smem_u32(sEpi)), c0, c1);
+                else
+                  tma_store_2d(&tmC, sEpi + (buf0 - smem_u32(sEpi)), c0, c1);
+                bulk_commit();
+              }
+              ++chunk_ctr;
+            }
+            continue;
+          }
   #pragma unroll 1
           constexpr int SCPW = (BN / COLS) / (EW / 4);  // store chunks per warp and TMEM half
           const int sc0 = (MODE == EPI_LSE ? 0 : cgrp) * SCPW;

@@ -162,6 +162,16 @@ int epi_warps_for(int kid) {
   if (kid < 0 || kid >= kKnobKids) return 4;
   return env[kid] == 4 ? 4 : (env[kid] == 16 ? 16 : 8);
 }
+// Epilogue warps of K6 (dW, fp32 store / reduce-add): RL_EPI_WARPS_DW = 8 (default: each warp
+// loads its 4 chunks of a TMEM half at once and releases it before storing; K6 17.61 -> 17.42 M
+// cycles, profiles/r02/k6_w8_early/) or 4. The NVLS-fused dW GEMM keeps 4.
+int epi_warps_dw() {
+  static const int v = [] {
+    const char* e = getenv("RL_EPI_WARPS_DW");
+    return (e && atoi(e) == 4) ? 4 : 8;
+  }();
+  return v;
+}
 int sync_slack_for(int kid) {
   static const std::array<int, kKnobKids> env = env_table("RL_SYNC_SLACK", -1);
   if (kid < 0 || kid >= kKnobKids) return 2;
@@ -284,6 +294,12 @@ rl_status launch_gemm(int kid, const CUtensorMap& a, const CUtensorMap& b, const
                       int64_t K, int group_m, const rl::EpiParams& ep, int sms, cudaStream_t st, int k_splits = 1,
                       int split_rows = 0, const int* dyn_count = nullptr, int dyn_mode = 0) {
   if (M <= 0 || N <= 0) return RL_OK;
+  if constexpr (MODE == rl::EPI_F32 || MODE == rl::EPI_F32_ADD) {
+    // the wide dW GEMM (K6) with 8 epilogue warps that release each TMEM half before storing
+    if (kid == RL_K_DW_GEMM && epi_warps_dw() == 8 && cta_group() == 2 && wide_for(kid) && N > rl::BN)
+      return launch_gemm_ew<MODE, A_MN, B_MN, 8>(kid, a, b, c, M, N, K, group_m, ep, sms, st, k_splits, split_rows,
+                                                 dyn_count, dyn_mode);
+  }
   if constexpr (MODE == rl::EPI_LSE) {
     if (epi_warps_for(kid) == 8)
       return launch_gemm_ew<MODE, A_MN, B_MN, 8>(kid, a, b, c, M, N, K, group_m, ep, sms, st, k_splits, split_rows,
