@@ -762,17 +762,13 @@ __global__ void __launch_bounds__(kernel_threads(MODE, EW), 1)
           const float sl2 = ep.invt_rows != nullptr ? it * 1.4426950408889634f : ep.scale_log2;
           constexpr int CPW = (BN / 32) / (EW / 4);  // 32-column chunks per warp
           const int cbeg = cgrp * CPW;
-  #pragma unroll 1
-          for (int c = cbeg; c < cbeg + CPW; ++c) {
-            uint32_t r[32];
-            tmem_ld32(taddr + c * 32, r);
-            tmem_wait_ld();
-            if (c == cbeg + CPW - 1) release_tmem(bi);
-            if (c * 32 >= nvalid) continue;  // columns past V (ragged last tile)
+          // one 32-column chunk of scaled logits into the online (m, s, u) state and z_target
+          auto lse_chunk = [&](int c, const uint32_t (&r)[32]) {
+            if (c * 32 >= nvalid) return;  // columns past V (ragged last tile)
 #ifdef RL_AB_K1_NOMATH
             // A/B measurement only: read the accumulator, skip the softmax arithmetic
             if (r[0] == 0x7fc00001u) srun += 1.f;
-            continue;
+            return;
 #endif
             if (tl >= c * 32 && tl < c * 32 + 32) {
               const int jt = tl - c * 32;
@@ -783,8 +779,7 @@ __global__ void __launch_bounds__(kernel_threads(MODE, EW), 1)
             }
             if (c * 32 + 32 <= nvalid) {
               // full chunk: max on the raw accumulator (sl2 > 0) and the scale folded into one
-              // FFMA per element; the drain is bound by the MUFU pipe (one ex2 per logit), not
-              // by TMEM reads (profiles/r02/k1_drain/)
+              // FFMA per element (one ex2 per logit on the MUFU pipe, profiles/r02/k1_drain/)
               float cr = __uint_as_float(r[0]);
   #pragma unroll
               for (int j = 1; j < 32; ++j) cr = fmaxf(cr, __uint_as_float(r[j]));
@@ -800,17 +795,12 @@ __global__ void __launch_bounds__(kernel_threads(MODE, EW), 1)
                 srun += e;
                 trun = fmaf(e, d, trun);
               }
-              continue;
+              return;
             }
             // the ragged last chunk of the vocabulary: columns past V are masked out
             float u[32];
   #pragma unroll
-            for (int j = 0; j < 32; ++j) u[j] = __uint_as_float(r[j]) * sl2;
-            if (nvalid < BN) {
-  #pragma unroll
-              for (int j = 0; j < 32; ++j)
-                if (c * 32 + j >= nvalid) u[j] = -1e30f;
-            }
+            for (int j = 0; j < 32; ++j) u[j] = (c * 32 + j < nvalid) ? __uint_as_float(r[j]) * sl2 : -1e30f;
             float cm = u[0];
   #pragma unroll
             for (int j = 1; j < 32; ++j) cm = fmaxf(cm, u[j]);
@@ -825,6 +815,27 @@ __global__ void __launch_bounds__(kernel_threads(MODE, EW), 1)
               const float e = ex2f(d);
               srun += e;
               trun = fmaf(e, d, trun);
+            }
+          };
+          if constexpr (EW >= 8) {
+            // every chunk of this warp's share of the half in registers at once, then the TMEM
+            // half goes back to the MMA: the softmax arithmetic (the drain's bottleneck) runs
+            // under the next MMAs instead of in front of them
+            uint32_t pre[CPW][32];
+  #pragma unroll
+            for (int k = 0; k < CPW; ++k) tmem_ld32(taddr + (cbeg + k) * 32, pre[k]);
+            tmem_wait_ld();
+            release_tmem(bi);
+  #pragma unroll
+            for (int k = 0; k < CPW; ++k) lse_chunk(cbeg + k, pre[k]);
+          } else {
+  #pragma unroll 1
+            for (int c = cbeg; c < cbeg + CPW; ++c) {
+              uint32_t r[32];
+              tmem_ld32(taddr + c * 32, r);
+              tmem_wait_ld();
+              if (c == cbeg + CPW - 1) release_tmem(bi);
+              lse_chunk(c, r);
             }
           }
           if constexpr (EW > 4) {
