@@ -727,6 +727,9 @@ __global__ void __launch_bounds__(kernel_threads(MODE, EW), 1)
         row = static_cast<int64_t>(m) * TL::TILE_M + r_in_tile;
         row_ok = row < ep.rows;
       }
+      // K1, 8 epilogue warps, wide tiles: one register set carries half 1 from the h = 0 pass
+      // into the h = 1 pass (see the EPI_LSE branch)
+      [[maybe_unused]] uint32_t lse_pre[(MODE == EPI_LSE && EW == 8 && NB == 2) ? 4 : 1][32];
 #pragma unroll 1
       for (int h = 0; h < NB; ++h) {
         const int bi = NB == 2 ? h : acc;  // TMEM half (wide tiles) or accumulator
@@ -817,7 +820,34 @@ __global__ void __launch_bounds__(kernel_threads(MODE, EW), 1)
               trun = fmaf(e, d, trun);
             }
           };
-          if constexpr (EW >= 8) {
+          if constexpr (EW >= 8 && NB == 2 && CPW == 4) {
+            // both TMEM halves of a wide tile through one 4-chunk register set: half 0 is loaded
+            // and released at once; its arithmetic is split around the loads of half 1 (issued
+            // into the slots already consumed), so half 1 goes back to the MMA after two
+            // chunks of math instead of four (profiles/r02/k1_early_release/)
+            if (h == 0) {
+  #pragma unroll
+              for (int k = 0; k < 4; ++k) tmem_ld32(taddr + (cbeg + k) * 32, lse_pre[k]);
+              tmem_wait_ld();
+              release_tmem(0);
+              lse_chunk(cbeg + 0, lse_pre[0]);
+              lse_chunk(cbeg + 1, lse_pre[1]);
+              mbar_wait_sleep(&tfull[1], aph);
+              tc_fence_after();
+              const uint32_t taddr1 = taddr + BN;
+              tmem_ld32(taddr1 + (cbeg + 0) * 32, lse_pre[0]);
+              tmem_ld32(taddr1 + (cbeg + 1) * 32, lse_pre[1]);
+              lse_chunk(cbeg + 2, lse_pre[2]);
+              lse_chunk(cbeg + 3, lse_pre[3]);
+              tmem_ld32(taddr1 + (cbeg + 2) * 32, lse_pre[2]);
+              tmem_ld32(taddr1 + (cbeg + 3) * 32, lse_pre[3]);
+              tmem_wait_ld();
+              release_tmem(1);
+            } else {
+  #pragma unroll
+              for (int k = 0; k < 4; ++k) lse_chunk(cbeg + k, lse_pre[k]);   // half 1, already loaded
+            }
+          } else if constexpr (EW >= 8) {
             // every chunk of this warp's share of the half in registers at once, then the TMEM
             // half goes back to the MMA: the softmax arithmetic (the drain's bottleneck) runs
             // under the next MMAs instead of in front of them
