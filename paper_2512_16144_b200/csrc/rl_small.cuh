@@ -700,4 +700,35 @@ __global__ void expert_load_kernel(const int32_t* __restrict__ offsets, int n_gr
   }
 }
 
+
+// Split-K dH (few output tiles): out[r, :] = sum_s part[s * rows_pad + r, :] in split order
+// (deterministic), for r < rows (or the device row count); bf16 (RN) or fp32 output.
+template <typename OutT>
+__global__ void split_sum_kernel(const float* __restrict__ part, int S, int64_t rows_pad, int64_t H, int64_t rows,
+                                 const int* __restrict__ cnt, OutT* __restrict__ out) {
+  int64_t n = rows;
+  if (cnt) {
+    const int64_t c = *cnt;
+    n = c < rows ? (c > 0 ? c : 0) : rows;
+  }
+  const int64_t n4 = n * H / 4, stride4 = rows_pad * H / 4;
+  const float4* p = reinterpret_cast<const float4*>(part);
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n4;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    float4 a = p[i];
+    for (int k = 1; k < S; ++k) {
+      const float4 b = p[k * stride4 + i];
+      a.x += b.x;
+      a.y += b.y;
+      a.z += b.z;
+      a.w += b.w;
+    }
+    if constexpr (sizeof(OutT) == 2) {
+      reinterpret_cast<uint2*>(out)[i] = make_uint2(pack_bf16x2(a.x, a.y), pack_bf16x2(a.z, a.w));
+    } else {
+      reinterpret_cast<float4*>(out)[i] = a;
+    }
+  }
+}
+
 }  // namespace rl

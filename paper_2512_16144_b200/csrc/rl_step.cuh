@@ -142,6 +142,48 @@ rl_status launch_dw_nvls(const CUtensorMap& t_dz_mn, const CUtensorMap& t_h_mn, 
                                                     dyn_count, dyn_count ? 2 : 0);
 }
 
+// K5 (dH = dU W) for `rows` rows into `out` (bf16 or fp32, row-major [rows, H]); `cnt` (device,
+// optional) is the actual row count of a compacted chunk. With fewer output tiles than CTA pairs
+// (L.dh_splits > 1) the vocabulary is split: fp32 partials per split, then a fixed-order sum.
+rl_status launch_dh(const CUtensorMap& t_dz_k, const CUtensorMap& t_w_mn, int64_t rows, int64_t H, int64_t V,
+                    void* out, bool bf16_out, const int* cnt, uint8_t* ws, const WsLayout& L, int sms, cudaStream_t st) {
+  rl::EpiParams e5 = {};
+  e5.rows = rows;
+  e5.cols = H;
+  const int dyn = cnt ? 1 : 0;
+  const int S = L.dh_splits;
+  if (S <= 1 || dh_split_factor(rows, H, V) <= 1) {
+    CUtensorMap t_dh;
+    if (bf16_out) {
+      RL_TRY(make_map(&t_dh, out, false, H, rows, H, 64, 32));
+      return launch_gemm<rl::EPI_BF16, false, true>(RL_K_DH_GEMM, t_dz_k, t_w_mn, t_dh, rows, H, V,
+                                                    group_m_for(RL_K_DH_GEMM, kGroupMBwd), e5, sms, st, 1, 0, cnt, dyn);
+    }
+    RL_TRY(make_map(&t_dh, out, true, H, rows, H, 32, 32));
+    return launch_gemm<rl::EPI_F32, false, true>(RL_K_DH_GEMM, t_dz_k, t_w_mn, t_dh, rows, H, V,
+                                                 group_m_for(RL_K_DH_GEMM, kGroupMBwd), e5, sms, st, 1, 0, cnt, dyn);
+  }
+  const int64_t rows_pad = (rows + 255) / 256 * 256;
+  float* part = reinterpret_cast<float*>(ws + L.dh_split);
+  CUtensorMap t_part;
+  RL_TRY(make_map(&t_part, part, true, H, S * rows_pad, H, 32, 32));
+  RL_TRY((launch_gemm<rl::EPI_F32, false, true>(RL_K_DH_GEMM, t_dz_k, t_w_mn, t_part, rows, H, V,
+                                                group_m_for(RL_K_DH_GEMM, kGroupMBwd), e5, sms, st, S,
+                                                static_cast<int>(rows_pad), cnt, dyn)));
+  {
+    ProfScope ps(RL_K_COMPACT, st);
+    const int64_t n4 = rows * H / 4;
+    const unsigned blocks = static_cast<unsigned>(std::min<int64_t>((n4 + 255) / 256, int64_t(sms) * 8));
+    if (bf16_out)
+      rl::split_sum_kernel<uint16_t><<<blocks, 256, 0, st>>>(part, S, rows_pad, H, rows, cnt,
+                                                             static_cast<uint16_t*>(out));
+    else
+      rl::split_sum_kernel<float><<<blocks, 256, 0, st>>>(part, S, rows_pad, H, rows, cnt, static_cast<float*>(out));
+  }
+  RL_CHECK_LAUNCH();
+  return RL_OK;
+}
+
 // Sparse backward: the same K4 -> K6 -> K5 over the rows whose coefficient is
 // non-zero only (their order kept). Row counts live on the device: the GEMMs read
 // them at start (dyn_mode), so nothing synchronises the host.
@@ -245,15 +287,7 @@ rl_status bwd_sparse_impl(const rl_lm_shape* s, const uint16_t* hidden, const ui
                                                              cnt, 1)));
         continue;
       }
-      if (dh) {
-        RL_TRY(make_map(&t_dh, dh_c, false, H, rows, H, 64, 32));
-        RL_TRY((launch_gemm<rl::EPI_BF16, false, true>(RL_K_DH_GEMM, t_dz_k, t_w_mn, t_dh, rows, H, V,
-                                                       group_m_for(RL_K_DH_GEMM, kGroupMBwd), e5, sms, st, 1, 0, cnt, 1)));
-      } else {
-        RL_TRY(make_map(&t_dh, dh_c, true, H, rows, H, 32, 32));
-        RL_TRY((launch_gemm<rl::EPI_F32, false, true>(RL_K_DH_GEMM, t_dz_k, t_w_mn, t_dh, rows, H, V,
-                                                      group_m_for(RL_K_DH_GEMM, kGroupMBwd), e5, sms, st, 1, 0, cnt, 1)));
-      }
+      RL_TRY(launch_dh(t_dz_k, t_w_mn, rows, H, V, dh_c, dh != nullptr, cnt, ws, L, sms, st));
       {
         ProfScope ps(RL_K_COMPACT, st);
         rl::scatter_rows_kernel<<<8 * sms, 256, 0, st>>>(dh_c, H * (dh ? 2 : 4), idx + c0, cnt,
@@ -336,16 +370,14 @@ rl_status bwd_impl(const rl_lm_shape* s, const uint16_t* hidden, const uint16_t*
       e5.rows = rows;
       e5.cols = H;
       if (dh) {
-        RL_TRY(make_map(&t_dh, dh + c0 * H, false, H, rows, H, 64, 32));
-        RL_TRY((launch_gemm<rl::EPI_BF16, false, true>(RL_K_DH_GEMM, t_dz_k, t_w_mn, t_dh, rows, H, V, group_m_for(RL_K_DH_GEMM, kGroupMBwd), e5, sms, st)));
-      } else {
+        RL_TRY(launch_dh(t_dz_k, t_w_mn, rows, H, V, dh + c0 * H, true, nullptr, ws, L, sms, st));
+      } else if (dh_nvls) {
         RL_TRY(make_map(&t_dh, dh32 + c0 * H, true, H, rows, H, 32, 32));
-        if (dh_nvls) {
-          set_nvls(e5, dh_nvls, dh32 + c0 * H, c0 * H, static_cast<int>(ch));
-          RL_TRY((launch_gemm<rl::EPI_F32_NVLS, false, true>(RL_K_DH_GEMM, t_dz_k, t_w_mn, t_dh, rows, H, V,
-                                                               group_m_for(RL_K_DH_GEMM, kGroupMBwd), e5, sms, st)));
-        } else
-        RL_TRY((launch_gemm<rl::EPI_F32, false, true>(RL_K_DH_GEMM, t_dz_k, t_w_mn, t_dh, rows, H, V, group_m_for(RL_K_DH_GEMM, kGroupMBwd), e5, sms, st)));
+        set_nvls(e5, dh_nvls, dh32 + c0 * H, c0 * H, static_cast<int>(ch));
+        RL_TRY((launch_gemm<rl::EPI_F32_NVLS, false, true>(RL_K_DH_GEMM, t_dz_k, t_w_mn, t_dh, rows, H, V,
+                                                             group_m_for(RL_K_DH_GEMM, kGroupMBwd), e5, sms, st)));
+      } else {
+        RL_TRY(launch_dh(t_dz_k, t_w_mn, rows, H, V, dh32 + c0 * H, false, nullptr, ws, L, sms, st));
       }
     }
   }

@@ -22,8 +22,34 @@ struct WsLayout {
   // sparse backward (rows with coef != 0): compact index, per-row vectors, counts,
   // gathered hidden rows and one chunk of compact dH
   size_t idx, coef_c, lse_c, tgt_c, invt_c, blk_counts, chunk_counts, h_c, dh_c;
+  // split-K dH for chunks with fewer 256 x 512 output tiles than CTA pairs: fp32 partials
+  size_t dh_split;
+  int dh_splits;
   int64_t n_tiles_v, ldz, chunk;
 };
+
+// K5 (dH = dU W, K = V) has only ceil(rows/256) x ceil(H/512) output tiles: with fewer than
+// a B200's 74 CTA pairs the GEMM leaves pairs idle for a whole (long) tile. Split the
+// vocabulary S ways (fp32 partials, summed in a fixed order) with the S in 2..8 that
+// minimises the waves per unit of work, when that saves at least a quarter (the partials
+// cost an extra S x rows x H x 8 bytes: at 2048 rows x 4096 an 8-way split measured slower,
+// profiles/r02/dh_split/); 1 otherwise.
+int dh_split_factor(int64_t rows, int64_t H, int64_t V) {
+  constexpr int kPairs = 74;
+  const int64_t tiles = ((rows + 255) / 256) * ((H + 511) / 512);
+  if (rows <= 0 || tiles >= kPairs) return 1;
+  int best_s = 1;
+  double best = 1.0;
+  for (int sp = 2; sp <= 8; ++sp) {
+    if (V < int64_t(sp) * 64 * 16) break;  // keep >= 16 k-blocks per split
+    const double t = static_cast<double>((tiles * sp + kPairs - 1) / kPairs) / sp;
+    if (t < best - 1e-9) {
+      best = t;
+      best_s = sp;
+    }
+  }
+  return best <= 0.75 ? best_s : 1;
+}
 
 int64_t n_vocab_tiles(const rl_lm_shape* s) { return (s->V_local + rl::BN - 1) / rl::BN; }
 
@@ -50,6 +76,9 @@ WsLayout ws_layout(const rl_lm_shape* s, int32_t R, int64_t chunk_rows) {
   w.chunk_counts = c.take(static_cast<size_t>((T + (w.chunk > 0 ? w.chunk : 1) - 1) / (w.chunk > 0 ? w.chunk : 1) + 2) * 4);
   w.h_c = c.take(static_cast<size_t>(Tp) * s->H * 2);
   w.dh_c = c.take(static_cast<size_t>((w.chunk + 255) / 256 * 256) * s->H * 4);
+  w.dh_splits = dh_split_factor(w.chunk, s->H, s->V_local);
+  w.dh_split = c.take(w.dh_splits > 1 ? static_cast<size_t>(w.dh_splits) * ((w.chunk + 255) / 256 * 256) * s->H * 4
+                                      : 0);
   w.end = align_up(c.off, 1024);
   return w;
 }
