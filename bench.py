@@ -311,6 +311,8 @@ def _setup(args):
     # dU in 16k-row chunks: keeps K5/K6's per-wave working set inside L2 (the K = T
     # reduction of K6 at 64k rows loses ~20% to HBM re-reads otherwise)
     r.chunk = 0 if r.T <= 16384 else 16384
+    if args.dz_chunk >= 0:
+        r.chunk = args.dz_chunk
     return r
 
 
@@ -705,6 +707,8 @@ def main():
     ap.add_argument("--comm-sms", type=int, default=24, help="DP overlap: SMs left to NCCL while K5 runs")
     ap.add_argument("--tokens", type=int, default=0,
                     help="override the workload's tokens per rank (A/B: micro-batch size sweep)")
+    ap.add_argument("--dz-chunk", type=int, default=-1,
+                    help="rows of the bf16 dU buffer per backward pass (A/B; -1 = auto: T up to 16k rows, else 16k)")
     ap.add_argument("--delta-sigma", type=float, default=None,
                     help="override the workload's log-prob mismatch sigma (A/B: 1.0 = the stress config's)")
     ap.add_argument("--targets", default="sampled", choices=["sampled", "uniform"],
