@@ -20,9 +20,12 @@
 // CTA), warps 2 .. 2+EW-1 = epilogue (thread = accumulator row; EW = 8 for K1:
 // two warps per TMEM lane quarter), and for EPI_F32_NVLS 4 more communication
 // warps that run the cross-rank slab reductions (comm_warps()).
-// Order of k-blocks: ascending, or serpentine (odd tiles of a CTA backwards,
-// EpiParams::k_serpentine) for K6 / Newton-Schulz. A soft k-barrier between the
-// producers keeps the CTAs sharing operands inside one L2 window (sync_*).
+// Order of k-blocks: ascending, or serpentine (tiles of odd waves backwards,
+// EpiParams::k_serpentine) for K6 / Newton-Schulz. Tile order: static round robin
+// (tile = pair + i * pairs) with a soft k-barrier between the producers that keeps the
+// CTAs sharing operands inside one L2 window (sync_*), or dynamic (dyn_tiles): each
+// pair's leader producer takes the next tile of the raster from a global counter and
+// passes it to every role of both CTAs through a shared-memory ring (next_tile).
 //
 // Epilogues:
 //   EPI_LSE  (K1): per row of the tile, online (m, s, u, z_target) over the
@@ -163,6 +166,8 @@ struct EpiParams {
   // row row_map[r] of nvls_local / nvls_mc (rows >= the device row count are skipped);
   // the store is a plain per-row global store instead of TMA
   const int32_t* row_map;
+  int* tile_ctr;
+  int dyn_tiles;
 };
 
 __device__ __forceinline__ void red_release_add(uint32_t* p, uint32_t v) {
@@ -318,6 +323,13 @@ __global__ void __launch_bounds__(kernel_threads(MODE, EW), 1)
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  // dynamic tile ring (EpiParams::dyn_tiles): TR slots after the TMEM slot
+  constexpr bool kDynOk = MODE == EPI_LSE || MODE == EPI_DZ || MODE == EPI_BF16 || MODE == EPI_F32 || MODE == EPI_F32_ADD;
+  constexpr int TR = 4;
+  static_assert(2 * STAGES + 4 <= 16 && (17 + 2 * TR) * 8 + TR * 4 <= BAR_BYTES, "barrier area");
+  uint64_t* rfull = full + 17;
+  uint64_t* rempty = rfull + TR;
+  int* rslot = reinterpret_cast<int*>(rempty + TR);
   constexpr bool GROUPED = MODE == EPI_BF16_GROUPED;
   int* s_prefix = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(full) + BAR_BYTES);  // GROUPED only
 
@@ -339,6 +351,12 @@ __global__ void __launch_bounds__(kernel_threads(MODE, EW), 1)
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], EW * CG);
+    }
+    if constexpr (kDynOk) {
+      for (int r = 0; r < TR; ++r) {
+        mbar_init(&rfull[r], 1);
+        mbar_init(&rempty[r], CG == 2 ? 2 + 2 * EW : 1 + EW);
+      }
     }
     fence_mbar_init();
     tma_prefetch(&tmA);
@@ -390,6 +408,48 @@ __global__ void __launch_bounds__(kernel_threads(MODE, EW), 1)
     n = local % sh.n_blocks;
   };
 
+  // Tile ti of this CTA's sequence (-1: none left; prev = tile ti - 1), called by whole warps
+  // in order. Static: unit + ti * n_units. Dynamic: the pair leader's producer takes tiles from the global
+  // counter and writes each into slot ti % TR of both CTAs' rings; every other role reads
+  // its slot and releases it on the leader's ring barrier. Either way a tile's k-blocks run
+  // on one pair in a fixed order, so the results do not depend on the schedule.
+  const bool dyn = kDynOk && ep.dyn_tiles != 0;
+  int* const tile_ctr = ep.tile_ctr;
+  // (captures by value: a by-reference capture costs K1 stack space)
+  auto next_tile = [=](int ti, int prev) -> int {
+    if (!kDynOk || !dyn) {
+      const int t = prev + n_units;
+      return t < total ? t : -1;
+    }
+    const int r = ti & (TR - 1);
+    const uint32_t par = static_cast<uint32_t>(ti / TR) & 1u;
+    if (warp == 0 && leader) {
+      mbar_wait_cluster(&rempty[r], par ^ 1u);
+      int t = 0;
+      if (lane == 0) {
+        t = atomicAdd(tile_ctr, 1);
+        if (t >= total) t = -1;
+        rslot[r] = t;
+        if constexpr (CG == 2) {
+          st_shared_cluster_s32(mapa_shared(smem_u32(&rslot[r]), 1), t);
+          mbar_arrive_cluster(mapa_shared(smem_u32(&rfull[r]), 1));
+        }
+        mbar_arrive(&rfull[r]);
+      }
+      return __shfl_sync(0xffffffffu, t, 0);
+    }
+    mbar_wait_cluster(&rfull[r], par);
+    const int t = *reinterpret_cast<volatile int*>(&rslot[r]);
+    __syncwarp();
+    if (lane == 0) {
+      if constexpr (CG == 2)
+        mbar_arrive_cluster(mapa_shared(smem_u32(&rempty[r]), 0));
+      else
+        mbar_arrive(&rempty[r]);
+    }
+    return t;
+  };
+
   if (warp == 0) {
     // ------------------------------------------------------------- producer
     // The whole warp walks the schedule (warp-uniform state lives in uniform
@@ -398,7 +458,7 @@ __global__ void __launch_bounds__(kernel_threads(MODE, EW), 1)
     uint32_t ph = 0;
     int gk = 0;            // k-blocks issued by this CTA so far (all tiles)
     int last_sync = 0;
-    for (int tile = unit; tile < total; tile += n_units) {
+    for (int ti = 0, tile = next_tile(0, unit - n_units); tile >= 0; ++ti, tile = next_tile(ti, tile)) {
       int m, n, a_row, b_row;
       if constexpr (GROUPED) {
         int g, row0, row_end;
@@ -414,7 +474,7 @@ __global__ void __launch_bounds__(kernel_threads(MODE, EW), 1)
       int kb0 = 0, kb1 = sh.k_blocks;
       if constexpr (!GROUPED) tile_k_range(tile, sh, kb0, kb1);
       // serpentine: the MMA accumulates in issue order, so only the loads are reordered
-      const bool k_rev = ep.k_serpentine && (((tile - unit) / n_units) & 1);
+      const bool k_rev = ep.k_serpentine && ((tile / n_units) & 1);
       for (int kb_i = kb0; kb_i < kb1; ++kb_i, ++gk) {
         const int kb = k_rev ? kb0 + kb1 - 1 - kb_i : kb_i;
         if (ep.sync_every > 0 && gk > 0 && gk % ep.sync_every == 0) {
@@ -519,7 +579,7 @@ __global__ void __launch_bounds__(kernel_threads(MODE, EW), 1)
         uint32_t aph = 0;
         int g0 = 0;  // k-blocks consumed before this tile (stage = g % STAGES)
         const uint32_t a_base = smem_u32(sA), b_base = smem_u32(sB);
-        for (int tile = unit; tile < total; tile += n_units) {
+        for (int ti = 0, tile = next_tile(0, unit - n_units); tile >= 0; ++ti, tile = next_tile(ti, tile)) {
           int kb0 = 0, kb1 = sh.k_blocks;
           tile_k_range(tile, sh, kb0, kb1);
           const int L = kb1 > kb0 ? kb1 - kb0 : 0;
@@ -598,7 +658,7 @@ __global__ void __launch_bounds__(kernel_threads(MODE, EW), 1)
       uint32_t aph = 0;
       const uint32_t a_base = smem_u32(sA), b_base = smem_u32(sB);
       RL_AB_CLK(t_mma0);
-      for (int tile = unit; tile < total; tile += n_units) {
+      for (int ti = 0, tile = next_tile(0, unit - n_units); tile >= 0; ++ti, tile = next_tile(ti, tile)) {
         {
           RL_AB_CLK(tw);
           mbar_wait(&tempty[acc], aph ^ 1);
@@ -709,7 +769,7 @@ __global__ void __launch_bounds__(kernel_threads(MODE, EW), 1)
           mbar_arrive(&tempty[a]);
       }
     };
-    for (int tile = unit; tile < total; tile += n_units) {
+    for (int ti = 0, tile = next_tile(0, unit - n_units); tile >= 0; ++ti, tile = next_tile(ti, tile)) {
       int m = 0, n;
       int64_t row;
       bool row_ok;

@@ -147,6 +147,21 @@ bool serpentine_for(int kid) {
   if (env[kid] >= 0) return env[kid] != 0;
   return kid == RL_K_DW_GEMM || kid == RL_K_NS_GEMM;
 }
+// Dynamic tile order (EpiParams::dyn_tiles): RL_DYN_TILES[_<K>] = 0/1. Tiles are handed out
+// in raster order from a global counter instead of the static round robin, so the tiles in
+// flight stay a contiguous stretch of the raster without the soft k-barrier (which it
+// replaces for that GEMM). Default on for K1 (FWD) and K4 (DZ): K = H is short, so a raster
+// group's operands stay in L2 wherever each pair is inside its tile; K4 88.6 -> 93.8%
+// tensor-active with DRAM reads 7.0 -> 5.4 GB, K1 reads 7.4 -> 5.3 GB, step -0.7 ms
+// (profiles/r02/dyn/, dyn2/). Off for K5 / K6, whose long K needs the k-lockstep of the
+// barrier (dynamic: DRAM reads 14.7 -> 22.8 / 13.3 -> 18.2 GB). Not for the NVLS-fused or
+// grouped GEMMs.
+bool dyn_tiles_for(int kid) {
+  static const std::array<int, kKnobKids> env = env_table("RL_DYN_TILES", -1);
+  if (kid < 0 || kid >= kKnobKids) return false;
+  if (env[kid] >= 0) return env[kid] > 0;
+  return kid == RL_K_FWD_GEMM || kid == RL_K_DZ_GEMM;
+}
 int skew() {
   static const int v = [] {
     const char* e = getenv("RL_SKEW");
@@ -232,7 +247,15 @@ rl_status launch_gemm_cg(int kid, const CUtensorMap& a, const CUtensorMap& b, co
   rl::EpiParams ep2 = ep;
   ep2.k_serpentine = serpentine_for(kid) ? 1 : 0;
   ep2.sync_every = 0;
-  if (g_sync_ctr && sync_every_for(kid) > 0) {
+  ep2.dyn_tiles = 0;
+  ep2.tile_ctr = nullptr;
+  if (g_sync_ctr && dyn_tiles_for(kid) &&
+      (MODE == rl::EPI_LSE || MODE == rl::EPI_DZ || MODE == rl::EPI_BF16 || MODE == rl::EPI_F32 ||
+       MODE == rl::EPI_F32_ADD)) {
+    RL_CUDA(cudaMemsetAsync(g_sync_ctr, 0, 4, st));
+    ep2.dyn_tiles = 1;
+    ep2.tile_ctr = reinterpret_cast<int*>(g_sync_ctr);
+  } else if (g_sync_ctr && sync_every_for(kid) > 0) {
     const int64_t max_tiles = (tiles + units - 1) / units;
     const int se = sync_every_for(kid);
     const int64_t max_sync = (max_tiles * sh.k_blocks - 1) / se;
