@@ -661,13 +661,22 @@ def main_ours(args):
     e2e = None
     if not args.no_e2e:
         e2e = _e2e_vocab(r, args) if r.vocab_par else _e2e_dp(r, args)
+    clocks = r.clk.summary()
+    if roof and clocks.get("sm_mhz"):
+        import torch
+        # the tcgen05 bound at the clock the step actually ran (median nvidia-smi sample of the
+        # timed region): 8192 dense bf16 FLOP per SM clock (the ideal-cycle count of DESIGN.md §5)
+        sms = torch.cuda.get_device_properties(r.dev).multi_processor_count
+        ideal = sms * 8192.0 * float(clocks["sm_mhz"]) * 1e6 / 1e12
+        roof["tensor_ideal_at_sm_clock"] = ideal
+        roof["frac_vs_ideal_at_sm_clock"] = roof["achieved"] / ideal
     if r.rank == 0:
         out = {"metric": METRIC, "value": r.value, "unit": "tokens/s", "n_gpus": r.world, "steps": args.steps,
                "warmup": args.warmup, "ms_per_step": r.ms_max, "higher_is_better": True,
                "scaling": "strong" if r.vocab_par else "weak", "vs_baseline": None, "dtype": "bf16",
                "data": "synthetic (seeded; GLM-4.5-Air-shaped rollouts, random-init W)", "config": _config(r, args),
                "roofline": roof, "e2e": e2e, "gpu_launches": r.launches * args.steps,
-               "clocks": r.clk.summary(), "kernels": kern, "impl": "ours",
+               "clocks": clocks, "kernels": kern, "impl": "ours",
                # the paper prints no number for this path; its whole-system
                # H200 figures, with their hardware, as context only (not a target)
                "context": {"paper_h200": "RL step ~1500 s on 60 nodes x 8 H200 (16 trainer nodes = 128 GPUs), "
