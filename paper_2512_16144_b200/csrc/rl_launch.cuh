@@ -153,14 +153,15 @@ bool serpentine_for(int kid) {
 // replaces for that GEMM). Default on for K1 (FWD) and K4 (DZ): K = H is short, so a raster
 // group's operands stay in L2 wherever each pair is inside its tile; K4 88.6 -> 93.8%
 // tensor-active with DRAM reads 7.0 -> 5.4 GB, K1 reads 7.4 -> 5.3 GB, step -0.7 ms
-// (profiles/r02/dyn/, dyn2/). Off for K5 / K6, whose long K needs the k-lockstep of the
-// barrier (dynamic: DRAM reads 14.7 -> 22.8 / 13.3 -> 18.2 GB). Not for the NVLS-fused or
-// grouped GEMMs.
+// (profiles/r02/dyn/, dyn2/); on for the Newton-Schulz GEMMs (split-K Gram, X C): 5 steps
+// 38.7-40.0 -> 37.5-38.3 ms (profiles/r02/ns_dyn/). Off for K5 / K6, whose long K needs the
+// k-lockstep of the barrier (dynamic: DRAM reads 14.7 -> 22.8 / 13.3 -> 18.2 GB). Not for the
+// NVLS-fused or grouped GEMMs.
 bool dyn_tiles_for(int kid) {
   static const std::array<int, kKnobKids> env = env_table("RL_DYN_TILES", -1);
   if (kid < 0 || kid >= kKnobKids) return false;
   if (env[kid] >= 0) return env[kid] > 0;
-  return kid == RL_K_FWD_GEMM || kid == RL_K_DZ_GEMM;
+  return kid == RL_K_FWD_GEMM || kid == RL_K_DZ_GEMM || kid == RL_K_NS_GEMM;
 }
 int skew() {
   static const int v = [] {
