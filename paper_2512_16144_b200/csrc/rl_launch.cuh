@@ -133,10 +133,9 @@ bool wide_for(int kid) {
   if (env[kid] >= 0) return env[kid] != 0;
   return kid == RL_K_FWD_GEMM || kid == RL_K_DH_GEMM || kid == RL_K_DW_GEMM || kid == RL_K_NS_GEMM;
 }
-// Serpentine K order (EpiParams::k_serpentine): a CTA's odd-numbered tiles walk their
-// k-blocks backwards. All CTAs are at the same tile number at the same time (the soft
-// k-barrier), so a wave starts on the operand rows the previous wave read last, which are
-// still in L2: the dW GEMM re-reads hidden [T, H] once per wave (~64 waves at GLM-16k).
+// Serpentine K order (EpiParams::k_serpentine): the tiles of odd waves (tile / pairs odd)
+// walk their k-blocks backwards. The CTAs of a wave run in k-lockstep (the soft k-barrier),
+// so a wave starts on the operand rows the previous wave read last, which are still in L2: the dW GEMM re-reads hidden [T, H] once per wave (~64 waves at GLM-16k).
 // RL_SERPENTINE[_<K>] = 0/1; default on for K6 (DW) and the Newton-Schulz GEMMs (the Gram
 // re-reads X). Off for K5 (DH): its accumulation order per dH row would then depend on the
 // wave the row lands in, and the sparse backward's dH is bitwise the dense one only while
