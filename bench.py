@@ -670,6 +670,8 @@ def main_ours(args):
         ideal = sms * 8192.0 * float(clocks["sm_mhz"]) * 1e6 / 1e12
         roof["tensor_ideal_at_sm_clock"] = ideal
         roof["frac_vs_ideal_at_sm_clock"] = roof["achieved"] / ideal
+        roof["ideal_note"] = (f"{sms} SMs x 8192 FLOP/clk at the step's median nvidia-smi SM clock (a few samples); "
+                              "the clock inside each kernel differs, ncu's cycle counts are the per-kernel figure")
     if r.rank == 0:
         out = {"metric": METRIC, "value": r.value, "unit": "tokens/s", "n_gpus": r.world, "steps": args.steps,
                "warmup": args.warmup, "ms_per_step": r.ms_max, "higher_is_better": True,
