@@ -492,7 +492,10 @@ def _kernel_report(r, args):
     hbm_peak = float(peaks.get("hbm_gbs", 6459.3))
     n_tiles = -(-V_local // 256)
     hbm_bytes = {"K2_merge": 16.0 * n_tiles * T + 12.0 * T,
-                 "compact": (8.0 * bwd_rows * H + 4.0 * T) if not dense else 0.0}
+                 "compact": (8.0 * bwd_rows * H + 4.0 * T) if not dense else 0.0,
+                 # K4 from K1's probability cache: fp16 p~ read + bf16 dU written per element,
+                 # one fp32 m per 32 columns
+                 "K4_dz_from_cache": (4.0 + 4.0 / 32) * bwd_rows * V_local}
     for k, v in kern.items():
         if k in flops:
             v["tflops"] = flops[k] / (v["avg_ms"] / 1e3) / 1e12
@@ -525,7 +528,8 @@ def _kernel_report(r, args):
             "step_frac_8HV_vs_burst": rate(step_flops) / float(peaks.get("bf16_tflops", peak)),
             "step_frac_6HV": rate(0.75 * step_flops) / peak,
             "bwd_rows": bwd_rows,
-            "step_frac_executed": rate(sum(step_kflops.values())) / peak}
+            # the GEMM FLOPs this step ran (K4 from K1's probability cache runs no GEMM)
+            "step_frac_executed": rate(sum(f for k, f in step_kflops.items() if k in per)) / peak}
     return kern, roof
 
 
@@ -629,7 +633,9 @@ def _config(r, args):
                                       if args.targets == "sampled" else " ids"),
            "kept_row_frac": r.kept_rows / T if T else 0.0,
            "delta_sigma": r.wl_rank.delta_sigma,
-           "backward": "dense" if args.dense_backward else "sparse (rows with coef != 0)",
+           "backward": ("dense" if args.dense_backward else "sparse (rows with coef != 0)") +
+                       ("; K4 from K1's probability cache" if any(k == "K4_dz_from_cache" for k, _ in r.prof)
+                        else "; K4 recomputes the logits"),
            "collectives": ([] if world == 1 else
                            (["all_gather partials (NCCL)", "dH fp32 all-reduce " +
                              ("fused in K5 epilogue (NVLS multimem)" if nv else "(NCCL)")]

@@ -446,7 +446,8 @@ typedef enum rl_kernel_id {
   RL_K_NS_GEMM = 9,    /* Newton-Schulz / Muon GEMMs (tcgen05)   */
   RL_K_NS_AUX = 10,    /* Newton-Schulz / Muon SIMT kernels      */
   RL_K_GROUPED_GEMM = 11, /* MoE grouped GEMM (tcgen05)          */
-  RL_K_COMPACT = 12    /* sparse-backward compaction / gather / scatter */
+  RL_K_COMPACT = 12,   /* sparse-backward compaction / gather / scatter */
+  RL_K_DZ_CACHE = 13   /* K4 S4 dU from K1's probability cache (elementwise, HBM-bound) */
 } rl_kernel_id;
 
 typedef struct rl_kernel_time {

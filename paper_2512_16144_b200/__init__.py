@@ -86,7 +86,7 @@ class rl_kernel_time(ctypes.Structure):
 
 KERNEL_NAMES = {0: "K0_group_adv", 1: "K1_fwd_gemm_lse", 2: "K2_merge", 3: "K3_loss_coef", 4: "K3b_finalize",
                 5: "K4_bwd_dz_gemm", 6: "K5_dh_gemm", 7: "K6_dw_gemm", 8: "memset", 9: "NS_gemm", 10: "NS_aux",
-                11: "grouped_gemm", 12: "compact"}
+                11: "grouped_gemm", 12: "compact", 13: "K4_dz_from_cache"}
 
 REPORT_BYTES = ctypes.sizeof(rl_loss_report)
 assert REPORT_BYTES == 48

@@ -334,17 +334,19 @@ static rl_status step_impl(const rl_lm_shape* shape, const rl_loss_params* param
       if (shape->inv_temperature_rows) sub.inv_temperature_rows = shape->inv_temperature_rows + r0;
       RL_CUDA(cudaStreamWaitEvent(st, slab_events[j], 0));
       RL_TRY(forward_impl(&sub, hidden + r0 * shape->H, w_vocab, targets + r0, out->logprob + r0,
-                          out->entropy ? out->entropy + r0 : nullptr, lse + r0, nullptr, ws, L, sms, st));
+                          out->entropy ? out->entropy + r0 : nullptr, lse + r0, nullptr, ws, L, sms, st, r0,
+                          shape->T));
     }
   } else {
-    RL_TRY(forward_impl(shape, hidden, w_vocab, targets, out->logprob, out->entropy, lse, nullptr, ws, L, sms, st));
+    RL_TRY(forward_impl(shape, hidden, w_vocab, targets, out->logprob, out->entropy, lse, nullptr, ws, L, sms, st, 0,
+                        shape->T));
   }
   RL_TRY(loss_impl(params, shape->T, shape->V_global, out->logprob, infer_logprobs, targets, rollout_adv,
                    rollout_offsets, loss_mask, coef, out->token_keep, out->rollout_guarded, out->report,
                    reinterpret_cast<rl::RolloutPartial*>(ws + L.rp), st));
   RL_TRY(bwd_impl(shape, hidden, w_vocab, targets, lse, coef, out->d_hidden, out->d_hidden_f32, out->d_w_vocab,
                   out->accumulate_dw, ws, L, sms, st, RL_BWD_ALL | (out->dense_backward ? RL_BWD_DENSE : 0),
-                  out->d_w_vocab_nvls, nullptr));
+                  out->d_w_vocab_nvls, nullptr, L.pcache));
   return RL_OK;
 }
 

@@ -168,6 +168,13 @@ struct EpiParams {
   const int32_t* row_map;
   int* tile_ctr;
   int dyn_tiles;
+  // EPI_LSE probability cache (K4 from the cache instead of the recompute GEMM): for every
+  // 32-column chunk, p_out[(p_row0 + row) * p_ld + col] = fp16(2^(z sl2 - m)) with m the row's
+  // running max after the chunk (log2 units, >= every value of the chunk), and
+  // p_m[(col / 32) * p_rows + p_row0 + row] = m. nullptr = off.
+  uint16_t* p_out;
+  float* p_m;
+  int64_t p_ld, p_row0, p_rows;
 };
 
 __device__ __forceinline__ void red_release_add(uint32_t* p, uint32_t v) {
@@ -826,7 +833,7 @@ __global__ void __launch_bounds__(kernel_threads(MODE, EW), 1)
           constexpr int CPW = (BN / 32) / (EW / 4);  // 32-column chunks per warp
           const int cbeg = cgrp * CPW;
           // one 32-column chunk of scaled logits into the online (m, s, u) state and z_target
-          auto lse_chunk = [&](int c, const uint32_t (&r)[32]) {
+          auto lse_chunk = [&](int c, uint32_t (&r)[32]) {
             if (c * 32 >= nvalid) return;  // columns past V (ragged last tile)
 #ifdef RL_AB_K1_NOMATH
             // A/B measurement only: read the accumulator, skip the softmax arithmetic
@@ -851,12 +858,35 @@ __global__ void __launch_bounds__(kernel_threads(MODE, EW), 1)
               trun = sc * fmaf(srun, mrun - mn, trun);
               srun *= sc;
               mrun = mn;
+              if (ep.p_out == nullptr) {
   #pragma unroll
-              for (int j = 0; j < 32; ++j) {
-                const float d = fmaf(__uint_as_float(r[j]), sl2, -mn);
-                const float e = ex2f(d);
-                srun += e;
-                trun = fmaf(e, d, trun);
+                for (int j = 0; j < 32; ++j) {
+                  const float d = fmaf(__uint_as_float(r[j]), sl2, -mn);
+                  const float e = ex2f(d);
+                  srun += e;
+                  trun = fmaf(e, d, trun);
+                }
+                return;
+              }
+              // probability cache: the same exponentials, packed to fp16 pairs in place (r[j/2]
+              // is rewritten only after r[j], r[j+1] are consumed) and stored with the chunk's m
+  #pragma unroll
+              for (int j = 0; j < 32; j += 2) {
+                const float d0 = fmaf(__uint_as_float(r[j]), sl2, -mn);
+                const float d1 = fmaf(__uint_as_float(r[j + 1]), sl2, -mn);
+                const float e0 = ex2f(d0), e1 = ex2f(d1);
+                srun += e0;
+                trun = fmaf(e0, d0, trun);
+                srun += e1;
+                trun = fmaf(e1, d1, trun);
+                r[j / 2] = pack_f16x2(e0, e1);
+              }
+              if (row_ok) {
+                const int64_t col = static_cast<int64_t>(n0) + c * 32;
+                uint4* dst = reinterpret_cast<uint4*>(ep.p_out + (ep.p_row0 + row) * ep.p_ld + col);
+  #pragma unroll
+                for (int k = 0; k < 4; ++k) dst[k] = make_uint4(r[4 * k], r[4 * k + 1], r[4 * k + 2], r[4 * k + 3]);
+                ep.p_m[(col >> 5) * ep.p_rows + ep.p_row0 + row] = mn;
               }
               return;
             }
@@ -878,6 +908,16 @@ __global__ void __launch_bounds__(kernel_threads(MODE, EW), 1)
               const float e = ex2f(d);
               srun += e;
               trun = fmaf(e, d, trun);
+              u[j] = e;
+            }
+            if (ep.p_out != nullptr && row_ok) {  // probability cache: the valid columns only
+              const int64_t col = static_cast<int64_t>(n0) + c * 32;
+              uint16_t* dst = ep.p_out + (ep.p_row0 + row) * ep.p_ld + col;
+              const int nv = nvalid - c * 32;
+  #pragma unroll
+              for (int j = 0; j < 32; ++j)
+                if (j < nv) dst[j] = f16_bits(u[j]);
+              ep.p_m[(col >> 5) * ep.p_rows + ep.p_row0 + row] = mn;
             }
           };
           if constexpr (EW >= 8 && NB == 2 && CPW == 4) {

@@ -731,4 +731,71 @@ __global__ void split_sum_kernel(const float* __restrict__ part, int S, int64_t 
   }
 }
 
+// K4 from the probability cache (S4 without the recompute GEMM; EpiParams::p_out): for
+// row i < n (n = *cnt when given) and column v < V,
+//   dU[i, v] = bf16(g_i 2^(m[t, v/32] - lse_i log2 e) p~[t, v] - [v == y_i] g_i),  g_i = coef_i invT_i,
+// the same value K4 computes as g_i 2^(z sl2 - lse_i log2 e) - [v == y_i] g_i, with t = row_map[i]
+// (compacted rows) or row0 + i; coef / lse / targets / invt are indexed by i. Rows n .. up to the
+// next multiple of 256 (at most `rows`) are written as zeros, as K4 does: K6 reads whole 64-row
+// k-blocks past the device row count. HBM-bound: 2 B read + 2 B written per element. One block
+// per row at a time (grid-stride over rows): each thread moves 16-byte vectors 256 apart, so
+// every warp instruction covers 512 contiguous bytes of the row; DZC_UNROLL vectors in flight.
+constexpr int DZC_THREADS = 256, DZC_UNROLL = 4;
+__global__ void __launch_bounds__(DZC_THREADS) dz_from_cache_kernel(
+    const uint16_t* __restrict__ pc, const float* __restrict__ pm, int64_t ld, int64_t p_rows,
+    const int32_t* __restrict__ row_map, int64_t row0, const int* __restrict__ cnt, int64_t rows, int64_t V,
+    const float* __restrict__ coef, const float* __restrict__ lse, const int32_t* __restrict__ targets,
+    int64_t vocab_offset, const float* __restrict__ invt_rows, float inv_temperature, uint16_t* __restrict__ dz) {
+  int64_t n = rows;
+  if (cnt) {
+    const int64_t c = *cnt;
+    n = c < rows ? (c > 0 ? c : 0) : rows;
+  }
+  const int64_t n_pad = (n + 255) / 256 * 256 < rows ? (n + 255) / 256 * 256 : rows;
+  const int nvec = static_cast<int>(V / 8);  // full 8-column vectors per row
+  for (int64_t i = blockIdx.x; i < n_pad; i += gridDim.x) {
+    uint16_t* drow = dz + i * ld;
+    if (i >= n) {  // padding rows of the last 256-row block
+      for (int k = threadIdx.x; k < nvec; k += DZC_THREADS) reinterpret_cast<uint4*>(drow)[k] = make_uint4(0u, 0u, 0u, 0u);
+      for (int64_t v = static_cast<int64_t>(nvec) * 8 + threadIdx.x; v < V; v += DZC_THREADS) drow[v] = 0;
+      continue;
+    }
+    const int64_t t = row_map ? static_cast<int64_t>(row_map[i]) : row0 + i;
+    const float g = coef[i] * (invt_rows ? invt_rows[i] : inv_temperature);
+    const float b2 = lse[i] * 1.4426950408889634f;
+    const int64_t y = static_cast<int64_t>(targets[i]) - vocab_offset;
+    const uint16_t* prow = pc + t * ld;
+    const float* mrow = pm + t;
+    auto one = [&](int k, const uint4 p) {
+      const int64_t v0 = static_cast<int64_t>(k) * 8;
+      const float sc = g * ex2f(mrow[(v0 >> 5) * p_rows] - b2);
+      const uint32_t w[4] = {p.x, p.y, p.z, p.w};
+      uint32_t o[4];
+  #pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        float a = sc * f16_to_f32(static_cast<uint16_t>(w[q] & 0xffffu));
+        float b = sc * f16_to_f32(static_cast<uint16_t>(w[q] >> 16));
+        if (y == v0 + 2 * q) a -= g;
+        if (y == v0 + 2 * q + 1) b -= g;
+        o[q] = pack_bf16x2(a, b);
+      }
+      reinterpret_cast<uint4*>(drow)[k] = make_uint4(o[0], o[1], o[2], o[3]);
+    };
+    int k = threadIdx.x;
+    for (; k + (DZC_UNROLL - 1) * DZC_THREADS < nvec; k += DZC_UNROLL * DZC_THREADS) {
+      uint4 p[DZC_UNROLL];
+  #pragma unroll
+      for (int u = 0; u < DZC_UNROLL; ++u) p[u] = reinterpret_cast<const uint4*>(prow)[k + u * DZC_THREADS];
+  #pragma unroll
+      for (int u = 0; u < DZC_UNROLL; ++u) one(k + u * DZC_THREADS, p[u]);
+    }
+    for (; k < nvec; k += DZC_THREADS) one(k, reinterpret_cast<const uint4*>(prow)[k]);
+    for (int64_t v = static_cast<int64_t>(nvec) * 8 + threadIdx.x; v < V; v += DZC_THREADS) {  // ragged tail
+      float a = g * ex2f(mrow[(v >> 5) * p_rows] - b2) * f16_to_f32(prow[v]);
+      if (y == v) a -= g;
+      drow[v] = static_cast<uint16_t>(pack_bf16x2(a, 0.f) & 0xffffu);
+    }
+  }
+}
+
 }  // namespace rl

@@ -7,9 +7,10 @@ namespace {
 
 // K1 (+ K2): forward over the local shard. If `merged` is non-null, write one
 // merged partial per row; else write logprob/entropy/lse.
+// pc_rows > 0: also fill the probability cache (rows pc_row0 .. of a batch of pc_rows).
 rl_status forward_impl(const rl_lm_shape* s, const uint16_t* hidden, const uint16_t* w, const int32_t* targets,
                        float* logprob, float* entropy, float* lse, float4* merged, uint8_t* ws, const WsLayout& L,
-                       int sms, cudaStream_t st) {
+                       int sms, cudaStream_t st, int64_t pc_row0 = 0, int64_t pc_rows = 0) {
   const int64_t T = s->T;
   if (T == 0) return RL_OK;
   CUtensorMap ta, tb;
@@ -25,6 +26,13 @@ rl_status forward_impl(const rl_lm_shape* s, const uint16_t* hidden, const uint1
   ep.vocab_offset = s->vocab_offset;
   float4* parts = reinterpret_cast<float4*>(ws + L.partials);
   ep.partials = parts;
+  if (pc_rows > 0 && L.pcache) {
+    ep.p_out = reinterpret_cast<uint16_t*>(ws + L.pc);
+    ep.p_m = reinterpret_cast<float*>(ws + L.pm);
+    ep.p_ld = L.ldz;
+    ep.p_row0 = pc_row0;
+    ep.p_rows = pc_rows;
+  }
   g_sync_ctr = reinterpret_cast<uint32_t*>(ws + L.sync);
   RL_TRY((launch_gemm<rl::EPI_LSE, false, false>(RL_K_FWD_GEMM, ta, tb, ta, T, s->V_local, s->H, group_m_for(RL_K_FWD_GEMM, 16), ep, sms, st)));
   const int blocks = static_cast<int>((T + rl::MERGE_ROWS - 1) / rl::MERGE_ROWS);
@@ -184,13 +192,28 @@ rl_status launch_dh(const CUtensorMap& t_dz_k, const CUtensorMap& t_w_mn, int64_
   return RL_OK;
 }
 
+// K4 from the probability cache (forward_impl filled it in the same fused call).
+rl_status launch_dz_from_cache(const rl_lm_shape* s, const uint8_t* ws, const WsLayout& L, const int32_t* row_map,
+                               int64_t row0, const int* cnt, int64_t rows, const float* coef, const float* lse,
+                               const int32_t* targets, const float* invt_rows, uint16_t* dz, int sms,
+                               cudaStream_t st) {
+  {
+    ProfScope ps(RL_K_DZ_CACHE, st);
+    rl::dz_from_cache_kernel<<<8 * sms, rl::DZC_THREADS, 0, st>>>(
+        reinterpret_cast<const uint16_t*>(ws + L.pc), reinterpret_cast<const float*>(ws + L.pm), L.ldz, s->T, row_map,
+        row0, cnt, rows, s->V_local, coef, lse, targets, s->vocab_offset, invt_rows, s->inv_temperature, dz);
+  }
+  RL_CHECK_LAUNCH();
+  return RL_OK;
+}
+
 // Sparse backward: the same K4 -> K6 -> K5 over the rows whose coefficient is
 // non-zero only (their order kept). Row counts live on the device: the GEMMs read
 // them at start (dyn_mode), so nothing synchronises the host.
 rl_status bwd_sparse_impl(const rl_lm_shape* s, const uint16_t* hidden, const uint16_t* w, const int32_t* targets,
                           const float* lse, const float* coef, uint16_t* dh, float* dh32, float* dw,
                           int accumulate_dw, uint8_t* ws, const WsLayout& L, int sms, cudaStream_t st, int phases,
-                          const rl_nvls_reduce* dw_nvls, const rl_nvls_reduce* dh_nvls) {
+                          const rl_nvls_reduce* dw_nvls, const rl_nvls_reduce* dh_nvls, bool from_cache) {
   const int64_t T = s->T, H = s->H, V = s->V_local;
   const int64_t chunk = L.chunk;
   const int n_chunks = static_cast<int>((T + chunk - 1) / chunk);
@@ -238,7 +261,10 @@ rl_status bwd_sparse_impl(const rl_lm_shape* s, const uint16_t* hidden, const ui
     const int* cnt = cc + ch;
     const uint16_t* hc = h_c + c0 * H;
     CUtensorMap t_h_k, t_dz_st, t_dz_k, t_dz_mn, t_h_mn, t_dh;
-    if (phases & RL_BWD_DU) {
+    if ((phases & RL_BWD_DU) && from_cache) {
+      RL_TRY(launch_dz_from_cache(s, ws, L, idx + c0, 0, cnt, rows, coef_c + c0, lse_c + c0, tgt_c + c0,
+                                  s->inv_temperature_rows ? invt_c + c0 : nullptr, dz, sms, st));
+    } else if (phases & RL_BWD_DU) {
       RL_TRY(make_map(&t_h_k, hc, false, H, rows, H, 64, kARows));
       RL_TRY(make_map(&t_dz_st, dz, false, V, rows, L.ldz, 64, 32));
       rl::EpiParams ep = {};
@@ -305,7 +331,8 @@ rl_status bwd_sparse_impl(const rl_lm_shape* s, const uint16_t* hidden, const ui
 rl_status bwd_impl(const rl_lm_shape* s, const uint16_t* hidden, const uint16_t* w, const int32_t* targets,
                    const float* lse, const float* coef, uint16_t* dh, float* dh32, float* dw, int accumulate_dw,
                    uint8_t* ws, const WsLayout& L, int sms, cudaStream_t st, int phases = RL_BWD_ALL,
-                   const rl_nvls_reduce* dw_nvls = nullptr, const rl_nvls_reduce* dh_nvls = nullptr) {
+                   const rl_nvls_reduce* dw_nvls = nullptr, const rl_nvls_reduce* dh_nvls = nullptr,
+                   bool from_cache = false) {
   const int64_t T = s->T, H = s->H, V = s->V_local;
   if (T == 0) {
     if (dw && dw_nvls && (phases & RL_BWD_DW)) {
@@ -324,7 +351,7 @@ rl_status bwd_impl(const rl_lm_shape* s, const uint16_t* hidden, const uint16_t*
   g_sync_ctr = reinterpret_cast<uint32_t*>(ws + L.sync);
   if (!(phases & RL_BWD_DENSE))
     return bwd_sparse_impl(s, hidden, w, targets, lse, coef, dh, dh32, dw, accumulate_dw, ws, L, sms, st, phases,
-                           dw_nvls, dh_nvls);
+                           dw_nvls, dh_nvls, from_cache);
   CUtensorMap t_h_k, t_w_k, t_dz_st, t_dz_k, t_w_mn, t_dh, t_dz_mn, t_h_mn, t_dw;
   RL_TRY(make_map(&t_w_k, w, false, H, V, H, 64, rl::BN / cta_group()));
   RL_TRY(make_map(&t_w_mn, w, false, H, V, H, 64, 64));
@@ -346,7 +373,10 @@ rl_status bwd_impl(const rl_lm_shape* s, const uint16_t* hidden, const uint16_t*
     ep.lse = lse + c0;
     ep.coef = coef + c0;
     ep.invt_rows = s->inv_temperature_rows ? s->inv_temperature_rows + c0 : nullptr;
-    if (phases & RL_BWD_DU)
+    if ((phases & RL_BWD_DU) && from_cache)
+      RL_TRY(launch_dz_from_cache(s, ws, L, nullptr, c0, nullptr, rows, coef + c0, lse + c0, targets + c0,
+                                  ep.invt_rows, dz, sms, st));
+    else if (phases & RL_BWD_DU)
       RL_TRY((launch_gemm<rl::EPI_DZ, false, false>(RL_K_DZ_GEMM, t_h_k, t_w_k, t_dz_st, rows, V, H, group_m_for(RL_K_DZ_GEMM, 16), ep, sms, st)));
     // K6: dW (+)= dU^T h
     if ((phases & RL_BWD_DW) && dw) {

@@ -26,7 +26,22 @@ struct WsLayout {
   size_t dh_split;
   int dh_splits;
   int64_t n_tiles_v, ldz, chunk;
+  // probability cache (fused step only, one dU chunk): K1 writes fp16 2^(z sl2 - m) [T x ldz]
+  // and the per-32-column m [ceil(V/32) x T]; K4 then reads it instead of recomputing z
+  size_t pc, pm;
+  bool pcache;
 };
+
+// RL_P_CACHE = 0/1 (default 1): cache the softmax numerators in K1 so the fused step's K4 is an
+// elementwise pass instead of a second LM-head GEMM. Needs the whole batch in
+// one dU chunk; the workspace grows by T x V x 2 + T x V / 8 bytes.
+bool pcache_enabled() {
+  static const int v = [] {
+    const char* e = getenv("RL_P_CACHE");
+    return e ? atoi(e) : 1;
+  }();
+  return v != 0;
+}
 
 // K5 (dH = dU W, K = V) has only ceil(rows/256) x ceil(H/512) output tiles: with fewer than
 // a B200's 74 CTA pairs the GEMM leaves pairs idle for a whole (long) tile. Split the
@@ -79,6 +94,9 @@ WsLayout ws_layout(const rl_lm_shape* s, int32_t R, int64_t chunk_rows) {
   w.dh_splits = dh_split_factor(w.chunk, s->H, s->V_local);
   w.dh_split = c.take(w.dh_splits > 1 ? static_cast<size_t>(w.dh_splits) * ((w.chunk + 255) / 256 * 256) * s->H * 4
                                       : 0);
+  w.pcache = pcache_enabled() && T > 0 && w.chunk >= T;
+  w.pc = c.take(w.pcache ? static_cast<size_t>(T) * w.ldz * 2 : 0);
+  w.pm = c.take(w.pcache ? static_cast<size_t>((s->V_local + 31) / 32) * T * 4 : 0);
   w.end = align_up(c.off, 1024);
   return w;
 }
