@@ -175,6 +175,7 @@ struct EpiParams {
   uint16_t* p_out;
   float* p_m;
   int64_t p_ld, p_row0, p_rows;
+  int p_evict_first;  // store the cache with an L2 evict-first policy
 };
 
 __device__ __forceinline__ void red_release_add(uint32_t* p, uint32_t v) {
@@ -884,8 +885,14 @@ __global__ void __launch_bounds__(kernel_threads(MODE, EW), 1)
               if (row_ok) {
                 const int64_t col = static_cast<int64_t>(n0) + c * 32;
                 uint4* dst = reinterpret_cast<uint4*>(ep.p_out + (ep.p_row0 + row) * ep.p_ld + col);
+                if (ep.p_evict_first) {
+                  const uint64_t pol = l2_evict_first_policy();
   #pragma unroll
-                for (int k = 0; k < 4; ++k) dst[k] = make_uint4(r[4 * k], r[4 * k + 1], r[4 * k + 2], r[4 * k + 3]);
+                  for (int k = 0; k < 4; ++k) st_global_v4_hint(dst + k, r[4 * k], r[4 * k + 1], r[4 * k + 2], r[4 * k + 3], pol);
+                } else {
+  #pragma unroll
+                  for (int k = 0; k < 4; ++k) dst[k] = make_uint4(r[4 * k], r[4 * k + 1], r[4 * k + 2], r[4 * k + 3]);
+                }
                 ep.p_m[(col >> 5) * ep.p_rows + ep.p_row0 + row] = mn;
               }
               return;

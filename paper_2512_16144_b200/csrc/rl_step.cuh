@@ -32,6 +32,7 @@ rl_status forward_impl(const rl_lm_shape* s, const uint16_t* hidden, const uint1
     ep.p_ld = L.ldz;
     ep.p_row0 = pc_row0;
     ep.p_rows = pc_rows;
+    ep.p_evict_first = pcache_evict_first() ? 1 : 0;
   }
   g_sync_ctr = reinterpret_cast<uint32_t*>(ws + L.sync);
   RL_TRY((launch_gemm<rl::EPI_LSE, false, false>(RL_K_FWD_GEMM, ta, tb, ta, T, s->V_local, s->H, group_m_for(RL_K_FWD_GEMM, 16), ep, sms, st)));

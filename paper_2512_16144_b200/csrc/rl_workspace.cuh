@@ -35,6 +35,14 @@ struct WsLayout {
 // RL_P_CACHE = 0/1 (default 1): cache the softmax numerators in K1 so the fused step's K4 is an
 // elementwise pass instead of a second LM-head GEMM. Needs the whole batch in
 // one dU chunk; the workspace grows by T x V x 2 + T x V / 8 bytes.
+// RL_P_EVICT = 0/1 (default 1): K1 stores the cache with an L2 evict-first policy.
+bool pcache_evict_first() {
+  static const int v = [] {
+    const char* e = getenv("RL_P_EVICT");
+    return e ? atoi(e) : 1;
+  }();
+  return v != 0;
+}
 bool pcache_enabled() {
   static const int v = [] {
     const char* e = getenv("RL_P_CACHE");

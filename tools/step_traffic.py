@@ -1,6 +1,7 @@
 """Run the fused step (rl_policy_loss_fwd_bwd, probability cache on by default) twice at the
 GLM-16k shape on random data, for an ncu pass over its kernels: launches per step are K0, K1,
-K2, K3, K3b, the compaction, K4 (from the cache), K6, K5. usage: python tools/step_traffic.py"""
+K2, K3, K3b, the compaction, K4 (from the cache), K6, K5 (a separate K1 computes the rollout
+log-probs first, so every token is kept). usage: python tools/step_traffic.py"""
 import os
 import sys
 
@@ -17,12 +18,13 @@ w = (torch.randn(V, H, generator=g, device=dev) * (4 / H ** 0.5)).to(torch.bfloa
 tg = torch.randint(0, V, (T,), generator=g, device=dev, dtype=torch.int64).to(torch.int32)
 shape = rl.make_shape(T, H, V)
 params = rl.make_params(R, float(T))
-infer = torch.full((T,), -12.0, device=dev)          # ratios around exp(logp + 12): most tokens kept
+infer = torch.empty(T, device=dev)
 rewards = torch.rand(R, generator=g, device=dev)
 offsets = torch.arange(0, T + 1, T // R, device=dev, dtype=torch.int32)
 mask = torch.ones(T, dtype=torch.uint8, device=dev)
 adv = rl.rl_group_advantages(rewards, G)
 ws = rl.alloc_workspace(rl.rl_workspace_bytes(shape, R, 0), dev)
+rl.rl_logprob_fwd(shape, h, w, tg, infer, workspace=ws)   # the rollout policy = this policy: every ratio 1, all kept
 f32 = dict(dtype=torch.float32, device=dev)
 lp, coef = torch.empty(T, **f32), torch.empty(T, **f32)
 dh = torch.empty(T, H, dtype=torch.bfloat16, device=dev)
