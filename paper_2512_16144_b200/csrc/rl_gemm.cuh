@@ -175,7 +175,9 @@ struct EpiParams {
   uint16_t* p_out;
   float* p_m;
   int64_t p_ld, p_row0, p_rows;
-  int p_evict_first;  // store the cache with an L2 evict-first policy
+  int p_evict_first;  // direct stores of the cache with an L2 evict-first policy
+  int p_tma;          // tmC maps the cache (32 x 32 boxes, 64B swizzle): 8-warp epilogues stage each
+                      // chunk in shared memory and TMA-store it
 };
 
 __device__ __forceinline__ void red_release_add(uint32_t* p, uint32_t v) {
@@ -833,6 +835,26 @@ __global__ void __launch_bounds__(kernel_threads(MODE, EW), 1)
           const float sl2 = ep.invt_rows != nullptr ? it * 1.4426950408889634f : ep.scale_log2;
           constexpr int CPW = (BN / 32) / (EW / 4);  // 32-column chunks per warp
           const int cbeg = cgrp * CPW;
+          // probability cache, 8-warp epilogue: the chunk's 16 packed fp16 pairs of every lane
+          // (32 rows x 64 bytes) go through this warp's 2 KB staging buffer (64B swizzle,
+          // conflict-free) and one TMA store; the global write leaves the drain's critical path
+          [[maybe_unused]] auto p_stage_store = [&](int c, const uint32_t (&pk)[32]) {
+            const uint32_t pbuf = smem_u32(sEpi) + 4096 + (warp - 2) * 2048;
+            if (lane == 0) bulk_wait_read<0>();
+            __syncwarp();
+  #pragma unroll
+            for (int k = 0; k < 4; ++k)
+              st_shared_v4(pbuf + lane * 64 + ((k ^ ((lane >> 1) & 3)) << 4), pk[4 * k], pk[4 * k + 1], pk[4 * k + 2],
+                           pk[4 * k + 3]);
+            fence_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              const int c0 = n0 + c * 32;
+              const int c1 = static_cast<int>(ep.p_row0) + m * TL::TILE_M + rank * 128 + q * 32;
+              tma_store_2d(&tmC, sEpi + (pbuf - smem_u32(sEpi)), c0, c1);
+              bulk_commit();
+            }
+          };
           // one 32-column chunk of scaled logits into the online (m, s, u) state and z_target
           auto lse_chunk = [&](int c, uint32_t (&r)[32]) {
             if (c * 32 >= nvalid) return;  // columns past V (ragged last tile)
@@ -882,6 +904,16 @@ __global__ void __launch_bounds__(kernel_threads(MODE, EW), 1)
                 trun = fmaf(e1, d1, trun);
                 r[j / 2] = pack_f16x2(e0, e1);
               }
+              if constexpr (EW == 8) {
+                if (ep.p_tma) {
+                  p_stage_store(c, r);
+                  if (row_ok) {
+                    const int64_t col = static_cast<int64_t>(n0) + c * 32;
+                    ep.p_m[(col >> 5) * ep.p_rows + ep.p_row0 + row] = mn;
+                  }
+                  return;
+                }
+              }
               if (row_ok) {
                 const int64_t col = static_cast<int64_t>(n0) + c * 32;
                 uint4* dst = reinterpret_cast<uint4*>(ep.p_out + (ep.p_row0 + row) * ep.p_ld + col);
@@ -916,6 +948,19 @@ __global__ void __launch_bounds__(kernel_threads(MODE, EW), 1)
               srun += e;
               trun = fmaf(e, d, trun);
               u[j] = e;
+            }
+            if constexpr (EW == 8) {
+              if (ep.p_out != nullptr && ep.p_tma) {  // TMA clips the columns past V
+                uint32_t pk[32];
+  #pragma unroll
+                for (int j = 0; j < 16; ++j) pk[j] = pack_f16x2(u[2 * j], u[2 * j + 1]);
+                p_stage_store(c, pk);
+                if (row_ok) {
+                  const int64_t col = static_cast<int64_t>(n0) + c * 32;
+                  ep.p_m[(col >> 5) * ep.p_rows + ep.p_row0 + row] = mn;
+                }
+                return;
+              }
             }
             if (ep.p_out != nullptr && row_ok) {  // probability cache: the valid columns only
               const int64_t col = static_cast<int64_t>(n0) + c * 32;

@@ -13,9 +13,10 @@ rl_status forward_impl(const rl_lm_shape* s, const uint16_t* hidden, const uint1
                        int sms, cudaStream_t st, int64_t pc_row0 = 0, int64_t pc_rows = 0) {
   const int64_t T = s->T;
   if (T == 0) return RL_OK;
-  CUtensorMap ta, tb;
+  CUtensorMap ta, tb, tp;
   RL_TRY(make_map(&ta, hidden, false, s->H, T, s->H, 64, kARows));
   RL_TRY(make_map(&tb, w, false, s->H, s->V_local, s->H, 64, rl::BN / cta_group()));
+  tp = ta;
   rl::EpiParams ep = {};
   ep.rows = T;
   ep.cols = s->V_local;
@@ -33,9 +34,14 @@ rl_status forward_impl(const rl_lm_shape* s, const uint16_t* hidden, const uint1
     ep.p_row0 = pc_row0;
     ep.p_rows = pc_rows;
     ep.p_evict_first = pcache_evict_first() ? 1 : 0;
+    // 32 x 32 fp16 boxes (64-byte rows, 64B swizzle) for the TMA stores of the 8-warp epilogue
+    if (pcache_tma()) {
+      RL_TRY(make_map(&tp, ws + L.pc, false, s->V_local, pc_rows, L.ldz, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B));
+      ep.p_tma = 1;
+    }
   }
   g_sync_ctr = reinterpret_cast<uint32_t*>(ws + L.sync);
-  RL_TRY((launch_gemm<rl::EPI_LSE, false, false>(RL_K_FWD_GEMM, ta, tb, ta, T, s->V_local, s->H, group_m_for(RL_K_FWD_GEMM, 16), ep, sms, st)));
+  RL_TRY((launch_gemm<rl::EPI_LSE, false, false>(RL_K_FWD_GEMM, ta, tb, tp, T, s->V_local, s->H, group_m_for(RL_K_FWD_GEMM, 16), ep, sms, st)));
   const int blocks = static_cast<int>((T + rl::MERGE_ROWS - 1) / rl::MERGE_ROWS);
   {
     ProfScope ps(RL_K_MERGE, st);

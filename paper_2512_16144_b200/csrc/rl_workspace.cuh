@@ -35,10 +35,20 @@ struct WsLayout {
 // RL_P_CACHE = 0/1 (default 1): cache the softmax numerators in K1 so the fused step's K4 is an
 // elementwise pass instead of a second LM-head GEMM. Needs the whole batch in
 // one dU chunk; the workspace grows by T x V x 2 + T x V / 8 bytes.
-// RL_P_EVICT = 0/1 (default 1): K1 stores the cache with an L2 evict-first policy.
+// RL_P_EVICT = 0/1 (default 0): K1's direct (non-TMA) cache stores with an L2 evict-first policy;
+// measured neutral (DRAM reads 6.98 vs 6.92 GB, same cycles; profiles/r02/pcache/pevict/).
 bool pcache_evict_first() {
   static const int v = [] {
     const char* e = getenv("RL_P_EVICT");
+    return e ? atoi(e) : 0;
+  }();
+  return v != 0;
+}
+// RL_P_TMA = 0/1 (default 1): the 8-warp K1 epilogue stages each cached chunk in shared memory and
+// TMA-stores it (0: direct 16-byte global stores from the registers).
+bool pcache_tma() {
+  static const int v = [] {
+    const char* e = getenv("RL_P_TMA");
     return e ? atoi(e) : 1;
   }();
   return v != 0;
