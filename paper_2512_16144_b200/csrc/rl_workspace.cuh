@@ -26,15 +26,15 @@ struct WsLayout {
   size_t dh_split;
   int dh_splits;
   int64_t n_tiles_v, ldz, chunk;
-  // probability cache (fused step only, one dU chunk): K1 writes fp16 2^(z sl2 - m) [T x ldz]
+  // probability cache (fused step): K1 writes fp16 2^(z sl2 - m) [T x ldz]
   // and the per-32-column m [ceil(V/32) x T]; K4 then reads it instead of recomputing z
   size_t pc, pm;
   bool pcache;
 };
 
 // RL_P_CACHE = 0/1 (default 1): cache the softmax numerators in K1 so the fused step's K4 is an
-// elementwise pass instead of a second LM-head GEMM. Needs the whole batch in
-// one dU chunk; the workspace grows by T x V x 2 + T x V / 8 bytes.
+// elementwise pass instead of a second LM-head GEMM. The workspace grows by
+// T x V x 2 + T x V / 8 bytes (the whole batch, also when dU is processed in chunks).
 // RL_P_EVICT = 0/1 (default 0): K1's direct (non-TMA) cache stores with an L2 evict-first policy;
 // measured neutral (DRAM reads 6.98 vs 6.92 GB, same cycles; profiles/r02/pcache/pevict/).
 bool pcache_evict_first() {
@@ -112,7 +112,8 @@ WsLayout ws_layout(const rl_lm_shape* s, int32_t R, int64_t chunk_rows) {
   w.dh_splits = dh_split_factor(w.chunk, s->H, s->V_local);
   w.dh_split = c.take(w.dh_splits > 1 ? static_cast<size_t>(w.dh_splits) * ((w.chunk + 255) / 256 * 256) * s->H * 4
                                       : 0);
-  w.pcache = pcache_enabled() && T > 0 && w.chunk >= T;
+  // the cache holds the whole batch (K4 fills each dU chunk from its rows); at most 64 GB
+  w.pcache = pcache_enabled() && T > 0 && static_cast<double>(T) * w.ldz * 2.125 <= 64e9;
   w.pc = c.take(w.pcache ? static_cast<size_t>(T) * w.ldz * 2 : 0);
   w.pm = c.take(w.pcache ? static_cast<size_t>((s->V_local + 31) / 32) * T * 4 : 0);
   w.end = align_up(c.off, 1024);
