@@ -411,7 +411,11 @@ rl_status rl_expert_load(const int32_t* offsets, int32_t n_groups, int64_t rows,
 
 /* ------------------------------------------------------------ utilities */
 /* Workspace needed by rl_logprob_fwd / rl_policy_loss_fwd_bwd / the split
- * phases for this shape. dz_chunk_rows = rows of the bf16 dU buffer (0 = T). */
+ * phases for this shape. dz_chunk_rows = rows of the bf16 dU buffer (0 = T).
+ * Includes the probability cache of rl_policy_loss_fwd_bwd[_hostio] (K1 stores
+ * fp16 softmax numerators and per-32-column maxima, T x V_local x 2.125 bytes,
+ * so that K4 needs no second LM-head GEMM) unless the environment sets
+ * RL_P_CACHE=0 or the cache would exceed 64 GB. */
 size_t rl_workspace_bytes(const rl_lm_shape* shape, int32_t num_rollouts, int64_t dz_chunk_rows);
 size_t rl_workspace_bytes_hostio(const rl_lm_shape* shape, int32_t num_rollouts, int64_t dz_chunk_rows);
 
