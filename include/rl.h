@@ -250,6 +250,14 @@ rl_status rl_policy_loss_fwd_bwd_hostio(const rl_lm_shape* shape, const rl_loss_
 rl_status rl_fwd_partials(const rl_lm_shape* shape, const uint16_t* hidden,
                           const uint16_t* w_vocab, const int32_t* targets, float* partials,
                           void* workspace, size_t workspace_bytes, void* stream);
+/* rl_fwd_partials with flags: RL_FWD_CACHE also stores the probability cache (fp16 softmax
+ * numerators of this shard and per-32-column maxima) into the workspace for a later
+ * rl_bwd_ex(phases | RL_BWD_FROM_CACHE) with the same inputs; the workspace must then be
+ * rl_workspace_bytes(shape, ...) large (RL_ERR_WORKSPACE otherwise). */
+#define RL_FWD_CACHE 1
+rl_status rl_fwd_partials_ex(const rl_lm_shape* shape, const uint16_t* hidden, const uint16_t* w_vocab,
+                             const int32_t* targets, float* partials, int32_t flags, void* workspace,
+                             size_t workspace_bytes, void* stream);
 
 /* S2: merge n_parts partial arrays ([n_parts, T] float4, e.g. all-gathered from
  * every vocab shard, merged in index order) into logprob, entropy, lse ([T]). */
@@ -325,6 +333,10 @@ rl_status rl_bwd(const rl_lm_shape* shape, const uint16_t* hidden, const uint16_
  * RL_BWD_DENSE into `phases` to run over every row (bitwise-reproducible either
  * way; the two differ only in fp32 summation order of dW). */
 #define RL_BWD_DENSE 8
+/* OR into `phases`: K4 reads the probability cache that rl_fwd_partials_ex(RL_FWD_CACHE) wrote into this
+ * workspace for the same shape, hidden, w_vocab and targets, instead of recomputing the logits
+ * (RL_ERR_INVALID_ARGUMENT if the workspace layout has no cache, i.e. RL_P_CACHE=0). */
+#define RL_BWD_FROM_CACHE 16
 rl_status rl_bwd_ex(const rl_lm_shape* shape, const uint16_t* hidden, const uint16_t* w_vocab,
                     const int32_t* targets, const float* lse, const float* coef, uint16_t* d_hidden,
                     float* d_hidden_f32, float* d_w_vocab, int32_t accumulate_dw, int64_t dz_chunk_rows,

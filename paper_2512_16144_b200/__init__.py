@@ -103,6 +103,8 @@ _SIGS = {
                                                      ctypes.POINTER(rl_loss_outputs),
                                                      ctypes.POINTER(rl_loss_report), _P, ctypes.c_size_t, _P]),
     "rl_fwd_partials": (ctypes.c_int, [ctypes.POINTER(rl_lm_shape), _P, _P, _P, _P, _P, ctypes.c_size_t, _P]),
+    "rl_fwd_partials_ex": (ctypes.c_int, [ctypes.POINTER(rl_lm_shape), _P, _P, _P, _P, ctypes.c_int32, _P,
+                                          ctypes.c_size_t, _P]),
     "rl_merge_partials": (ctypes.c_int, [_P, ctypes.c_int32, ctypes.c_int64, _P, _P, _P, _P]),
     "rl_loss_coef": (ctypes.c_int, [ctypes.POINTER(rl_loss_params), ctypes.c_int64, ctypes.c_int64, _P, _P, _P, _P,
                                     _P, _P, _P, _P, _P, _P, _P, ctypes.c_size_t, _P]),
@@ -312,6 +314,16 @@ def rl_fwd_partials(shape: rl_lm_shape, hidden, w_vocab, targets, partials, work
                                           _ptr(ws), ws.numel(), _stream(stream)))
 
 
+def rl_fwd_partials_ex(shape: rl_lm_shape, hidden, w_vocab, targets, partials, flags: int = 0, workspace=None,
+                       stream=None):
+    """rl_fwd_partials; flags = RL_FWD_CACHE also fills the probability cache in `workspace` for a
+    later rl_bwd_ex(phases | RL_BWD_FROM_CACHE) on the same inputs and workspace."""
+    ws = workspace if workspace is not None else alloc_workspace(rl_workspace_bytes(shape), hidden.device)
+    _check(load_library().rl_fwd_partials_ex(ctypes.byref(shape), _ptr(_bf16(hidden, "hidden")),
+                                             _ptr(_bf16(w_vocab, "w_vocab")), _ptr(targets), _ptr(partials),
+                                             int(flags), _ptr(ws), ws.numel(), _stream(stream)))
+
+
 def rl_merge_partials(partials, n_parts: int, T: int, logprob, entropy=None, lse=None, stream=None):
     """S2: merge [n_parts, T, 4] partials (index order) into logprob / entropy / lse."""
     _check(load_library().rl_merge_partials(_ptr(partials), int(n_parts), int(T), _ptr(logprob), _ptr(entropy),
@@ -380,7 +392,8 @@ def rl_profile_read(cap: int = 4096) -> list:
     return [(KERNEL_NAMES.get(buf[i].kernel, str(buf[i].kernel)), float(buf[i].ms)) for i in range(min(n, cap))]
 
 
-RL_BWD_DU, RL_BWD_DW, RL_BWD_DH, RL_BWD_ALL, RL_BWD_DENSE = 1, 2, 4, 7, 8
+RL_BWD_DU, RL_BWD_DW, RL_BWD_DH, RL_BWD_ALL, RL_BWD_DENSE, RL_BWD_FROM_CACHE = 1, 2, 4, 7, 8, 16
+RL_FWD_CACHE = 1
 
 
 def rl_bwd_ex(shape: rl_lm_shape, hidden, w_vocab, targets, lse, coef, d_hidden=None, d_hidden_f32=None,

@@ -141,10 +141,11 @@ rl_status rl_logprob_fwd(const rl_lm_shape* shape, const uint16_t* hidden, const
                       static_cast<uint8_t*>(workspace), L, d.sms, static_cast<cudaStream_t>(stream));
 }
 
-rl_status rl_fwd_partials(const rl_lm_shape* shape, const uint16_t* hidden, const uint16_t* w_vocab,
-                          const int32_t* targets, float* partials, void* workspace, size_t workspace_bytes,
-                          void* stream) {
+rl_status rl_fwd_partials_ex(const rl_lm_shape* shape, const uint16_t* hidden, const uint16_t* w_vocab,
+                             const int32_t* targets, float* partials, int32_t flags, void* workspace,
+                             size_t workspace_bytes, void* stream) {
   g_launches = 0;
+  if ((flags & ~RL_FWD_CACHE) != 0) return fail(RL_ERR_INVALID_ARGUMENT, "unknown rl_fwd_partials_ex flags %d", flags);
   RL_TRY(check_shape(shape));
   if (shape->T > 0) {
     RL_NONNULL(hidden);
@@ -155,12 +156,22 @@ rl_status rl_fwd_partials(const rl_lm_shape* shape, const uint16_t* hidden, cons
       return fail(RL_ERR_ALIGNMENT, "hidden, w_vocab, partials and workspace must be 16-byte aligned");
   }
   const WsLayout L = ws_layout(shape, 1, 0);
-  if (shape->T > 0 && (!workspace || workspace_bytes < L.dz))
-    return fail(RL_ERR_WORKSPACE, "workspace needs %zu bytes, got %zu", L.dz, workspace_bytes);
+  const bool cache = (flags & RL_FWD_CACHE) != 0;
+  if (cache && !L.pcache) return fail(RL_ERR_INVALID_ARGUMENT, "RL_FWD_CACHE: no probability cache (RL_P_CACHE=0)");
+  const size_t need = cache ? L.end : L.dz;
+  if (shape->T > 0 && (!workspace || workspace_bytes < need))
+    return fail(RL_ERR_WORKSPACE, "workspace needs %zu bytes, got %zu", need, workspace_bytes);
   DevInfo d;
   RL_TRY(device_info(d));
   return forward_impl(shape, hidden, w_vocab, targets, nullptr, nullptr, nullptr, reinterpret_cast<float4*>(partials),
-                      static_cast<uint8_t*>(workspace), L, d.sms, static_cast<cudaStream_t>(stream));
+                      static_cast<uint8_t*>(workspace), L, d.sms, static_cast<cudaStream_t>(stream), 0,
+                      cache ? shape->T : 0);
+}
+
+rl_status rl_fwd_partials(const rl_lm_shape* shape, const uint16_t* hidden, const uint16_t* w_vocab,
+                          const int32_t* targets, float* partials, void* workspace, size_t workspace_bytes,
+                          void* stream) {
+  return rl_fwd_partials_ex(shape, hidden, w_vocab, targets, partials, 0, workspace, workspace_bytes, stream);
 }
 
 rl_status rl_merge_partials(const float* partials, int32_t n_parts, int64_t T, float* logprob, float* entropy,
@@ -285,7 +296,7 @@ rl_status rl_bwd_ex(const rl_lm_shape* shape, const uint16_t* hidden, const uint
   RL_TRY(check_nvls(dh_nvls, "dh_nvls"));
   if (dw_nvls && !d_w_vocab) return fail(RL_ERR_INVALID_ARGUMENT, "dw_nvls reduces d_w_vocab");
   if (dh_nvls && !d_hidden_f32) return fail(RL_ERR_INVALID_ARGUMENT, "dh_nvls reduces d_hidden_f32");
-  if ((phases & RL_BWD_ALL) == 0 || (phases & ~(RL_BWD_ALL | RL_BWD_DENSE)) != 0)
+  if ((phases & RL_BWD_ALL) == 0 || (phases & ~(RL_BWD_ALL | RL_BWD_DENSE | RL_BWD_FROM_CACHE)) != 0)
     return fail(RL_ERR_INVALID_ARGUMENT, "phases must be a non-empty RL_BWD_* mask");
   if (max_sms < 0) return fail(RL_ERR_INVALID_ARGUMENT, "max_sms must be >= 0");
   RL_TRY(check_shape(shape));
@@ -303,6 +314,8 @@ rl_status rl_bwd_ex(const rl_lm_shape* shape, const uint16_t* hidden, const uint
   const WsLayout L = ws_layout(shape, 1, dz_chunk_rows);
   if (shape->T > 0 && (!workspace || workspace_bytes < L.end))
     return fail(RL_ERR_WORKSPACE, "workspace needs %zu bytes, got %zu", L.end, workspace_bytes);
+  if ((phases & RL_BWD_FROM_CACHE) && !L.pcache)
+    return fail(RL_ERR_INVALID_ARGUMENT, "RL_BWD_FROM_CACHE: no probability cache (RL_P_CACHE=0)");
   if ((phases & RL_BWD_ALL) != RL_BWD_ALL && L.chunk < shape->T)
     return fail(RL_ERR_INVALID_ARGUMENT, "partial backward phases need one dU chunk (dz_chunk_rows = 0 or >= T)");
   if ((dw_nvls || dh_nvls) && shape->T > 0 && (shape->T + L.chunk - 1) / L.chunk > kNvlsChunkEpochs)
@@ -312,8 +325,8 @@ rl_status rl_bwd_ex(const rl_lm_shape* shape, const uint16_t* hidden, const uint
   int sms = d.sms;
   if (max_sms > 0 && max_sms < sms) sms = max_sms < 2 ? 2 : max_sms;
   return bwd_impl(shape, hidden, w_vocab, targets, lse, coef, d_hidden, d_hidden_f32, d_w_vocab, accumulate_dw,
-                  static_cast<uint8_t*>(workspace), L, sms, static_cast<cudaStream_t>(stream), phases, dw_nvls,
-                  dh_nvls);
+                  static_cast<uint8_t*>(workspace), L, sms, static_cast<cudaStream_t>(stream),
+                  phases & ~RL_BWD_FROM_CACHE, dw_nvls, dh_nvls, (phases & RL_BWD_FROM_CACHE) != 0);
 }
 
 // The whole step. With slab_events, the forward runs slab by slab (slab_rows

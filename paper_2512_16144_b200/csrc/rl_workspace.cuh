@@ -93,6 +93,12 @@ WsLayout ws_layout(const rl_lm_shape* s, int32_t R, int64_t chunk_rows) {
   w.n_tiles_v = n_vocab_tiles(s);
   w.ldz = (s->V_local + 7) / 8 * 8;
   w.chunk = (chunk_rows <= 0 || chunk_rows > T) ? T : chunk_rows;
+  // the probability cache first: its offset depends on T and V only, so a split-phase forward
+  // (rl_fwd_partials_ex) and backward (rl_bwd_ex) with different dz_chunk_rows agree on it
+  // the cache holds the whole batch (K4 fills each dU chunk from its rows); at most 64 GB
+  w.pcache = pcache_enabled() && T > 0 && static_cast<double>(T) * w.ldz * 2.125 <= 64e9;
+  w.pc = c.take(w.pcache ? static_cast<size_t>(T) * w.ldz * 2 : 0);
+  w.pm = c.take(w.pcache ? static_cast<size_t>((s->V_local + 31) / 32) * T * 4 : 0);
   w.partials = c.take(static_cast<size_t>(w.n_tiles_v) * T * 16);
   w.lse = c.take(static_cast<size_t>(T) * 4);
   w.coef = c.take(static_cast<size_t>(T) * 4);
@@ -112,10 +118,6 @@ WsLayout ws_layout(const rl_lm_shape* s, int32_t R, int64_t chunk_rows) {
   w.dh_splits = dh_split_factor(w.chunk, s->H, s->V_local);
   w.dh_split = c.take(w.dh_splits > 1 ? static_cast<size_t>(w.dh_splits) * ((w.chunk + 255) / 256 * 256) * s->H * 4
                                       : 0);
-  // the cache holds the whole batch (K4 fills each dU chunk from its rows); at most 64 GB
-  w.pcache = pcache_enabled() && T > 0 && static_cast<double>(T) * w.ldz * 2.125 <= 64e9;
-  w.pc = c.take(w.pcache ? static_cast<size_t>(T) * w.ldz * 2 : 0);
-  w.pm = c.take(w.pcache ? static_cast<size_t>((s->V_local + 31) / 32) * T * 4 : 0);
   w.end = align_up(c.off, 1024);
   return w;
 }

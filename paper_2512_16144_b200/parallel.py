@@ -25,7 +25,8 @@ import torch
 import torch.distributed as dist
 
 from . import (RL_BWD_ALL, RL_BWD_DENSE, RL_BWD_DH, RL_BWD_DU, RL_BWD_DW, alloc_workspace, make_params,
-               make_shape, rl_bwd_ex, rl_fwd_partials, rl_group_advantages, rl_last_launch_count, rl_logprob_fwd, rl_loss_coef,
+               make_shape, rl_bwd_ex, rl_fwd_partials, rl_fwd_partials_ex, RL_FWD_CACHE, RL_BWD_FROM_CACHE,
+               rl_group_advantages, rl_last_launch_count, rl_logprob_fwd, rl_loss_coef,
                rl_loss_coef_ex, rl_rollout_stats,
                rl_merge_partials, rl_ns_shard_apply, rl_ns_shard_gram, rl_ns_shard_sumsq,
                rl_nvls_flag_count, rl_nvls_reduce, rl_nvls_shard_rows, rl_policy_loss_fwd_bwd, rl_workspace_bytes)
@@ -76,6 +77,8 @@ class LibrlPhases:
     `dense_backward` runs the backward GEMMs over all rows (RL_BWD_DENSE) instead of
     the rows with a non-zero coefficient."""
 
+    supports_cache = True   # fwd_partials(cache=True) + bwd(from_cache=True): K4 from K1's probability cache
+
     def __init__(self, dense_backward: bool = False):
         self.launches = 0
         self.dense = RL_BWD_DENSE if dense_backward else 0
@@ -100,8 +103,11 @@ class LibrlPhases:
         rl_ns_shard_apply(j, steps, gram, M_local, N, out, workspace)
         self._count()
 
-    def fwd_partials(self, shape, hidden, w_shard, targets, partials, workspace=None):
-        rl_fwd_partials(shape, hidden, w_shard, targets, partials, workspace=workspace)
+    def fwd_partials(self, shape, hidden, w_shard, targets, partials, workspace=None, cache=False):
+        if cache:   # also fill the probability cache for bwd(..., from_cache=True) on the same workspace
+            rl_fwd_partials_ex(shape, hidden, w_shard, targets, partials, RL_FWD_CACHE, workspace=workspace)
+        else:
+            rl_fwd_partials(shape, hidden, w_shard, targets, partials, workspace=workspace)
         self._count()
 
     def merge_partials(self, parts, n_parts, T, logprob, entropy, lse):
@@ -127,9 +133,10 @@ class LibrlPhases:
         self._count()
 
     def bwd(self, shape, hidden, w_shard, targets, lse, coef, d_hidden_f32, d_w_vocab, dz_chunk_rows=0,
-            workspace=None, dh_nvls=None):
+            workspace=None, dh_nvls=None, from_cache=False):
         rl_bwd_ex(shape, hidden, w_shard, targets, lse, coef, d_hidden_f32=d_hidden_f32, d_w_vocab=d_w_vocab,
-                  dz_chunk_rows=dz_chunk_rows, phases=RL_BWD_ALL | self.dense, dh_nvls=dh_nvls,
+                  dz_chunk_rows=dz_chunk_rows,
+                  phases=RL_BWD_ALL | self.dense | (RL_BWD_FROM_CACHE if from_cache else 0), dh_nvls=dh_nvls,
                   workspace=workspace)
         self._count()
 
@@ -152,6 +159,13 @@ class LibrlPhases:
                                d_w_vocab_nvls=d_w_vocab_nvls, dz_chunk_rows=dz_chunk_rows,
                                dense_backward=bool(self.dense), workspace=workspace, accumulate_dw=accumulate_dw)
         self._count()
+
+
+def prob_cache_enabled() -> bool:
+    """librl's RL_P_CACHE knob (default on): the split phases use the cache only when the
+    workspace layout has one."""
+    import os
+    return os.environ.get("RL_P_CACHE", "1") != "0"
 
 
 def _all_gather_rows(parts: torch.Tensor, mine: torch.Tensor, group=None):
@@ -210,18 +224,25 @@ class VocabParallelPolicyLoss:
     def step(self, hidden, w_shard, targets, infer, rewards, offsets, loss_mask, d_w_vocab):
         ph = self.ph
         ph.group_advantages(rewards, self.G, self.adv)
-        ph.fwd_partials(self.shape, hidden, w_shard, targets, self.parts[self.rank], workspace=self.ws)
+        # the probability cache lives in this engine's workspace from the forward to the backward
+        cache = self.ws is not None and getattr(ph, "supports_cache", False) and prob_cache_enabled()
+        if cache:
+            ph.fwd_partials(self.shape, hidden, w_shard, targets, self.parts[self.rank], workspace=self.ws,
+                            cache=True)
+        else:
+            ph.fwd_partials(self.shape, hidden, w_shard, targets, self.parts[self.rank], workspace=self.ws)
         _all_gather_rows(self.parts, self.parts[self.rank], self.group)                 # exchange 1
         ph.merge_partials(self.parts, self.world, self.T, self.logprob, self.entropy, self.lse)
         ph.loss_coef(self.params, self.T, self.V_global, self.logprob, infer, targets, self.adv, offsets,
                      loss_mask, self.coef, self.keep, self.guarded, self.report, workspace=self.loss_ws)
+        kw = {"from_cache": True} if cache else {}
         if self.nvls is not None:
             ph.bwd(self.shape, hidden, w_shard, targets, self.lse, self.coef, self.d_hidden, d_w_vocab,
-                   dz_chunk_rows=self.chunk, workspace=self.ws, dh_nvls=self.nvls.descriptor())
+                   dz_chunk_rows=self.chunk, workspace=self.ws, dh_nvls=self.nvls.descriptor(), **kw)
             self.nvls.barrier()                                   # exchange 2, fused into K5's epilogue
             return self.d_hidden
         ph.bwd(self.shape, hidden, w_shard, targets, self.lse, self.coef, self.d_hidden, d_w_vocab,
-               dz_chunk_rows=self.chunk, workspace=self.ws)
+               dz_chunk_rows=self.chunk, workspace=self.ws, **kw)
         dist.all_reduce(self.d_hidden, group=self.group)                                  # exchange 2
         return self.d_hidden
 
