@@ -252,8 +252,8 @@ rl_status rl_fwd_partials(const rl_lm_shape* shape, const uint16_t* hidden,
                           void* workspace, size_t workspace_bytes, void* stream);
 /* rl_fwd_partials with flags: RL_FWD_CACHE also stores the probability cache (fp16 softmax
  * numerators of this shard and per-32-column maxima) into the workspace for a later
- * rl_bwd_ex(phases | RL_BWD_FROM_CACHE) with the same inputs; the workspace must then be
- * rl_workspace_bytes(shape, ...) large (RL_ERR_WORKSPACE otherwise). */
+ * rl_bwd_ex(phases | RL_BWD_FROM_CACHE) with the same inputs and workspace (a workspace of
+ * rl_workspace_bytes(shape, ...) holds it; RL_ERR_WORKSPACE if it is too small). */
 #define RL_FWD_CACHE 1
 rl_status rl_fwd_partials_ex(const rl_lm_shape* shape, const uint16_t* hidden, const uint16_t* w_vocab,
                              const int32_t* targets, float* partials, int32_t flags, void* workspace,

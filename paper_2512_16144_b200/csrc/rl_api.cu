@@ -158,7 +158,7 @@ rl_status rl_fwd_partials_ex(const rl_lm_shape* shape, const uint16_t* hidden, c
   const WsLayout L = ws_layout(shape, 1, 0);
   const bool cache = (flags & RL_FWD_CACHE) != 0;
   if (cache && !L.pcache) return fail(RL_ERR_INVALID_ARGUMENT, "RL_FWD_CACHE: no probability cache (RL_P_CACHE=0)");
-  const size_t need = cache ? L.end : L.dz;
+  const size_t need = L.dz;  // the forward's regions (the cache first, then the partials) end where dU begins
   if (shape->T > 0 && (!workspace || workspace_bytes < need))
     return fail(RL_ERR_WORKSPACE, "workspace needs %zu bytes, got %zu", need, workspace_bytes);
   DevInfo d;
