@@ -206,7 +206,12 @@ rl_status launch_dz_from_cache(const rl_lm_shape* s, const uint8_t* ws, const Ws
                                cudaStream_t st) {
   {
     ProfScope ps(RL_K_DZ_CACHE, st);
-    rl::dz_from_cache_kernel<<<8 * sms, rl::DZC_THREADS, 0, st>>>(
+    static const int bps = [] {  // RL_DZC_BLOCKS_PER_SM: blocks per SM of the grid-stride row loop (A/B)
+      const char* e = getenv("RL_DZC_BLOCKS_PER_SM");
+      const int v = e ? atoi(e) : 8;
+      return v > 0 ? v : 8;
+    }();
+    rl::dz_from_cache_kernel<<<bps * sms, rl::DZC_THREADS, 0, st>>>(
         reinterpret_cast<const uint16_t*>(ws + L.pc), reinterpret_cast<const float*>(ws + L.pm), L.ldz, s->T, row_map,
         row0, cnt, rows, s->V_local, coef, lse, targets, s->vocab_offset, invt_rows, s->inv_temperature, dz);
   }
